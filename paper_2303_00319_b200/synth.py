@@ -1,0 +1,146 @@
+"""Seeded synthetic image pairs standing in for the paper's datasets.
+
+The LNIFT SAR-optical / infrared-optical sets the paper measures on are not
+available here, and the reference's own `synthetic.py` does
+not contain the BASELINE.json generator, so this module is a
+builder-written restatement of the BASELINE.json config text:
+
+* image 1: anisotropic Gaussian blobs (sigma 2-20 px, x4 for 4096^2) plus
+  band-limited white noise (all FFT bins with radial frequency >= 0.2
+  cyc/px zeroed), min-max normalised to [0, 1];
+* image 2: image 1 under a similarity p' = s R (p - c) + c + t about the
+  centre c (bilinear, zero fill, `warp_rigid` semantics of
+  ref: imaging.py:208-247), then inversion (p = 0.5), gamma in [0.4, 2.5],
+  multiplicative Gamma(L, 1/L) speckle, re-normalised to [0, 1].
+
+Everything is numpy float64 on the host and deterministic per seed.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class PairTruth:
+    """Ground truth of one generated pair (maps reference -> target)."""
+
+    theta_deg: float
+    scale: float
+    translation: tuple
+    inverted: bool
+    gamma: float
+    looks: int
+    size: int
+    matrix: np.ndarray = field(default=None)   # 2x3 affine, (x, y) convention
+
+    def apply(self, pts) -> np.ndarray:
+        pts = np.asarray(pts, dtype=np.float64).reshape(-1, 2)
+        return pts @ self.matrix[:, :2].T + self.matrix[:, 2]
+
+
+def blob_field(size: int, seed: int, n_blobs: int = 200, sigma_scale: float = 1.0,
+               noise_weight: float = 0.5, f_cut: float = 0.2) -> np.ndarray:
+    """Image 1 of the BASELINE generator (see module docstring)."""
+    rng = np.random.default_rng(seed)
+    img = np.zeros((size, size))
+    for _ in range(n_blobs):
+        cx, cy = rng.uniform(0, size, 2)
+        sx, sy = rng.uniform(2.0, 20.0, 2) * sigma_scale
+        phi = rng.uniform(0, math.pi)
+        amp = rng.uniform(-1.0, 1.0)
+        ext = int(math.ceil(4.0 * max(sx, sy)))
+        x0, x1 = max(int(cx) - ext, 0), min(int(cx) + ext + 1, size)
+        y0, y1 = max(int(cy) - ext, 0), min(int(cy) + ext + 1, size)
+        if x0 >= x1 or y0 >= y1:
+            continue
+        ys, xs = np.mgrid[y0:y1, x0:x1].astype(np.float64)
+        dx, dy = xs - cx, ys - cy
+        u = math.cos(phi) * dx + math.sin(phi) * dy
+        v = -math.sin(phi) * dx + math.cos(phi) * dy
+        img[y0:y1, x0:x1] += amp * np.exp(-0.5 * ((u / sx) ** 2 + (v / sy) ** 2))
+    white = rng.standard_normal((size, size))
+    spec = np.fft.fft2(white)
+    f = np.fft.fftfreq(size)
+    spec[np.hypot(f[:, None], f[None, :]) >= f_cut] = 0.0
+    noise = np.fft.ifft2(spec).real
+    noise /= max(noise.std(), 1e-12)
+    img /= max(img.std(), 1e-12)
+    img = img + noise_weight * noise
+    return (img - img.min()) / (img.max() - img.min())
+
+
+def similarity(size: int, theta_deg: float, scale: float, t) -> np.ndarray:
+    """2x3 matrix of p' = s R (p - c) + c + t, c the image centre."""
+    c = (size - 1) / 2.0
+    th = math.radians(theta_deg)
+    co, si = math.cos(th), math.sin(th)
+    # snap quarter turns like ref: imaging.py:61-63
+    co = 0.0 if abs(co) < 1e-15 else (math.copysign(1.0, co) if abs(abs(co) - 1) < 1e-15 else co)
+    si = 0.0 if abs(si) < 1e-15 else (math.copysign(1.0, si) if abs(abs(si) - 1) < 1e-15 else si)
+    a = scale * np.array([[co, -si], [si, co]])
+    off = np.array([c, c]) + np.asarray(t, dtype=np.float64) - a @ np.array([c, c])
+    return np.concatenate([a, off[:, None]], axis=1)
+
+
+def warp(img: np.ndarray, m: np.ndarray) -> np.ndarray:
+    """Output p samples img at m^-1(p), bilinear, zero outside
+    (ref: imaging.py:208-247 semantics, generalised to a similarity)."""
+    h, w = img.shape
+    a_inv = np.linalg.inv(m[:, :2])
+    t_inv = -a_inv @ m[:, 2]
+    xs, ys = np.meshgrid(np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64))
+    sx = a_inv[0, 0] * xs + a_inv[0, 1] * ys + t_inv[0]
+    sy = a_inv[1, 0] * xs + a_inv[1, 1] * ys + t_inv[1]
+    x0 = np.floor(sx).astype(np.int64)
+    y0 = np.floor(sy).astype(np.int64)
+    fx, fy = sx - x0, sy - y0
+    out = np.zeros((h, w))
+    ok = (x0 >= 0) & (x0 < w - 1) & (y0 >= 0) & (y0 < h - 1)
+    on = (fx == 0) & (fy == 0) & (x0 >= 0) & (x0 < w) & (y0 >= 0) & (y0 < h)
+    xv, yv, fxv, fyv = x0[ok], y0[ok], fx[ok], fy[ok]
+    out[ok] = (img[yv, xv] * (1 - fxv) * (1 - fyv) + img[yv, xv + 1] * fxv * (1 - fyv)
+               + img[yv + 1, xv] * (1 - fxv) * fyv + img[yv + 1, xv + 1] * fxv * fyv)
+    edge = on & ~ok
+    out[edge] = img[y0[edge], x0[edge]]
+    return out
+
+
+def make_pair(size: int = 1024, seed: int = 0, theta_deg: float | None = None,
+              scale_jitter: float = 0.0, looks: int | None = 4,
+              sigma_scale: float | None = None, radiometric: bool = True):
+    """(image1, image2, truth) per the BASELINE.json generator, float64."""
+    rng = np.random.default_rng(10_000 + seed)
+    if sigma_scale is None:
+        sigma_scale = 4.0 if size >= 4096 else 1.0
+    img1 = blob_field(size, seed, sigma_scale=sigma_scale)
+    theta = float(rng.uniform(0.0, 360.0)) if theta_deg is None else float(theta_deg)
+    scale = float(rng.uniform(1.0 - scale_jitter, 1.0 + scale_jitter)) if scale_jitter else 1.0
+    t = tuple(float(v) for v in rng.uniform(-20.0, 20.0, 2))
+    m = similarity(size, theta, scale, t)
+    img2 = warp(img1, m)
+    inverted = bool(rng.uniform() < 0.5)
+    gamma = float(rng.uniform(0.4, 2.5))
+    if radiometric:
+        if inverted:
+            img2 = 1.0 - img2
+        img2 = np.clip(img2, 0.0, 1.0) ** gamma
+        if looks:
+            img2 = img2 * rng.gamma(float(looks), 1.0 / looks, img2.shape)
+        img2 = (img2 - img2.min()) / max(img2.max() - img2.min(), 1e-12)
+    truth = PairTruth(theta, scale, t, inverted, gamma, looks or 0, size, m)
+    return img1, img2, truth
+
+
+def make_batch(n_pairs: int, size: int = 1024, seed0: int = 0, dtype=np.float32, **kw):
+    """(2*n_pairs, size, size) stack [ref0, tgt0, ref1, tgt1, ...] + truths."""
+    out = np.empty((2 * n_pairs, size, size), dtype=dtype)
+    truths = []
+    for i in range(n_pairs):
+        a, b, tr = make_pair(size, seed0 + i, **kw)
+        out[2 * i], out[2 * i + 1] = a, b
+        truths.append(tr)
+    return out, truths
