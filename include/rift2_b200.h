@@ -1,0 +1,150 @@
+/*
+ * rift2_b200 -- C ABI of the B200 RIFT2 feature pipeline.
+ *
+ * Plain pointers and sizes only.  Every device pointer is caller-owned
+ * (the library allocates nothing per call; the only cached state is the
+ * per-(device, length) FFT twiddle tables and per-angle descriptor gather
+ * tables).  All work is enqueued on `stream` (a cudaStream_t, NULL = legacy
+ * default stream) and the calls are reentrant across streams and devices.
+ *
+ * Status codes (mapped onto the reference's exception types by the Python
+ * layer, ref: pkg/src/rift2/errors.py:4-21):
+ *   0 RIFT2_OK
+ *   1 RIFT2_BAD_ARGUMENT   -> ParameterError (ref preconditions, e.g.
+ *                             loggabor.py:57-67, detector.py:96-99,146-149,
+ *                             matcher.py:105-106)
+ *   2 RIFT2_UNSUPPORTED    -> ParameterError (size/parameter outside the
+ *                             kernels' range, e.g. an FFT length with a
+ *                             prime factor other than 2, 3, 5)
+ *   3 RIFT2_CUDA_ERROR     -> RiftError (text from rift2_last_error())
+ *   4 RIFT2_CAPACITY       -> RiftError (an output buffer was too small)
+ */
+#ifndef RIFT2_B200_H
+#define RIFT2_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RIFT2_OK 0
+#define RIFT2_BAD_ARGUMENT 1
+#define RIFT2_UNSUPPORTED 2
+#define RIFT2_CUDA_ERROR 3
+#define RIFT2_CAPACITY 4
+
+/* Filter-bank parameters; mirrors ref: pkg/src/rift2/loggabor.py:35-80
+ * (BankParams) and config.py:73-84.  orientation_spread <= 0 selects the
+ * reference default pi / n_orient. */
+typedef struct rift2_bank_params {
+  int32_t n_scales;
+  int32_t n_orient;
+  double min_wavelength;
+  double scale_mult;
+  double sigma_on_f;
+  double orientation_spread;
+  double noise_k;
+  double spread_cutoff;
+  double spread_gain;
+} rift2_bank_params;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int32_t rift2_version(void);
+
+/* Human-readable text of the last non-zero status on this thread. */
+const char* rift2_last_error(void);
+
+/* ---- stage 1: phase-congruency moments + maximum index map -------------
+ * Replaces ref: pkg/src/rift2/pipeline.py:42-50 (compute_fields), i.e.
+ * loggabor.py:131-251 (build_filter_bank / apply_bank /
+ * phase_congruency_moments / orientation_amplitudes) and mim.py:43-55
+ * (build_mim), for a batch of `batch` images.
+ *   images       [batch][height][width] float32, device
+ *   moment_max   [batch][height][width] float32 out        (PCField.moment_max)
+ *   moment_min   [batch][height][width] float32 out        (PCField.moment_min)
+ *   mim          [batch][height][width] uint8 out, 1-based (IndexMap.indices)
+ *   a_o, pc_o    [batch][n_orient][height][width] float32 out, may be NULL
+ *   a_max        [batch][height][width] float32 out, may be NULL
+ * height, width >= 16 with prime factors in {2, 3, 5}; n_scales <= 8,
+ * n_orient <= 16. */
+int32_t rift2_fields_workspace_size(int32_t batch, int32_t height, int32_t width,
+                                    const rift2_bank_params* params, size_t* bytes);
+int32_t rift2_fields(const float* images, int32_t batch, int32_t height, int32_t width,
+                     const rift2_bank_params* params, float* moment_max, float* moment_min,
+                     uint8_t* mim, float* a_o, float* pc_o, float* a_max, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* ---- stage 2: FAST keypoints on both moment maps -------------------------
+ * Replaces ref: pkg/src/rift2/detector.py:140-155 (detect_keypoints) for a
+ * batch; with single_map != 0 it replaces detector.py:87-113 (detect_fast)
+ * on `maps` alone (kind 0).
+ *   maps         [batch][2][height][width] (moment_min, moment_max), either
+ *                float32 (rift2_detect_f32) or float64 (rift2_detect_f64);
+ *                must be finite (the Python layer checks, ref: detector.py:96-97)
+ *   kp_x, kp_y   [batch][max_points] int32 out
+ *   kp_response  [batch][max_points] float64 out
+ *   kp_kind      [batch][max_points] uint8 out (0 corner, 1 edge)
+ *   kp_count     [batch] int32 out
+ * Keypoints are ordered by (-response, y, x), corner before edge on ties. */
+int32_t rift2_detect_workspace_size(int32_t batch, int32_t height, int32_t width, int32_t max_points,
+                                    size_t* bytes);
+int32_t rift2_detect_f32(const float* maps, int32_t batch, int32_t height, int32_t width,
+                         double threshold, int32_t max_points, int32_t border_margin, int32_t single_map,
+                         int32_t* kp_x, int32_t* kp_y, double* kp_response, uint8_t* kp_kind,
+                         int32_t* kp_count, void* workspace, size_t workspace_bytes, void* stream);
+int32_t rift2_detect_f64(const double* maps, int32_t batch, int32_t height, int32_t width,
+                         double threshold, int32_t max_points, int32_t border_margin, int32_t single_map,
+                         int32_t* kp_x, int32_t* kp_y, double* kp_response, uint8_t* kp_kind,
+                         int32_t* kp_count, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- stage 3: RIFT2 dominant-index descriptors ---------------------------
+ * Replaces ref: pkg/src/rift2/descriptor.py:179-216 (describe_rift2),
+ * :219-236 (describe_ring, mode 1) and :239-254 (describe_plain, mode 0).
+ *   mim          [batch][height][width] uint8 (1..n_orient)
+ *   kp_x, kp_y   [batch][kp_stride] int32, kp_count [batch] int32
+ *   desc_counts  [batch][desc_capacity][desc_stride] float16 out: integer
+ *                cell-histogram counts (zero padded to desc_stride >= dim)
+ *   desc_sqnorm  [batch][desc_capacity] int32 out: sum of squared counts
+ *   desc_kp      [batch][desc_capacity] int32 out: keypoint id
+ *   desc_variant [batch][desc_capacity] uint8 out: dominant index / layer
+ *   desc_count   [batch] int32 out, desc_skipped [batch] int32 out
+ * Descriptors are ordered by keypoint, then [peak, runner-up] (rift2) or
+ * layer 1..n (ring).  mode: 0 plain, 1 ring, 2 rift2. */
+int32_t rift2_describe_workspace_size(int32_t batch, int32_t kp_stride, int32_t grid, int32_t n_orient,
+                                      size_t* bytes);
+int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
+                       const int32_t* kp_x, const int32_t* kp_y, const int32_t* kp_count, int32_t kp_stride,
+                       int32_t patch_size, int32_t grid, double dominant_ratio, int32_t rotate_patch,
+                       int32_t mode, void* desc_counts, int32_t desc_stride, int32_t desc_capacity,
+                       int32_t* desc_sqnorm, int32_t* desc_kp, uint8_t* desc_variant, int32_t* desc_count,
+                       int32_t* desc_skipped, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- stage 4: brute-force nearest-neighbour matching ---------------------
+ * Replaces ref: pkg/src/rift2/matcher.py:102-148 (match_nn) for `n_pairs`
+ * independent (reference, target) descriptor sets.  Descriptor blocks use
+ * the stage-3 layout; pair p uses reference block ref_block[p] and target
+ * block tgt_block[p] of the descriptor arrays (device int32 arrays);
+ * n_blocks is the number of blocks the descriptor arrays hold.  desc_stride
+ * must be 224 or 256 (the tensor-core tiles cover K <= 256).
+ *   out_ref, out_tgt [n_pairs][tgt_kp_capacity] int32 out (keypoint ids)
+ *   out_dist         [n_pairs][tgt_kp_capacity] float64 out
+ *   out_count        [n_pairs] int32 out (= number of target keypoints
+ *                    with a descriptor)
+ * Pairs are sorted by (dist, ref, tgt) as the reference returns them.
+ * Ranking is exact: candidates are compared on integer dot products and
+ * squared norms, ties resolve to the smallest reference keypoint id. */
+int32_t rift2_match_workspace_size(int32_t n_pairs, int32_t desc_capacity, int32_t tgt_kp_capacity,
+                                   size_t* bytes);
+int32_t rift2_match(const void* desc_counts, const int32_t* desc_sqnorm, const int32_t* desc_kp,
+                    const int32_t* desc_count, int32_t n_blocks, int32_t desc_stride, int32_t desc_capacity,
+                    int32_t dim, int32_t n_pairs, const int32_t* ref_block, const int32_t* tgt_block,
+                    int32_t tgt_kp_capacity, int32_t* out_ref, int32_t* out_tgt, double* out_dist,
+                    int32_t* out_count, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RIFT2_B200_H */

@@ -1,0 +1,264 @@
+// extern "C" boundary of librift2_b200.so (declared in include/rift2_b200.h).
+//
+// Argument validation mirrors the reference's preconditions so the Python
+// layer can raise the same exception types:
+//   ref: pkg/src/rift2/loggabor.py:57-67   (BankParams.__post_init__)
+//   ref: pkg/src/rift2/loggabor.py:134-135 (filter bank needs >= 16 px)
+//   ref: pkg/src/rift2/detector.py:96-99   (finite map, threshold > 0)
+//   ref: pkg/src/rift2/matcher.py:105-106  (non-empty descriptor lists)
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "../../include/rift2_b200.h"
+#include "detect.h"
+#include "describe.h"
+#include "fields.h"
+#include "match.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int32_t fail(int32_t code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int32_t cuda_status(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(RIFT2_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
+  return RIFT2_OK;
+}
+
+int32_t map_internal(int32_t rc, const char* where) {
+  if (rc == 0) return RIFT2_OK;
+  if (rc == 3) {
+    cudaError_t e = cudaGetLastError();
+    return fail(RIFT2_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
+  }
+  if (rc == 1) return fail(RIFT2_BAD_ARGUMENT, "%s: workspace too small or bad argument", where);
+  if (rc == 4) return fail(RIFT2_CAPACITY, "%s: output capacity exceeded", where);
+  return fail(RIFT2_UNSUPPORTED, "%s: unsupported size or parameter", where);
+}
+
+bool fft_len_ok(int n) {
+  if (n < 1) return false;
+  for (int p : {2, 3, 5})
+    while (n % p == 0) n /= p;
+  return n == 1;
+}
+
+int32_t bank_consts(const rift2_bank_params* p, r2::BankConsts& k) {
+  if (!p) return fail(RIFT2_BAD_ARGUMENT, "params is NULL");
+  if (p->n_scales < 1) return fail(RIFT2_BAD_ARGUMENT, "n_scales must be >= 1");
+  if (p->n_orient < 2) return fail(RIFT2_BAD_ARGUMENT, "n_orient must be >= 2");
+  if (!(p->min_wavelength >= 2)) return fail(RIFT2_BAD_ARGUMENT, "min_wavelength must be >= 2");
+  if (!(p->scale_mult > 1)) return fail(RIFT2_BAD_ARGUMENT, "scale_mult must be > 1");
+  if (!(p->sigma_on_f > 0 && p->sigma_on_f < 1)) return fail(RIFT2_BAD_ARGUMENT, "sigma_on_f must be in (0, 1)");
+  if (p->n_scales > 8 || p->n_orient > 16)
+    return fail(RIFT2_UNSUPPORTED, "n_scales <= 8 and n_orient <= 16 supported");
+  k.n_scales = p->n_scales;
+  k.n_orient = p->n_orient;
+  for (int s = 0; s < p->n_scales; ++s) k.log_lambda[s] = std::log(p->min_wavelength * std::pow(p->scale_mult, s));
+  const double ls = std::log(p->sigma_on_f);
+  k.inv_den_r = 1.0 / (2.0 * ls * ls);
+  const double st = p->orientation_spread > 0 ? p->orientation_spread : M_PI / p->n_orient;
+  k.inv_den_a = 1.0 / (2.0 * st * st);
+  for (int o = 0; o < p->n_orient; ++o) {
+    k.angle[o] = o * M_PI / p->n_orient;
+    k.cos_a[o] = std::cos(k.angle[o]);
+    k.sin_a[o] = std::sin(k.angle[o]);
+  }
+  k.spread_cutoff = p->spread_cutoff;
+  k.spread_gain = p->spread_gain;
+  k.lp_lncut = std::log(0.45);
+  // ref: loggabor.py:221-227
+  const double q = 1.0 / p->scale_mult;
+  const double total = (1.0 - std::pow(q, p->n_scales)) / (1.0 - q);
+  k.thr_factor = total / std::sqrt(std::log(4.0)) *
+                 (std::sqrt(M_PI / 2.0) + p->noise_k * std::sqrt((4.0 - M_PI) / 2.0));
+  return RIFT2_OK;
+}
+
+std::mutex g_tw_mu;
+std::unordered_map<long long, float2*> g_tw;
+
+}  // namespace
+
+namespace r2 {
+const float2* twiddle_table(int n) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  const long long key = ((long long)dev << 32) | (unsigned)n;
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto it = g_tw.find(key);
+  if (it != g_tw.end()) return it->second;
+  float2* host = new float2[n];
+  for (int j = 0; j < n; ++j) {
+    const double a = -2.0 * M_PI * (double)j / (double)n;
+    host[j] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  float2* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(float2) * n);
+  if (e == cudaSuccess) e = cudaMemcpy(d, host, sizeof(float2) * n, cudaMemcpyHostToDevice);
+  delete[] host;
+  if (e != cudaSuccess) { if (d) cudaFree(d); return nullptr; }
+  g_tw[key] = d;
+  return d;
+}
+}  // namespace r2
+
+template <class T>
+static int32_t detect_impl(const T* maps, int32_t batch, int32_t height, int32_t width, double threshold,
+                           int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
+                           int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (!(threshold > 0)) return fail(RIFT2_BAD_ARGUMENT, "FAST threshold must be positive");
+  if (batch < 1 || height < 1 || width < 1 || max_points < 0 || border_margin < 0)
+    return fail(RIFT2_BAD_ARGUMENT, "bad detect dimensions");
+  if (!maps || !kp_count || !workspace || (max_points > 0 && (!kp_x || !kp_y || !kp_response || !kp_kind)))
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  r2::DetectArgs a{batch, height, width, threshold, max_points, border_margin, single_map != 0,
+                   kp_x, kp_y, kp_response, kp_kind, kp_count};
+  int32_t rc = r2::detect_run(maps, a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  return map_internal(rc, "rift2_detect");
+}
+
+extern "C" {
+
+int32_t rift2_version(void) { return 100; }
+
+const char* rift2_last_error(void) { return g_err; }
+
+// ------------------------------------------------------------------ fields
+static int32_t check_fields_dims(int32_t batch, int32_t h, int32_t w) {
+  if (batch < 1) return fail(RIFT2_BAD_ARGUMENT, "batch must be >= 1");
+  if (h < 16 || w < 16) return fail(RIFT2_BAD_ARGUMENT, "filter bank needs width and height >= 16");
+  if (!fft_len_ok(h) || !fft_len_ok(w))
+    return fail(RIFT2_UNSUPPORTED, "image %dx%d: FFT lengths must factor into 2, 3 and 5", h, w);
+  if ((w > 4096 || h > 4096) && !((w & (w - 1)) == 0 && (h & (h - 1)) == 0))
+    return fail(RIFT2_UNSUPPORTED, "non power-of-two sizes above 4096 are not supported");
+  if (w > 4096 || h > 4096) return fail(RIFT2_UNSUPPORTED, "sizes above 4096 are not supported");
+  return RIFT2_OK;
+}
+
+int32_t rift2_fields_workspace_size(int32_t batch, int32_t height, int32_t width,
+                                    const rift2_bank_params* params, size_t* bytes) {
+  r2::BankConsts k;
+  int32_t rc = bank_consts(params, k);
+  if (rc) return rc;
+  if ((rc = check_fields_dims(batch, height, width))) return rc;
+  if (!bytes) return fail(RIFT2_BAD_ARGUMENT, "bytes is NULL");
+  *bytes = r2::fields_workspace_bytes(batch, height, width, k.n_scales, k.n_orient);
+  return RIFT2_OK;
+}
+
+int32_t rift2_fields(const float* images, int32_t batch, int32_t height, int32_t width,
+                     const rift2_bank_params* params, float* moment_max, float* moment_min, uint8_t* mim,
+                     float* a_o, float* pc_o, float* a_max, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+  r2::BankConsts k;
+  int32_t rc = bank_consts(params, k);
+  if (rc) return rc;
+  if ((rc = check_fields_dims(batch, height, width))) return rc;
+  if (!images || !moment_max || !moment_min || !mim || !workspace)
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  r2::FieldsOutputs out{moment_max, moment_min, mim, a_o, pc_o, a_max};
+  rc = r2::fields_run(images, batch, height, width, k, out, workspace, workspace_bytes,
+                      static_cast<cudaStream_t>(stream));
+  return map_internal(rc, "rift2_fields");
+}
+
+// ------------------------------------------------------------------ detect
+int32_t rift2_detect_workspace_size(int32_t batch, int32_t height, int32_t width, int32_t max_points,
+                                    size_t* bytes) {
+  if (batch < 1 || height < 1 || width < 1 || max_points < 0 || !bytes)
+    return fail(RIFT2_BAD_ARGUMENT, "bad detect dimensions");
+  *bytes = r2::detect_workspace_bytes(batch, height, width, max_points);
+  return RIFT2_OK;
+}
+
+int32_t rift2_detect_f32(const float* maps, int32_t batch, int32_t height, int32_t width, double threshold,
+                         int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
+                         int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  return detect_impl(maps, batch, height, width, threshold, max_points, border_margin, single_map, kp_x, kp_y,
+                     kp_response, kp_kind, kp_count, workspace, workspace_bytes, stream);
+}
+
+int32_t rift2_detect_f64(const double* maps, int32_t batch, int32_t height, int32_t width, double threshold,
+                         int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
+                         int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  return detect_impl(maps, batch, height, width, threshold, max_points, border_margin, single_map, kp_x, kp_y,
+                     kp_response, kp_kind, kp_count, workspace, workspace_bytes, stream);
+}
+
+// ---------------------------------------------------------------- describe
+int32_t rift2_describe_workspace_size(int32_t batch, int32_t kp_stride, int32_t grid, int32_t n_orient,
+                                      size_t* bytes) {
+  if (batch < 1 || kp_stride < 0 || grid < 1 || grid > 16 || n_orient < 2 || n_orient > 16 || !bytes)
+    return fail(RIFT2_BAD_ARGUMENT, "bad describe dimensions");
+  *bytes = r2::describe_workspace_bytes(batch, kp_stride, grid, n_orient);
+  return RIFT2_OK;
+}
+
+int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
+                       const int32_t* kp_x, const int32_t* kp_y, const int32_t* kp_count, int32_t kp_stride,
+                       int32_t patch_size, int32_t grid, double dominant_ratio, int32_t rotate_patch,
+                       int32_t mode, void* desc_counts, int32_t desc_stride, int32_t desc_capacity,
+                       int32_t* desc_sqnorm, int32_t* desc_kp, uint8_t* desc_variant, int32_t* desc_count,
+                       int32_t* desc_skipped, void* workspace, size_t workspace_bytes, void* stream) {
+  if (batch < 1 || height < 1 || width < 1 || kp_stride < 0) return fail(RIFT2_BAD_ARGUMENT, "bad dimensions");
+  if (n_orient < 2 || n_orient > 16) return fail(RIFT2_UNSUPPORTED, "n_orient must be in [2, 16]");
+  if (grid < 1 || patch_size < grid || patch_size % grid != 0)
+    return fail(RIFT2_BAD_ARGUMENT, "patch %d does not divide into %d cells", patch_size, grid);
+  if (patch_size > 256 || grid > 16 || grid * grid * n_orient > desc_stride)
+    return fail(RIFT2_UNSUPPORTED, "patch_size <= 256, grid <= 16 and grid^2*n_orient <= desc_stride required");
+  if (!(dominant_ratio > 0 && dominant_ratio <= 1)) return fail(RIFT2_BAD_ARGUMENT, "dominant_ratio in (0, 1]");
+  if (mode < 0 || mode > 2) return fail(RIFT2_BAD_ARGUMENT, "mode must be 0 plain, 1 ring, 2 rift2");
+  if (!mim || !kp_count || !desc_counts || !desc_sqnorm || !desc_kp || !desc_variant || !desc_count ||
+      !desc_skipped || !workspace)
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  r2::DescribeArgs a{batch, height, width, n_orient, kp_x, kp_y, kp_count, kp_stride, patch_size, grid,
+                     dominant_ratio, rotate_patch != 0, mode, static_cast<__half*>(desc_counts), desc_stride,
+                     desc_capacity, desc_sqnorm, desc_kp, desc_variant, desc_count, desc_skipped};
+  int32_t rc = r2::describe_run(mim, a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  return map_internal(rc, "rift2_describe");
+}
+
+// ------------------------------------------------------------------- match
+int32_t rift2_match_workspace_size(int32_t n_pairs, int32_t desc_capacity, int32_t tgt_kp_capacity,
+                                   size_t* bytes) {
+  if (n_pairs < 1 || desc_capacity < 0 || tgt_kp_capacity < 0 || !bytes)
+    return fail(RIFT2_BAD_ARGUMENT, "bad match dimensions");
+  *bytes = r2::match_workspace_bytes(n_pairs, desc_capacity, tgt_kp_capacity);
+  return RIFT2_OK;
+}
+
+int32_t rift2_match(const void* desc_counts, const int32_t* desc_sqnorm, const int32_t* desc_kp,
+                    const int32_t* desc_count, int32_t n_blocks, int32_t desc_stride, int32_t desc_capacity,
+                    int32_t dim, int32_t n_pairs, const int32_t* ref_block, const int32_t* tgt_block, int32_t tgt_kp_capacity,
+                    int32_t* out_ref, int32_t* out_tgt, double* out_dist, int32_t* out_count, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  if (n_pairs < 1 || n_blocks < 1 || desc_capacity < 1 || dim < 1 || dim > desc_stride || desc_stride % 8 != 0)
+    return fail(RIFT2_BAD_ARGUMENT, "bad match dimensions");
+  if (desc_stride != 224 && desc_stride != 256) return fail(RIFT2_UNSUPPORTED, "desc_stride must be 224 or 256");
+  if (!desc_counts || !desc_sqnorm || !desc_kp || !desc_count || !ref_block || !tgt_block || !out_ref ||
+      !out_tgt || !out_dist || !out_count || !workspace)
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  r2::MatchArgs a{static_cast<const __half*>(desc_counts), desc_sqnorm, desc_kp, desc_count, desc_stride,
+                  desc_capacity, dim, n_pairs, n_blocks, ref_block, tgt_block, tgt_kp_capacity, out_ref, out_tgt,
+                  out_dist, out_count};
+  int32_t rc = r2::match_run(a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  return map_internal(rc, "rift2_match");
+}
+
+}  // extern "C"

@@ -1,0 +1,473 @@
+// FAST keypoints on the moment maps, exact to the reference.
+//
+// Replaces ref: pkg/src/rift2/detector.py:50-155:
+//   _normalize (:80-84), _fast_score (:50-77), detect_fast (:87-113),
+//   _merge_within_radius (:116-137), detect_keypoints (:140-155).
+//
+// Exactness: the reference scores d_j = n_j - n_c on the min-max normalised
+// map n.  Normalisation fl(fl(v - lo) / fl(hi - lo)) and fl(a - c) are both
+// monotone non-decreasing, so max_k min_arc fl(n_j - n_c) equals
+// fl(n(max_k min_arc v_j) - n(v_c)) bit for bit.  The arc min/max therefore
+// run on the raw map values (float32 for the GPU's own maps) and only three
+// float64 operations per pixel touch the normalised values.
+//
+// Kernels: k_init -> k_minmax -> k_fast_nms (score + 3x3 NMS + margin +
+// candidate keys) -> k_select_sort (radix-select the max_points smallest
+// (-score, y, x, kind) keys, sort) -> k_merge_suppress (2-px greedy merge of
+// corners and edges as a parallel priority MIS, cap).
+#include <cfloat>
+
+#include "detect.h"
+#include "sort.cuh"
+
+namespace r2 {
+
+namespace {
+
+constexpr int kTile = 32;
+constexpr int kHalo = 4;                  // 3 for the ring + 1 for NMS
+constexpr int kIn = kTile + 2 * kHalo;    // 40
+constexpr int kSc = kTile + 2;            // 34
+constexpr int kMaxNbr = 32;
+
+__constant__ int c_ring_dx[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
+__constant__ int c_ring_dy[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+
+R2_DEV unsigned long long ord_key(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+R2_DEV double ord_val(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+__global__ void k_init(unsigned long long* mm, unsigned* cnt, int planes) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < planes) { mm[2 * i] = ~0ull; mm[2 * i + 1] = 0ull; cnt[i] = 0; }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_minmax(const T* __restrict__ maps, size_t n, unsigned long long* mm) {
+  const int plane = blockIdx.y;
+  const T* p = maps + (size_t)plane * n;
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ord_key((double)p[i]);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, off);
+    const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, off);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[2 * plane], lo);
+    atomicMax(&mm[2 * plane + 1], hi);
+  }
+}
+
+// Largest threshold at which some 9-arc of the ring is brighter (A) /
+// darker (B) than the centre, on raw values: A = max_k min_{j<9} v[k+j],
+// B = min_k max_{j<9} v[k+j].
+template <class T>
+R2_DEV void arc_extrema(const T (&v)[16], T& A, T& B) {
+  T m2[16], M2[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) { m2[k] = min(v[k], v[(k + 1) & 15]); M2[k] = max(v[k], v[(k + 1) & 15]); }
+  T m4[16], M4[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) { m4[k] = min(m2[k], m2[(k + 2) & 15]); M4[k] = max(M2[k], M2[(k + 2) & 15]); }
+  T a = min(min(m4[0], m4[4]), v[8]);
+  T b = max(max(M4[0], M4[4]), v[8]);
+#pragma unroll
+  for (int k = 1; k < 16; ++k) {
+    a = max(a, min(min(m4[k], m4[(k + 4) & 15]), v[(k + 8) & 15]));
+    b = min(b, max(max(M4[k], M4[(k + 4) & 15]), v[(k + 8) & 15]));
+  }
+  A = a;
+  B = b;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ maps, int H, int W,
+                                                  const unsigned long long* __restrict__ mm, double thr,
+                                                  int margin, int nm, K128* __restrict__ cand,
+                                                  unsigned* __restrict__ cnt, size_t cap) {
+  __shared__ T sv[kIn][kIn + 1];
+  __shared__ double ss[kSc][kSc + 1];
+  const int plane = blockIdx.z;
+  const int kind = nm == 2 ? (plane & 1) : 0;
+  const T* p = maps + (size_t)plane * H * W;
+  const double lo = ord_val(mm[2 * plane]);
+  const double hi = ord_val(mm[2 * plane + 1]);
+  const double span = hi - lo;
+  if (!(span > 0)) return;   // normalised map is all zeros: no keypoints
+  const int ty0 = blockIdx.y * kTile, tx0 = blockIdx.x * kTile;
+  for (int i = threadIdx.x; i < kIn * kIn; i += blockDim.x) {
+    const int yy = ty0 - kHalo + i / kIn, xx = tx0 - kHalo + i % kIn;
+    sv[i / kIn][i % kIn] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? p[(size_t)yy * W + xx] : T(0);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSc * kSc; i += blockDim.x) {
+    const int sy = i / kSc, sx = i % kSc;
+    const int y = ty0 - 1 + sy, x = tx0 - 1 + sx;
+    double s;
+    if (y < 0 || y >= H || x < 0 || x >= W) {
+      s = -DBL_MAX;
+    } else if (y < 3 || y >= H - 3 || x < 3 || x >= W - 3) {
+      s = 0.0;
+    } else {
+      const int cy = sy + kHalo - 1, cx = sx + kHalo - 1;
+      T v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = sv[cy + c_ring_dy[k]][cx + c_ring_dx[k]];
+      T A, B;
+      arc_extrema(v, A, B);
+      const double nc = ((double)sv[cy][cx] - lo) / span;
+      const double na = ((double)A - lo) / span;
+      const double nb = ((double)B - lo) / span;
+      s = fmax(fmax(na - nc, nc - nb), 0.0);
+    }
+    ss[sy][sx] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
+    const int ly = i / kTile, lx = i % kTile;
+    const int y = ty0 + ly, x = tx0 + lx;
+    bool keep = false;
+    double s = 0.0;
+    if (y < H && x < W) {
+      s = ss[ly + 1][lx + 1];
+      keep = s > thr;
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) keep = keep && s >= ss[ly + dy][lx + dx];
+      keep = keep && x >= margin && x <= W - 1 - margin && y >= margin && y <= H - 1 - margin;
+    }
+    const unsigned slot = agg_inc(&cnt[plane], keep);
+    if (keep && slot < cap) {
+      K128 k;
+      k.hi = ~(unsigned long long)__double_as_longlong(s);
+      k.lo = ((unsigned long long)y << 32) | ((unsigned long long)x << 8) | (unsigned long long)kind;
+      cand[(size_t)plane * cap + slot] = k;
+    }
+  }
+}
+
+R2_DEV bool top_bits_le(const K128& k, const K128& pref, int bits) {
+  // compare the top `bits` bits of k and pref as unsigned 128-bit numbers
+  K128 a = k, b = pref;
+  if (bits < 64) {
+    const unsigned long long m = bits == 0 ? 0ull : (~0ull << (64 - bits));
+    a.hi &= m; b.hi &= m; a.lo = 0; b.lo = 0;
+  } else {
+    const int lb = bits - 64;
+    const unsigned long long m = lb == 0 ? 0ull : (~0ull << (64 - lb));
+    a.lo &= m; b.lo &= m;
+  }
+  return !k_less(b, a);
+}
+
+R2_DEV unsigned digit_of(const K128& k, int d) {   // d = 0..15, MSB first
+  return d < 8 ? (unsigned)(k.hi >> (56 - 8 * d)) & 255u : (unsigned)(k.lo >> (56 - 8 * (d - 8))) & 255u;
+}
+
+// Select the K smallest keys of each plane and sort them.
+__global__ void __launch_bounds__(1024) k_select_sort(const K128* __restrict__ cand, const unsigned* __restrict__ cnt,
+                                                      size_t cap, int K, K128* __restrict__ sorted,
+                                                      K128* __restrict__ tmp, unsigned* __restrict__ nsel) {
+  extern __shared__ K128 s_keys[];
+  __shared__ unsigned h[256];
+  __shared__ unsigned s_need, s_bin, s_done, s_out;
+  const int plane = blockIdx.x;
+  const K128* c = cand + (size_t)plane * cap;
+  const int n = (int)min((size_t)cnt[plane], cap);
+  K128* out = sorted + (size_t)plane * K;
+  K128* scratch = tmp + (size_t)plane * K;
+  int m = n;
+  if (n > K) {
+    K128 pref{0ull, 0ull};
+    int bits = 0;
+    if (threadIdx.x == 0) { s_need = K; s_done = 0; }
+    __syncthreads();
+    for (int d = 0; d < 16; ++d) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const K128 k = c[i];
+        bool match;
+        if (bits == 0) match = true;
+        else {
+          K128 a = k;
+          if (bits <= 64) {
+            const unsigned long long msk = ~0ull << (64 - bits);
+            match = (a.hi & msk) == (pref.hi & msk);
+          } else {
+            const unsigned long long msk = ~0ull << (128 - bits);
+            match = a.hi == pref.hi && (a.lo & msk) == (pref.lo & msk);
+          }
+        }
+        if (match) atomicAdd(&h[digit_of(k, d)], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned cum = 0, need = s_need;
+        for (int b = 0; b < 256; ++b) {
+          if (cum + h[b] >= need) {
+            s_bin = b;
+            s_need = need - cum;
+            s_done = (h[b] == need - cum) ? 1u : 0u;
+            break;
+          }
+          cum += h[b];
+        }
+      }
+      __syncthreads();
+      const unsigned long long bv = s_bin;
+      if (d < 8) pref.hi |= bv << (56 - 8 * d);
+      else pref.lo |= bv << (56 - 8 * (d - 8));
+      bits += 8;
+      const bool done = s_done;
+      __syncthreads();
+      if (done) break;
+    }
+    if (threadIdx.x == 0) s_out = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const K128 k = c[i];
+      if (top_bits_le(k, pref, bits)) {
+        const unsigned slot = atomicAdd(&s_out, 1u);
+        if (slot < (unsigned)K) out[slot] = k;
+      }
+    }
+    __syncthreads();
+    m = min((int)s_out, K);
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = c[i];
+    __syncthreads();
+  }
+  sort_keys_block(out, scratch, m, s_keys);
+  if (threadIdx.x == 0) nsel[plane] = m;
+}
+
+R2_DEV void write_kp(const K128& k, int idx, const DetectArgs& a, int b) {
+  const size_t o = (size_t)b * a.max_points + idx;
+  a.kp_y[o] = (int32_t)(k.lo >> 32);
+  a.kp_x[o] = (int32_t)((k.lo >> 8) & 0xffffffull);
+  a.kp_kind[o] = (uint8_t)(k.lo & 0xffull);
+  a.kp_resp[o] = __longlong_as_double((long long)~k.hi);
+}
+
+__global__ void __launch_bounds__(1024) k_emit_single(const K128* __restrict__ sorted, const unsigned* __restrict__ nsel,
+                                                      DetectArgs a) {
+  const int b = blockIdx.x;
+  const int m = nsel[b];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) write_kp(sorted[(size_t)b * a.max_points + i], i, a, b);
+  if (threadIdx.x == 0) a.kp_count[b] = m;
+}
+
+R2_DEV unsigned hash_pix(unsigned p, unsigned mask) { return (p * 2654435761u) & mask; }
+
+// Greedy 2-px suppression (ref: detector.py:116-137) as a priority MIS:
+// a point is accepted once every higher-priority neighbour is rejected and
+// rejected as soon as one of them is accepted; rounds repeat to a fixpoint,
+// which equals the sequential greedy walk.
+__global__ void __launch_bounds__(1024) k_merge_suppress(const K128* __restrict__ sorted, const unsigned* __restrict__ nsel,
+                                                         K128* __restrict__ merged, int* __restrict__ hkey,
+                                                         int* __restrict__ hval, int tsz, int* __restrict__ nbr,
+                                                         int W, DetectArgs a) {
+  extern __shared__ unsigned char s_status[];   // 0 undecided, 1 accepted, 2 rejected
+  __shared__ int s_flag;
+  __shared__ int s_base;
+  __shared__ int s_warp[32];
+  const int b = blockIdx.x;
+  const int K = a.max_points;
+  const K128* corners = sorted + (size_t)(2 * b) * K;
+  const K128* edges = sorted + (size_t)(2 * b + 1) * K;
+  const int nc = nsel[2 * b], ne = nsel[2 * b + 1];
+  const int n = nc + ne;
+  K128* mg = merged + (size_t)b * 2 * K;
+  int* hk = hkey + (size_t)b * tsz;
+  int* hv = hval + (size_t)b * tsz;
+  int* nb = nbr + (size_t)b * 2 * K * kMaxNbr;
+  const unsigned mask = (unsigned)tsz - 1;
+  merge_path_block(corners, nc, edges, ne, mg);
+  for (int i = threadIdx.x; i < tsz; i += blockDim.x) hk[i] = -1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const K128 k = mg[i];
+    const int pix = (int)(k.lo >> 32) * W + (int)((k.lo >> 8) & 0xffffffull);
+    unsigned h = hash_pix((unsigned)pix, mask);
+    while (true) {
+      if (atomicCAS(&hk[h], -1, pix) == -1) { hv[h] = i; break; }
+      h = (h + 1) & mask;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const K128 k = mg[i];
+    const int y = (int)(k.lo >> 32), x = (int)((k.lo >> 8) & 0xffffffull);
+    int cntn = 0;
+    for (int dy = -2; dy <= 2; ++dy)
+      for (int dx = -2; dx <= 2; ++dx) {
+        if (dx * dx + dy * dy > 4) continue;
+        const int yy = y + dy, xx = x + dx;
+        if (yy < 0 || xx < 0 || xx >= W) continue;
+        const int pix = yy * W + xx;
+        unsigned h = hash_pix((unsigned)pix, mask);
+        while (hk[h] != -1) {
+          if (hk[h] == pix) {
+            const int j = hv[h];
+            if (j < i && cntn < kMaxNbr) nb[(size_t)i * kMaxNbr + cntn++] = j;
+          }
+          h = (h + 1) & mask;
+        }
+      }
+    if (cntn < kMaxNbr) nb[(size_t)i * kMaxNbr + cntn] = -1;
+    s_status[i] = cntn == 0 ? 1 : 0;
+  }
+  __syncthreads();
+  while (true) {
+    if (threadIdx.x == 0) s_flag = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (s_status[i] != 0) continue;
+      bool all_rej = true, any_acc = false;
+      for (int q = 0; q < kMaxNbr; ++q) {
+        const int j = nb[(size_t)i * kMaxNbr + q];
+        if (j < 0) break;
+        const unsigned char st = ((volatile unsigned char*)s_status)[j];
+        if (st == 1) { any_acc = true; break; }
+        if (st != 2) all_rej = false;
+      }
+      if (any_acc) s_status[i] = 2;
+      else if (all_rej) s_status[i] = 1;
+      else s_flag = 1;
+    }
+    __syncthreads();
+    if (!s_flag) break;
+    __syncthreads();
+  }
+  // ordered compaction of the accepted points, capped at K
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const bool acc = i < n && s_status[i] == 1;
+    const unsigned bal = __ballot_sync(0xffffffffu, acc);
+    if (lane == 0) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { const int t = s_warp[w]; s_warp[w] = run; run += t; }
+      s_flag = run;
+    }
+    __syncthreads();
+    if (acc) {
+      const int pos = s_base + s_warp[wid] + __popc(bal & ((1u << lane) - 1u));
+      if (pos < K) write_kp(mg[i], pos, a, b);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += s_flag;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.kp_count[b] = min(s_base, K);
+}
+
+struct DetectPlan {
+  int P, K, tsz;
+  size_t cap;
+  size_t off_mm, off_cnt, off_nsel, off_cand, off_sorted, off_tmp, off_merged, off_hk, off_hv, off_nbr, total;
+};
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+DetectPlan plan_detect(int B, int H, int W, int K) {
+  DetectPlan p{};
+  p.P = 2 * B;
+  p.K = K > 0 ? K : 1;
+  p.cap = (size_t)H * W;
+  int t = 1024;
+  while (t < 4 * p.K) t <<= 1;
+  p.tsz = t;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = al(off + bytes); return o; };
+  p.off_mm = take((size_t)p.P * 2 * sizeof(unsigned long long));
+  p.off_cnt = take((size_t)p.P * sizeof(unsigned));
+  p.off_nsel = take((size_t)p.P * sizeof(unsigned));
+  p.off_cand = take((size_t)p.P * p.cap * sizeof(K128));
+  p.off_sorted = take((size_t)p.P * p.K * sizeof(K128));
+  p.off_tmp = take((size_t)p.P * p.K * sizeof(K128));
+  p.off_merged = take((size_t)B * 2 * p.K * sizeof(K128));
+  p.off_hk = take((size_t)B * p.tsz * sizeof(int));
+  p.off_hv = take((size_t)B * p.tsz * sizeof(int));
+  p.off_nbr = take((size_t)B * 2 * p.K * kMaxNbr * sizeof(int));
+  p.total = off;
+  return p;
+}
+
+template <class T>
+int detect_impl(const T* maps, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const DetectPlan p = plan_detect(a.B, a.H, a.W, a.max_points);
+  if (ws_bytes < p.total) return 1;
+  char* w = static_cast<char*>(ws);
+  auto* mm = reinterpret_cast<unsigned long long*>(w + p.off_mm);
+  auto* cnt = reinterpret_cast<unsigned*>(w + p.off_cnt);
+  auto* nsel = reinterpret_cast<unsigned*>(w + p.off_nsel);
+  auto* cand = reinterpret_cast<K128*>(w + p.off_cand);
+  auto* sorted = reinterpret_cast<K128*>(w + p.off_sorted);
+  auto* tmp = reinterpret_cast<K128*>(w + p.off_tmp);
+  auto* merged = reinterpret_cast<K128*>(w + p.off_merged);
+  auto* hk = reinterpret_cast<int*>(w + p.off_hk);
+  auto* hv = reinterpret_cast<int*>(w + p.off_hv);
+  auto* nbr = reinterpret_cast<int*>(w + p.off_nbr);
+  const int nm = a.single_map ? 1 : 2;
+  const int planes = a.B * nm;
+  if (a.max_points == 0) {
+    cudaMemsetAsync(a.kp_count, 0, sizeof(int32_t) * a.B, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
+  k_init<<<(planes + 255) / 256, 256, 0, st>>>(mm, cnt, planes);
+  const size_t n = (size_t)a.H * a.W;
+  {
+    dim3 grid((unsigned)min((size_t)32, (n + 255) / 256), planes);
+    k_minmax<T><<<grid, 256, 0, st>>>(maps, n, mm);
+  }
+  {
+    dim3 grid((a.W + kTile - 1) / kTile, (a.H + kTile - 1) / kTile, planes);
+    k_fast_nms<T><<<grid, 256, 0, st>>>(maps, a.H, a.W, mm, a.threshold, a.margin, nm, cand, cnt, p.cap);
+  }
+  const size_t sort_smem = kSortChunk * sizeof(K128);
+  cudaFuncSetAttribute(k_select_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
+  k_select_sort<<<planes, 1024, sort_smem, st>>>(cand, cnt, p.cap, a.max_points, sorted, tmp, nsel);
+  if (a.single_map) {
+    k_emit_single<<<a.B, 1024, 0, st>>>(sorted, nsel, a);
+  } else {
+    const size_t smem = (size_t)2 * a.max_points;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_merge_suppress, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_merge_suppress<<<a.B, 1024, smem, st>>>(sorted, nsel, merged, hk, hv, p.tsz, nbr, a.W, a);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+}  // namespace
+
+size_t detect_workspace_bytes(int B, int H, int W, int max_points) {
+  return plan_detect(B, H, W, max_points).total;
+}
+
+int detect_run(const float* maps, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return detect_impl(maps, a, ws, ws_bytes, st);
+}
+
+int detect_run(const double* maps, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return detect_impl(maps, a, ws, ws_bytes, st);
+}
+
+}  // namespace r2

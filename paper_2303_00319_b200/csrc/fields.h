@@ -1,0 +1,36 @@
+// Internal interface of the filter-bank stage (see fields.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace r2 {
+
+// Host-derived constants of the log-Gabor bank (double precision on the host).
+struct BankConsts {
+  int n_scales, n_orient;
+  double log_lambda[8];
+  double inv_den_r, inv_den_a;
+  double angle[16], cos_a[16], sin_a[16];
+  double spread_cutoff, spread_gain;
+  double lp_lncut;
+  double thr_factor;
+};
+
+struct FieldsOutputs {
+  float* mmax;
+  float* mmin;
+  uint8_t* mim;
+  float* a_o;   // nullable
+  float* pc;    // nullable
+  float* amax;  // nullable
+};
+
+// W_n^j = exp(-2 pi i j / n), j < n, cached per (device, n); nullptr on failure.
+const float2* twiddle_table(int n);
+
+size_t fields_workspace_bytes(int B, int H, int W, int S, int O);
+int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, const FieldsOutputs& out,
+               void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace r2

@@ -1,0 +1,509 @@
+// Brute-force nearest-neighbour matching on the 5th-gen tensor cores.
+//
+// Replaces ref: pkg/src/rift2/matcher.py:67-148 (_group, _min_over_row_groups,
+// match_nn).  The reference ranks reference descriptors r for a target
+// descriptor t by |r|^2 - 2 r.t on unit float64 vectors, i.e. by the cosine
+// c_r.c_t / (|c_r| |c_t|) of the integer count vectors.  Here:
+//
+//   k_match_gemm  D = C_tgt . C_ref^T on fp16 counts (exact: counts <= 256,
+//                 dots < 2^24) with tcgen05.mma (M=128 tgt rows, N=128 ref
+//                 columns, K=224 in 14 steps) into a double-buffered TMEM
+//                 accumulator; operands staged by TMA (128B swizzle); one
+//                 warp produces, one warp issues MMA, four epilogue warps
+//                 tcgen05.ld the tile and keep a running exact argmax per
+//                 target row (fp32 screen, integer D^2 q comparison inside a
+//                 1e-5 window, ties to the smallest reference keypoint id).
+//   k_match_index per pair: target variant groups, reference keypoint ranges
+//   k_match_combine per target keypoint: best over its variants and over the
+//                 column splits (exact 128-bit comparison), then the exact
+//                 float64 distance of the winner (ref: matcher.py:137-141)
+//   k_match_sort  per pair: order by (dist, ref, tgt) (ref: matcher.py:143-146)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "match.h"
+#include "sort.cuh"
+
+namespace r2 {
+
+namespace {
+
+constexpr int BM = 128;            // target rows per CTA (UMMA M)
+constexpr int BN = 128;            // reference columns per tile (UMMA N)
+constexpr int BK = 64;             // fp16 elements per 128-byte swizzle atom
+constexpr int KBOX = 4;            // K boxes of 64 -> 256 >= 224
+constexpr int TILE_BYTES = BM * BK * 2;        // 16 KB per box
+constexpr int OPER_BYTES = KBOX * TILE_BYTES;  // 64 KB per operand tile
+constexpr int STAGES = 2;
+constexpr int GEMM_THREADS = 192;
+constexpr int SMEM_GEMM = OPER_BYTES * (1 + STAGES) + 1024 + 256;
+
+struct Part {
+  int D;      // integer dot product
+  int q;      // reference squared norm
+  int kp;     // reference keypoint id (-1: none)
+  float s;    // screening score D / |c_r|
+};
+
+// ------------------------------------------------------------ PTX helpers
+R2_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+R2_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+R2_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+R2_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+R2_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+R2_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)) : "memory");
+}
+R2_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+R2_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128-byte swizzled operand descriptor (8-row core groups 1024 B apart)
+R2_DEV uint64_t smem_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3fff);
+  d |= (uint64_t)1 << 16;                 // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // stride byte offset
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: f16 x f16 -> f32, both K-major, M=128, N=128
+constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+R2_DEV void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      :: "r"(tmem_d), "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate) : "memory");
+}
+R2_DEV void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"(smem_u32(bar)) : "memory");
+}
+
+R2_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// exact "a beats b" for candidates of the same target row: D_a/|c_a| > D_b/|c_b|
+R2_DEV int cmp_exact(float Da, int qa, float Db, int qb) {
+  const unsigned long long da = (unsigned long long)Da, db = (unsigned long long)Db;
+  const unsigned long long l = da * da * (unsigned long long)qb;
+  const unsigned long long r = db * db * (unsigned long long)qa;
+  return l > r ? 1 : (l < r ? -1 : 0);
+}
+
+struct GemmParams {
+  const int32_t* sqnorm;
+  const int32_t* kp;
+  const int32_t* count;
+  const int32_t* ref_block;
+  const int32_t* tgt_block;
+  int cap, splits;
+  Part* part;   // [n_pairs][cap][splits]
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+k_match_gemm(const __grid_constant__ CUtensorMap tmap, GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + OPER_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OPER_BYTES * (1 + STAGES));
+  uint64_t* full = bars;                 // [STAGES]
+  uint64_t* empty = bars + STAGES;       // [STAGES]
+  uint64_t* a_full = bars + 2 * STAGES;
+  uint64_t* t_full = a_full + 1;         // [2]
+  uint64_t* t_empty = t_full + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  float* s_inv = reinterpret_cast<float*>(tmem_slot + 4);   // [4 warps][BN]   (placed after bars)
+
+  const int pair = blockIdx.y;
+  const int split = blockIdx.x % p.splits;
+  const int mt = blockIdx.x / p.splits;
+  const int rb = p.ref_block[pair], tb = p.tgt_block[pair];
+  const int n_t = p.count[tb], n_r = p.count[rb];
+  if (mt * BM >= n_t) return;
+  const int n_tiles_all = (n_r + BN - 1) / BN;
+  const int per = (n_tiles_all + p.splits - 1) / p.splits;
+  const int nt0 = split * per;
+  const int nt1 = min(n_tiles_all, nt0 + per);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Part* out = p.part + ((size_t)pair * p.cap) * p.splits;
+  if (nt0 >= nt1) {
+    // empty split: publish "no candidate" for this tile's rows
+    for (int r = threadIdx.x; r < BM; r += blockDim.x) {
+      const int row = mt * BM + r;
+      if (row < n_t) out[(size_t)row * p.splits + split] = Part{0, 1, -1, -1.f};
+    }
+    return;
+  }
+  const int ntiles = nt1 - nt0;
+  const int rowA = tb * p.cap + mt * BM;
+  const int rowB0 = rb * p.cap;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(a_full, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" :: "r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer
+      mbar_expect_tx(a_full, OPER_BYTES);
+      for (int kb = 0; kb < KBOX; ++kb) tma_load_2d(sA + kb * TILE_BYTES, &tmap, kb * BK, rowA, a_full);
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[s], OPER_BYTES);
+        const int rowB = rowB0 + (nt0 + i) * BN;
+        for (int kb = 0; kb < KBOX; ++kb)
+          tma_load_2d(sB + s * OPER_BYTES + kb * TILE_BYTES, &tmap, kb * BK, rowB, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer (single thread)
+      mbar_wait(a_full, 0);
+      const uint32_t a_base = smem_u32(sA);
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % STAGES, acc = i & 1;
+        mbar_wait(&full[s], (i / STAGES) & 1);
+        mbar_wait(&t_empty[acc], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t b_base = smem_u32(sB + s * OPER_BYTES);
+        const uint32_t d = tmem + acc * BN;
+#pragma unroll
+        for (int ks = 0; ks < 14; ++ks) {
+          const uint32_t off = (ks >> 2) * TILE_BYTES + (ks & 3) * 32;
+          mma_f16(d, smem_desc(a_base + off), smem_desc(b_base + off), ks > 0 ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);
+        mma_commit(&t_full[acc]);
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    const int row_loc = q * 32 + lane;
+    const int row = mt * BM + row_loc;
+    float* inv = s_inv + (warp - 2) * BN;
+    float best = -1.f, bestD = 0.f;
+    int bestq = 1, bestcol = -1;
+    for (int i = 0; i < ntiles; ++i) {
+      const int acc = i & 1;
+      const int col0 = (nt0 + i) * BN;
+      // stage 1/|c_r| of this tile's columns (per warp)
+      for (int j = lane; j < BN; j += 32) {
+        const int c = col0 + j;
+        inv[j] = c < n_r ? rsqrtf((float)__ldg(&p.sqnorm[(size_t)rb * p.cap + c])) : 0.f;
+      }
+      __syncwarp();
+      mbar_wait(&t_full[acc], (i >> 1) & 1);
+      tc_fence_after();
+      const int nvalid = min(BN, n_r - col0);
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, v);
+        if (ch * 32 >= nvalid) continue;
+        float cm = -2.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float s = (ch * 32 + j < nvalid) ? v[j] * inv[ch * 32 + j] : -2.f;
+          cm = fmaxf(cm, s);
+        }
+        if (cm >= best * (1.f - 1e-5f)) {
+          for (int j = 0; j < 32; ++j) {
+            const int jj = ch * 32 + j;
+            if (jj >= nvalid) break;
+            const float s = v[j] * inv[jj];
+            if (s > best * (1.f + 1e-5f) || bestcol < 0) {
+              best = s; bestD = v[j]; bestcol = col0 + jj;
+              bestq = __ldg(&p.sqnorm[(size_t)rb * p.cap + bestcol]);
+            } else if (s >= best * (1.f - 1e-5f)) {
+              const int qq = __ldg(&p.sqnorm[(size_t)rb * p.cap + col0 + jj]);
+              if (cmp_exact(v[j], qq, bestD, bestq) > 0) {
+                best = s; bestD = v[j]; bestcol = col0 + jj; bestq = qq;
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[acc]);
+    }
+    if (row < n_t) {
+      Part r;
+      r.D = (int)bestD;
+      r.q = bestq;
+      r.kp = bestcol >= 0 ? __ldg(&p.kp[(size_t)rb * p.cap + bestcol]) : -1;
+      r.s = best;
+      out[(size_t)row * p.splits + split] = r;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" :: "r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------ index / combine
+struct IdxWs {
+  int* gstart;   // [n_pairs][cap] target group start
+  int* ng;       // [n_pairs]
+  int* rstart;   // [n_pairs][cap] by reference kp id
+  int* rend;     // [n_pairs][cap]
+};
+
+__global__ void __launch_bounds__(1024) k_match_index(MatchArgs a, IdxWs w) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base, s_tot;
+  const int pair = blockIdx.x;
+  const int tb = a.tgt_block[pair], rb = a.ref_block[pair];
+  const int n_t = a.count[tb], n_r = a.count[rb];
+  const int* tk = a.kp + (size_t)tb * a.cap;
+  const int* rk = a.kp + (size_t)rb * a.cap;
+  int* gs = w.gstart + (size_t)pair * (a.cap + 1);
+  int* rs = w.rstart + (size_t)pair * a.cap;
+  int* re = w.rend + (size_t)pair * a.cap;
+  for (int i = threadIdx.x; i < n_r; i += blockDim.x) {
+    if (i == 0 || rk[i] != rk[i - 1]) rs[rk[i]] = i;
+    if (i == n_r - 1 || rk[i + 1] != rk[i]) re[rk[i]] = i + 1;
+  }
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < n_t; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const bool st = i < n_t && (i == 0 || tk[i] != tk[i - 1]);
+    const unsigned bal = __ballot_sync(0xffffffffu, st);
+    if (lane == 0) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { const int t = s_warp[q]; s_warp[q] = run; run += t; }
+      s_tot = run;
+    }
+    __syncthreads();
+    if (st) gs[s_base + s_warp[wid] + __popc(bal & ((1u << lane) - 1u))] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += s_tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { w.ng[pair] = s_base; gs[s_base] = n_t; }
+}
+
+// a beats b across target variants: Da^2 q_rb q_tb > Db^2 q_ra q_ta (128-bit)
+R2_DEV int cmp_cross(const Part& a, int qta, const Part& b, int qtb) {
+  const unsigned __int128 l = (unsigned __int128)((unsigned long long)a.D * (unsigned long long)a.D) *
+                              ((unsigned long long)b.q * (unsigned long long)qtb);
+  const unsigned __int128 r = (unsigned __int128)((unsigned long long)b.D * (unsigned long long)b.D) *
+                              ((unsigned long long)a.q * (unsigned long long)qta);
+  return l > r ? 1 : (l < r ? -1 : 0);
+}
+
+__global__ void __launch_bounds__(256) k_match_combine(MatchArgs a, IdxWs w, const Part* __restrict__ part,
+                                                       int splits, K128* __restrict__ keys) {
+  const int pair = blockIdx.y;
+  const int warp_g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int ng = w.ng[pair];
+  if (warp_g >= ng) return;
+  const int tb = a.tgt_block[pair], rb = a.ref_block[pair];
+  const int* gs = w.gstart + (size_t)pair * (a.cap + 1);
+  const int t0 = gs[warp_g], t1 = gs[warp_g + 1];
+  const Part* pp = part + (size_t)pair * a.cap * splits;
+  // best candidate over variants x splits (all lanes compute the same; cheap)
+  Part best{0, 1, -1, -1.f};
+  int best_qt = 1;
+  for (int t = t0; t < t1; ++t) {
+    const int qt = a.sqnorm[(size_t)tb * a.cap + t];
+    for (int s = 0; s < splits; ++s) {
+      const Part c = pp[(size_t)t * splits + s];
+      if (c.kp < 0) continue;
+      if (best.kp < 0) { best = c; best_qt = qt; continue; }
+      const int r = cmp_cross(c, qt, best, best_qt);
+      if (r > 0 || (r == 0 && c.kp < best.kp)) { best = c; best_qt = qt; }
+    }
+  }
+  const int tkp = a.kp[(size_t)tb * a.cap + t0];
+  double dmin = 0.0;
+  if (best.kp >= 0) {
+    const int r0 = w.rstart[(size_t)pair * a.cap + best.kp], r1 = w.rend[(size_t)pair * a.cap + best.kp];
+    dmin = 1e300;
+    for (int r = r0; r < r1; ++r) {
+      const double ir = 1.0 / sqrt((double)a.sqnorm[(size_t)rb * a.cap + r]);
+      const __half* cr = a.counts + ((size_t)rb * a.cap + r) * a.stride;
+      for (int t = t0; t < t1; ++t) {
+        const double it = 1.0 / sqrt((double)a.sqnorm[(size_t)tb * a.cap + t]);
+        const __half* ct = a.counts + ((size_t)tb * a.cap + t) * a.stride;
+        double acc = 0.0;
+        for (int i = lane; i < a.dim; i += 32) {
+          // reference vectors are c / sqrt(c.c) in float64 (ref: descriptor.py:161-164)
+          const double dv = (double)__half2float(cr[i]) * ir - (double)__half2float(ct[i]) * it;
+          acc += dv * dv;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        dmin = fmin(dmin, acc);
+      }
+    }
+    dmin = sqrt(dmin);
+  }
+  if (lane == 0) {
+    K128 k;
+    k.hi = (unsigned long long)__double_as_longlong(dmin);
+    k.lo = ((unsigned long long)(unsigned)best.kp << 32) | (unsigned)tkp;
+    keys[(size_t)pair * a.cap + warp_g] = k;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_match_sort(MatchArgs a, IdxWs w, K128* __restrict__ keys,
+                                                     K128* __restrict__ tmp) {
+  extern __shared__ K128 s_keys[];
+  const int pair = blockIdx.x;
+  const int ng = w.ng[pair];
+  K128* k = keys + (size_t)pair * a.cap;
+  sort_keys_block(k, tmp + (size_t)pair * a.cap, ng, s_keys);
+  const int n = min(ng, a.tgt_kp_cap);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const size_t o = (size_t)pair * a.tgt_kp_cap + i;
+    a.out_dist[o] = __longlong_as_double((long long)k[i].hi);
+    a.out_ref[o] = (int32_t)(k[i].lo >> 32);
+    a.out_tgt[o] = (int32_t)(k[i].lo & 0xffffffffull);
+  }
+  if (threadIdx.x == 0) a.out_count[pair] = ng;
+}
+
+// ------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+constexpr int kMaxSplits = 8;
+
+struct MatchWs {
+  size_t off_part, off_gstart, off_ng, off_rstart, off_rend, off_keys, off_tmp, total;
+};
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+MatchWs plan_match(int n_pairs, int cap) {
+  MatchWs p{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = al(off + bytes); return o; };
+  p.off_part = take((size_t)n_pairs * cap * kMaxSplits * sizeof(Part));
+  p.off_gstart = take((size_t)n_pairs * (cap + 1) * sizeof(int));
+  p.off_ng = take((size_t)n_pairs * sizeof(int));
+  p.off_rstart = take((size_t)n_pairs * cap * sizeof(int));
+  p.off_rend = take((size_t)n_pairs * cap * sizeof(int));
+  p.off_keys = take((size_t)n_pairs * cap * sizeof(K128));
+  p.off_tmp = take((size_t)n_pairs * cap * sizeof(K128));
+  p.total = off;
+  return p;
+}
+
+}  // namespace
+
+size_t match_workspace_bytes(int n_pairs, int cap, int tgt_kp_cap) {
+  (void)tgt_kp_cap;
+  return plan_match(n_pairs, cap > 0 ? cap : 1).total;
+}
+
+int match_run(const MatchArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int n_blocks = a.n_blocks;
+  const MatchWs p = plan_match(a.n_pairs, a.cap);
+  if (ws_bytes < p.total) return 1;
+  if (a.stride != 224 && a.stride != 256) return 2;   // TMA boxes cover K <= 256
+  char* w = static_cast<char*>(ws);
+  Part* part = reinterpret_cast<Part*>(w + p.off_part);
+  IdxWs iw{reinterpret_cast<int*>(w + p.off_gstart), reinterpret_cast<int*>(w + p.off_ng),
+           reinterpret_cast<int*>(w + p.off_rstart), reinterpret_cast<int*>(w + p.off_rend)};
+  K128* keys = reinterpret_cast<K128*>(w + p.off_keys);
+  K128* tmp = reinterpret_cast<K128*>(w + p.off_tmp);
+
+  auto encode = get_encode();
+  if (!encode) return 3;
+  CUtensorMap tmap;
+  cuuint64_t dims[2] = {(cuuint64_t)a.stride, (cuuint64_t)n_blocks * a.cap};
+  cuuint64_t strides[1] = {(cuuint64_t)a.stride * 2};
+  cuuint32_t box[2] = {BK, BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a.counts), dims, strides,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return 3;
+
+  const int m_tiles = (a.cap + BM - 1) / BM;
+  int splits = (2 * 148 + a.n_pairs * m_tiles - 1) / (a.n_pairs * m_tiles);
+  splits = splits < 1 ? 1 : (splits > kMaxSplits ? kMaxSplits : splits);
+  GemmParams gp{a.sqnorm, a.kp, a.count, a.ref_block, a.tgt_block, a.cap, splits, part};
+  cudaFuncSetAttribute(k_match_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_GEMM + 4 * BN * 4);
+  dim3 grid(m_tiles * splits, a.n_pairs);
+  k_match_gemm<<<grid, GEMM_THREADS, SMEM_GEMM + 4 * BN * 4, st>>>(tmap, gp);
+  k_match_index<<<a.n_pairs, 1024, 0, st>>>(a, iw);
+  {
+    dim3 g2((a.cap + 7) / 8, a.n_pairs);
+    k_match_combine<<<g2, 256, 0, st>>>(a, iw, part, splits, keys);
+  }
+  const size_t sort_smem = kSortChunk * sizeof(K128);
+  cudaFuncSetAttribute(k_match_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
+  k_match_sort<<<a.n_pairs, 1024, sort_smem, st>>>(a, iw, keys, tmp);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+}  // namespace r2

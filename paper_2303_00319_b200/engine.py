@@ -1,0 +1,168 @@
+"""Device-level stage calls: torch tensors in, torch tensors out.
+
+PyTorch is only the carrier here (device memory, streams); every stage is
+one call into the C ABI (include/rift2_b200.h), enqueued on the current
+torch stream.  Workspaces are cached per (device, stage) and grown on
+demand, so steady-state calls allocate nothing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from .errors import ParameterError
+
+DESC_STRIDE = 224      # 216-D descriptors padded to the tensor-core K tile
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class _Workspaces:
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, key: str, nbytes: int) -> torch.Tensor:
+        dev = torch.cuda.current_device()
+        buf = self._bufs.get((dev, key))
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=f"cuda:{dev}")
+            self._bufs[(dev, key)] = buf
+        return buf
+
+
+WORKSPACES = _Workspaces()
+
+
+def bank_c(bank) -> _lib.BankParamsC:
+    return _lib.BankParamsC(
+        int(bank.n_scales), int(bank.n_orient), float(bank.min_wavelength), float(bank.scale_mult),
+        float(bank.sigma_on_f), float(bank.orientation_spread or 0.0), float(bank.noise_k),
+        float(bank.spread_cutoff), float(bank.spread_gain))
+
+
+def fields(images: torch.Tensor, bank, extras: bool = False, ws_key: str = "fields", out=None):
+    """images (B, H, W) float32 CUDA -> dict(mmax, mmin, mim[, a_o, pc, amax])."""
+    lib = _lib.load(require_gpu=True)
+    if images.dim() != 3 or images.dtype != torch.float32 or not images.is_cuda:
+        raise ParameterError("images must be a (B, H, W) float32 CUDA tensor")
+    images = images.contiguous()
+    B, H, W = images.shape
+    p = bank_c(bank)
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_fields_workspace_size(B, H, W, ctypes.byref(p), ctypes.byref(nbytes)), "fields")
+    ws = WORKSPACES.get(ws_key, nbytes.value)
+    dev = images.device
+    if out is None:
+        out = dict(mmax=torch.empty((B, H, W), dtype=torch.float32, device=dev),
+                   mmin=torch.empty((B, H, W), dtype=torch.float32, device=dev),
+                   mim=torch.empty((B, H, W), dtype=torch.uint8, device=dev))
+        if extras:
+            O = int(bank.n_orient)
+            out["a_o"] = torch.empty((B, O, H, W), dtype=torch.float32, device=dev)
+            out["pc"] = torch.empty((B, O, H, W), dtype=torch.float32, device=dev)
+            out["amax"] = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+    rc = lib.rift2_fields(_ptr(images), B, H, W, ctypes.byref(p), _ptr(out["mmax"]), _ptr(out["mmin"]),
+                          _ptr(out["mim"]), _ptr(out.get("a_o")), _ptr(out.get("pc")), _ptr(out.get("amax")),
+                          _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "rift2_fields")
+    return out
+
+
+def detect(maps: torch.Tensor, threshold: float, max_points: int, margin: int, single_map: bool = False,
+           ws_key: str = "detect", out=None):
+    """maps (B, 2, H, W) [moment_min, moment_max] (or (B, 1, H, W) with
+    single_map) float32/float64 CUDA -> dict(x, y, response, kind, count)."""
+    lib = _lib.load(require_gpu=True)
+    maps = maps.contiguous()
+    B, _, H, W = maps.shape
+    K = int(max_points)
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_detect_workspace_size(B, H, W, K, ctypes.byref(nbytes)), "detect")
+    ws = WORKSPACES.get(ws_key, nbytes.value)
+    dev = maps.device
+    if out is None:
+        kk = max(K, 1)
+        out = dict(x=torch.empty((B, kk), dtype=torch.int32, device=dev),
+                   y=torch.empty((B, kk), dtype=torch.int32, device=dev),
+                   response=torch.empty((B, kk), dtype=torch.float64, device=dev),
+                   kind=torch.empty((B, kk), dtype=torch.uint8, device=dev),
+                   count=torch.empty((B,), dtype=torch.int32, device=dev))
+    fn = lib.rift2_detect_f64 if maps.dtype == torch.float64 else lib.rift2_detect_f32
+    if maps.dtype not in (torch.float32, torch.float64):
+        raise ParameterError("maps must be float32 or float64")
+    rc = fn(_ptr(maps), B, H, W, float(threshold), K, int(margin), 1 if single_map else 0,
+            _ptr(out["x"]), _ptr(out["y"]), _ptr(out["response"]), _ptr(out["kind"]), _ptr(out["count"]),
+            _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "rift2_detect")
+    return out
+
+
+MODE_CODE = {"plain": 0, "ring": 1, "rift2": 2}
+
+
+def describe(mim: torch.Tensor, kp_x: torch.Tensor, kp_y: torch.Tensor, kp_count: torch.Tensor,
+             n_orient: int, patch: int = 96, grid: int = 6, ratio: float = 0.8, rotate: bool = True,
+             mode: str = "rift2", capacity: int | None = None, ws_key: str = "describe", out=None):
+    """mim (B, H, W) uint8 CUDA, keypoints (B, S) int32 -> dict(counts (B, cap,
+    224) f16, sqnorm, kp, variant, count, skipped)."""
+    lib = _lib.load(require_gpu=True)
+    B, H, W = mim.shape
+    S = kp_x.shape[1]
+    per = {"plain": 1, "ring": n_orient, "rift2": 2}[mode]
+    cap = capacity if capacity is not None else max(S * per, 1)
+    dim = grid * grid * n_orient
+    stride = DESC_STRIDE if dim <= DESC_STRIDE else int(math.ceil(dim / 32) * 32)
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_describe_workspace_size(B, S, grid, n_orient, ctypes.byref(nbytes)), "describe")
+    ws = WORKSPACES.get(ws_key, nbytes.value)
+    dev = mim.device
+    if out is None:
+        out = dict(counts=torch.zeros((B, cap, stride), dtype=torch.float16, device=dev),
+                   sqnorm=torch.zeros((B, cap), dtype=torch.int32, device=dev),
+                   kp=torch.zeros((B, cap), dtype=torch.int32, device=dev),
+                   variant=torch.zeros((B, cap), dtype=torch.uint8, device=dev),
+                   count=torch.empty((B,), dtype=torch.int32, device=dev),
+                   skipped=torch.empty((B,), dtype=torch.int32, device=dev))
+    rc = lib.rift2_describe(_ptr(mim.contiguous()), B, H, W, int(n_orient), _ptr(kp_x), _ptr(kp_y),
+                            _ptr(kp_count), S, int(patch), int(grid), float(ratio), 1 if rotate else 0,
+                            MODE_CODE[mode], _ptr(out["counts"]), out["counts"].shape[2], out["counts"].shape[1],
+                            _ptr(out["sqnorm"]), _ptr(out["kp"]), _ptr(out["variant"]), _ptr(out["count"]),
+                            _ptr(out["skipped"]), _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "rift2_describe")
+    return out
+
+
+def match(desc: dict, dim: int, ref_block: torch.Tensor, tgt_block: torch.Tensor, tgt_kp_cap: int,
+          ws_key: str = "match", out=None):
+    """Nearest reference keypoint for every target keypoint of each pair.
+    desc: the describe() dict (blocks = its batch); blocks given as int32
+    CUDA tensors.  -> dict(ref, tgt, dist, count) sorted by (dist, ref, tgt)."""
+    lib = _lib.load(require_gpu=True)
+    counts = desc["counts"]
+    n_blocks, cap, stride = counts.shape
+    P = ref_block.numel()
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_match_workspace_size(P, cap, tgt_kp_cap, ctypes.byref(nbytes)), "match")
+    ws = WORKSPACES.get(ws_key, nbytes.value)
+    dev = counts.device
+    kc = max(int(tgt_kp_cap), 1)
+    if out is None:
+        out = dict(ref=torch.empty((P, kc), dtype=torch.int32, device=dev),
+                   tgt=torch.empty((P, kc), dtype=torch.int32, device=dev),
+                   dist=torch.empty((P, kc), dtype=torch.float64, device=dev),
+                   count=torch.empty((P,), dtype=torch.int32, device=dev))
+    rc = lib.rift2_match(_ptr(counts), _ptr(desc["sqnorm"]), _ptr(desc["kp"]), _ptr(desc["count"]), n_blocks,
+                         stride, cap, int(dim), P, _ptr(ref_block), _ptr(tgt_block), kc, _ptr(out["ref"]),
+                         _ptr(out["tgt"]), _ptr(out["dist"]), _ptr(out["count"]), _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "rift2_match")
+    return out
