@@ -80,9 +80,11 @@ int32_t rift2_fields(const float* images, int32_t batch, int32_t height, int32_t
  * Replaces ref: pkg/src/rift2/detector.py:140-155 (detect_keypoints) for a
  * batch; with single_map != 0 it replaces detector.py:87-113 (detect_fast)
  * on `maps` alone (kind 0).
- *   maps         [batch][2][height][width] (moment_min, moment_max), either
- *                float32 (rift2_detect_f32) or float64 (rift2_detect_f64);
- *                must be finite (the Python layer checks, ref: detector.py:96-97)
+ *   min_maps     [batch][height][width] moment_min (corners, kind 0)
+ *   max_maps     [batch][height][width] moment_max (edges, kind 1; unused
+ *                with single_map); float32 (rift2_detect_f32) or float64
+ *                (rift2_detect_f64), finite (the Python layer checks,
+ *                ref: detector.py:96-97)
  *   kp_x, kp_y   [batch][max_points] int32 out
  *   kp_response  [batch][max_points] float64 out
  *   kp_kind      [batch][max_points] uint8 out (0 corner, 1 edge)
@@ -90,12 +92,12 @@ int32_t rift2_fields(const float* images, int32_t batch, int32_t height, int32_t
  * Keypoints are ordered by (-response, y, x), corner before edge on ties. */
 int32_t rift2_detect_workspace_size(int32_t batch, int32_t height, int32_t width, int32_t max_points,
                                     size_t* bytes);
-int32_t rift2_detect_f32(const float* maps, int32_t batch, int32_t height, int32_t width,
-                         double threshold, int32_t max_points, int32_t border_margin, int32_t single_map,
+int32_t rift2_detect_f32(const float* min_maps, const float* max_maps, int32_t batch, int32_t height,
+                         int32_t width, double threshold, int32_t max_points, int32_t border_margin, int32_t single_map,
                          int32_t* kp_x, int32_t* kp_y, double* kp_response, uint8_t* kp_kind,
                          int32_t* kp_count, void* workspace, size_t workspace_bytes, void* stream);
-int32_t rift2_detect_f64(const double* maps, int32_t batch, int32_t height, int32_t width,
-                         double threshold, int32_t max_points, int32_t border_margin, int32_t single_map,
+int32_t rift2_detect_f64(const double* min_maps, const double* max_maps, int32_t batch, int32_t height,
+                         int32_t width, double threshold, int32_t max_points, int32_t border_margin, int32_t single_map,
                          int32_t* kp_x, int32_t* kp_y, double* kp_response, uint8_t* kp_kind,
                          int32_t* kp_count, void* workspace, size_t workspace_bytes, void* stream);
 
@@ -142,6 +144,18 @@ int32_t rift2_match(const void* desc_counts, const int32_t* desc_sqnorm, const i
                     int32_t dim, int32_t n_pairs, const int32_t* ref_block, const int32_t* tgt_block,
                     int32_t tgt_kp_capacity, int32_t* out_ref, int32_t* out_tgt, double* out_dist,
                     int32_t* out_count, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Generic variant of stage 4 for arbitrary float64 descriptor vectors (not
+ * integer histograms), e.g. unit vectors built by the caller: the
+ * reference's own key |r|^2 - 2 r.t in float64 (ref: matcher.py:125-135).
+ * Rows must be grouped by keypoint id (stable order, ref: matcher.py:67-79).
+ *   ref_vec [n_ref][dim], tgt_vec [n_tgt][dim] float64 device
+ *   out_* [n_tgt] (one entry per target keypoint), sorted (dist, ref, tgt). */
+int32_t rift2_match_vectors_workspace_size(int32_t n_ref, int32_t n_tgt, size_t* bytes);
+int32_t rift2_match_vectors(const double* ref_vec, const int32_t* ref_kp, int32_t n_ref, const double* tgt_vec,
+                            const int32_t* tgt_kp, int32_t n_tgt, int32_t dim, int32_t* out_ref, int32_t* out_tgt,
+                            double* out_dist, int32_t* out_count, void* workspace, size_t workspace_bytes,
+                            void* stream);
 
 #ifdef __cplusplus
 }

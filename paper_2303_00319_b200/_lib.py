@@ -37,10 +37,10 @@ _SIGNATURES = {
     "rift2_fields": (_c_int, [_c_p, _c_int, _c_int, _c_int, ctypes.POINTER(BankParamsC), _c_p, _c_p, _c_p,
                               _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "rift2_detect_workspace_size": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
-    "rift2_detect_f32": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_d, _c_int, _c_int, _c_int, _c_p, _c_p,
-                                  _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
-    "rift2_detect_f64": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_d, _c_int, _c_int, _c_int, _c_p, _c_p,
-                                  _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "rift2_detect_f32": (_c_int, [_c_p, _c_p, _c_int, _c_int, _c_int, _c_d, _c_int, _c_int, _c_int, _c_p,
+                                  _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "rift2_detect_f64": (_c_int, [_c_p, _c_p, _c_int, _c_int, _c_int, _c_d, _c_int, _c_int, _c_int, _c_p,
+                                  _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "rift2_describe_workspace_size": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
     "rift2_describe": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p, _c_int, _c_int, _c_int,
                                 _c_d, _c_int, _c_int, _c_p, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p,
@@ -48,6 +48,9 @@ _SIGNATURES = {
     "rift2_match_workspace_size": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
     "rift2_match": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p,
                              _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "rift2_match_vectors_workspace_size": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_sz)]),
+    "rift2_match_vectors": (_c_int, [_c_p, _c_p, _c_int, _c_p, _c_p, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p,
+                                     _c_p, _c_sz, _c_p]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -116,18 +116,18 @@ const float2* twiddle_table(int n) {
 }  // namespace r2
 
 template <class T>
-static int32_t detect_impl(const T* maps, int32_t batch, int32_t height, int32_t width, double threshold,
+static int32_t detect_impl(const T* mins, const T* maxs, int32_t batch, int32_t height, int32_t width, double threshold,
                            int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
                            int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
                            void* workspace, size_t workspace_bytes, void* stream) {
   if (!(threshold > 0)) return fail(RIFT2_BAD_ARGUMENT, "FAST threshold must be positive");
   if (batch < 1 || height < 1 || width < 1 || max_points < 0 || border_margin < 0)
     return fail(RIFT2_BAD_ARGUMENT, "bad detect dimensions");
-  if (!maps || !kp_count || !workspace || (max_points > 0 && (!kp_x || !kp_y || !kp_response || !kp_kind)))
+  if (!mins || (!single_map && !maxs) || !kp_count || !workspace || (max_points > 0 && (!kp_x || !kp_y || !kp_response || !kp_kind)))
     return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
   r2::DetectArgs a{batch, height, width, threshold, max_points, border_margin, single_map != 0,
                    kp_x, kp_y, kp_response, kp_kind, kp_count};
-  int32_t rc = r2::detect_run(maps, a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  int32_t rc = r2::detect_run(mins, maxs, a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
   return map_internal(rc, "rift2_detect");
 }
 
@@ -185,19 +185,21 @@ int32_t rift2_detect_workspace_size(int32_t batch, int32_t height, int32_t width
   return RIFT2_OK;
 }
 
-int32_t rift2_detect_f32(const float* maps, int32_t batch, int32_t height, int32_t width, double threshold,
+int32_t rift2_detect_f32(const float* min_maps, const float* max_maps, int32_t batch, int32_t height,
+                         int32_t width, double threshold,
                          int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
                          int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
                          void* workspace, size_t workspace_bytes, void* stream) {
-  return detect_impl(maps, batch, height, width, threshold, max_points, border_margin, single_map, kp_x, kp_y,
+  return detect_impl(min_maps, max_maps, batch, height, width, threshold, max_points, border_margin, single_map, kp_x, kp_y,
                      kp_response, kp_kind, kp_count, workspace, workspace_bytes, stream);
 }
 
-int32_t rift2_detect_f64(const double* maps, int32_t batch, int32_t height, int32_t width, double threshold,
+int32_t rift2_detect_f64(const double* min_maps, const double* max_maps, int32_t batch, int32_t height,
+                         int32_t width, double threshold,
                          int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
                          int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
                          void* workspace, size_t workspace_bytes, void* stream) {
-  return detect_impl(maps, batch, height, width, threshold, max_points, border_margin, single_map, kp_x, kp_y,
+  return detect_impl(min_maps, max_maps, batch, height, width, threshold, max_points, border_margin, single_map, kp_x, kp_y,
                      kp_response, kp_kind, kp_count, workspace, workspace_bytes, stream);
 }
 
@@ -259,6 +261,26 @@ int32_t rift2_match(const void* desc_counts, const int32_t* desc_sqnorm, const i
                   out_dist, out_count};
   int32_t rc = r2::match_run(a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
   return map_internal(rc, "rift2_match");
+}
+
+int32_t rift2_match_vectors_workspace_size(int32_t n_ref, int32_t n_tgt, size_t* bytes) {
+  if (n_ref < 1 || n_tgt < 1 || !bytes) return fail(RIFT2_BAD_ARGUMENT, "descriptor lists must be nonempty");
+  *bytes = r2::match_vectors_workspace_bytes(n_ref, n_tgt);
+  return RIFT2_OK;
+}
+
+int32_t rift2_match_vectors(const double* ref_vec, const int32_t* ref_kp, int32_t n_ref, const double* tgt_vec,
+                            const int32_t* tgt_kp, int32_t n_tgt, int32_t dim, int32_t* out_ref, int32_t* out_tgt,
+                            double* out_dist, int32_t* out_count, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  if (n_ref < 1 || n_tgt < 1) return fail(RIFT2_BAD_ARGUMENT, "descriptor lists must be nonempty");
+  if (dim < 1 || !ref_vec || !ref_kp || !tgt_vec || !tgt_kp || !out_ref || !out_tgt || !out_dist || !out_count ||
+      !workspace)
+    return fail(RIFT2_BAD_ARGUMENT, "bad match_vectors arguments");
+  int32_t rc = r2::match_vectors_run(ref_vec, ref_kp, n_ref, tgt_vec, tgt_kp, n_tgt, dim, out_ref, out_tgt,
+                                     out_dist, out_count, workspace, workspace_bytes,
+                                     static_cast<cudaStream_t>(stream));
+  return map_internal(rc, "rift2_match_vectors");
 }
 
 }  // extern "C"

@@ -42,15 +42,23 @@ R2_DEV double ord_val(unsigned long long k) {
   return __longlong_as_double((long long)b);
 }
 
+// plane = image * nm + map; map 0 = moment_min (corners), 1 = moment_max (edges)
+template <class T>
+R2_DEV const T* plane_ptr(const T* mins, const T* maxs, int plane, int nm, size_t n) {
+  const int b = plane / nm, m = plane % nm;
+  return (m == 0 ? mins : maxs) + (size_t)b * n;
+}
+
 __global__ void k_init(unsigned long long* mm, unsigned* cnt, int planes) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < planes) { mm[2 * i] = ~0ull; mm[2 * i + 1] = 0ull; cnt[i] = 0; }
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k_minmax(const T* __restrict__ maps, size_t n, unsigned long long* mm) {
+__global__ void __launch_bounds__(256) k_minmax(const T* __restrict__ mins, const T* __restrict__ maxs, int nm,
+                                                size_t n, unsigned long long* mm) {
   const int plane = blockIdx.y;
-  const T* p = maps + (size_t)plane * n;
+  const T* p = plane_ptr(mins, maxs, plane, nm, n);
   unsigned long long lo = ~0ull, hi = 0ull;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const unsigned long long k = ord_key((double)p[i]);
@@ -93,7 +101,7 @@ R2_DEV void arc_extrema(const T (&v)[16], T& A, T& B) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ maps, int H, int W,
+__global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, const T* __restrict__ maxs, int H, int W,
                                                   const unsigned long long* __restrict__ mm, double thr,
                                                   int margin, int nm, K128* __restrict__ cand,
                                                   unsigned* __restrict__ cnt, size_t cap) {
@@ -101,7 +109,7 @@ __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ maps, in
   __shared__ double ss[kSc][kSc + 1];
   const int plane = blockIdx.z;
   const int kind = nm == 2 ? (plane & 1) : 0;
-  const T* p = maps + (size_t)plane * H * W;
+  const T* p = plane_ptr(mins, maxs, plane, nm, (size_t)H * W);
   const double lo = ord_val(mm[2 * plane]);
   const double hi = ord_val(mm[2 * plane + 1]);
   const double span = hi - lo;
@@ -413,7 +421,7 @@ DetectPlan plan_detect(int B, int H, int W, int K) {
 }
 
 template <class T>
-int detect_impl(const T* maps, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   const DetectPlan p = plan_detect(a.B, a.H, a.W, a.max_points);
   if (ws_bytes < p.total) return 1;
   char* w = static_cast<char*>(ws);
@@ -437,11 +445,11 @@ int detect_impl(const T* maps, const DetectArgs& a, void* ws, size_t ws_bytes, c
   const size_t n = (size_t)a.H * a.W;
   {
     dim3 grid((unsigned)min((size_t)32, (n + 255) / 256), planes);
-    k_minmax<T><<<grid, 256, 0, st>>>(maps, n, mm);
+    k_minmax<T><<<grid, 256, 0, st>>>(mins, maxs, nm, n, mm);
   }
   {
     dim3 grid((a.W + kTile - 1) / kTile, (a.H + kTile - 1) / kTile, planes);
-    k_fast_nms<T><<<grid, 256, 0, st>>>(maps, a.H, a.W, mm, a.threshold, a.margin, nm, cand, cnt, p.cap);
+    k_fast_nms<T><<<grid, 256, 0, st>>>(mins, maxs, a.H, a.W, mm, a.threshold, a.margin, nm, cand, cnt, p.cap);
   }
   const size_t sort_smem = kSortChunk * sizeof(K128);
   cudaFuncSetAttribute(k_select_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
@@ -462,12 +470,14 @@ size_t detect_workspace_bytes(int B, int H, int W, int max_points) {
   return plan_detect(B, H, W, max_points).total;
 }
 
-int detect_run(const float* maps, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
-  return detect_impl(maps, a, ws, ws_bytes, st);
+int detect_run(const float* mins, const float* maxs, const DetectArgs& a, void* ws, size_t ws_bytes,
+               cudaStream_t st) {
+  return detect_impl(mins, maxs, a, ws, ws_bytes, st);
 }
 
-int detect_run(const double* maps, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
-  return detect_impl(maps, a, ws, ws_bytes, st);
+int detect_run(const double* mins, const double* maxs, const DetectArgs& a, void* ws, size_t ws_bytes,
+               cudaStream_t st) {
+  return detect_impl(mins, maxs, a, ws, ws_bytes, st);
 }
 
 }  // namespace r2

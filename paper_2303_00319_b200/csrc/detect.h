@@ -19,7 +19,10 @@ struct DetectArgs {
 };
 
 size_t detect_workspace_bytes(int B, int H, int W, int max_points);
-int detect_run(const float* maps, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
-int detect_run(const double* maps, const DetectArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
+// min_maps / max_maps: [B][H][W]; with single_map only min_maps is read (kind 0)
+int detect_run(const float* min_maps, const float* max_maps, const DetectArgs& a, void* ws, size_t ws_bytes,
+               cudaStream_t st);
+int detect_run(const double* min_maps, const double* max_maps, const DetectArgs& a, void* ws, size_t ws_bytes,
+               cudaStream_t st);
 
 }  // namespace r2

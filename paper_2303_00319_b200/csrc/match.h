@@ -25,4 +25,10 @@ struct MatchArgs {
 size_t match_workspace_bytes(int n_pairs, int cap, int tgt_kp_cap);
 int match_run(const MatchArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
 
+// generic float64 descriptor vectors (rows grouped by keypoint id)
+size_t match_vectors_workspace_bytes(int nr, int nt);
+int match_vectors_run(const double* R, const int* rkp, int nr, const double* T, const int* tkp, int nt, int dim,
+                      int* out_ref, int* out_tgt, double* out_dist, int* out_count, void* ws, size_t ws_bytes,
+                      cudaStream_t st);
+
 }  // namespace r2

@@ -78,13 +78,17 @@ def fields(images: torch.Tensor, bank, extras: bool = False, ws_key: str = "fiel
     return out
 
 
-def detect(maps: torch.Tensor, threshold: float, max_points: int, margin: int, single_map: bool = False,
-           ws_key: str = "detect", out=None):
-    """maps (B, 2, H, W) [moment_min, moment_max] (or (B, 1, H, W) with
-    single_map) float32/float64 CUDA -> dict(x, y, response, kind, count)."""
+def detect(mins: torch.Tensor, maxs: torch.Tensor | None, threshold: float, max_points: int, margin: int,
+           single_map: bool = False, ws_key: str = "detect", out=None):
+    """mins / maxs (B, H, W) moment_min / moment_max (maxs unused with
+    single_map), float32 or float64 CUDA -> dict(x, y, response, kind, count)."""
     lib = _lib.load(require_gpu=True)
-    maps = maps.contiguous()
-    B, _, H, W = maps.shape
+    mins = mins.contiguous()
+    maxs = mins if (single_map or maxs is None) else maxs.contiguous()
+    if maxs.dtype != mins.dtype or maxs.shape != mins.shape:
+        raise ParameterError("moment maps differ in shape or dtype")
+    B, H, W = mins.shape
+    maps = mins
     K = int(max_points)
     nbytes = ctypes.c_size_t()
     _lib.check(lib.rift2_detect_workspace_size(B, H, W, K, ctypes.byref(nbytes)), "detect")
@@ -100,7 +104,7 @@ def detect(maps: torch.Tensor, threshold: float, max_points: int, margin: int, s
     fn = lib.rift2_detect_f64 if maps.dtype == torch.float64 else lib.rift2_detect_f32
     if maps.dtype not in (torch.float32, torch.float64):
         raise ParameterError("maps must be float32 or float64")
-    rc = fn(_ptr(maps), B, H, W, float(threshold), K, int(margin), 1 if single_map else 0,
+    rc = fn(_ptr(mins), _ptr(maxs), B, H, W, float(threshold), K, int(margin), 1 if single_map else 0,
             _ptr(out["x"]), _ptr(out["y"]), _ptr(out["response"]), _ptr(out["kind"]), _ptr(out["count"]),
             _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "rift2_detect")
@@ -139,6 +143,25 @@ def describe(mim: torch.Tensor, kp_x: torch.Tensor, kp_y: torch.Tensor, kp_count
                             _ptr(out["sqnorm"]), _ptr(out["kp"]), _ptr(out["variant"]), _ptr(out["count"]),
                             _ptr(out["skipped"]), _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "rift2_describe")
+    return out
+
+
+def match_vectors(ref_vec: torch.Tensor, ref_kp: torch.Tensor, tgt_vec: torch.Tensor, tgt_kp: torch.Tensor,
+                  ws_key: str = "match_vectors"):
+    """Generic float64 descriptor vectors (rows grouped by keypoint id)."""
+    lib = _lib.load(require_gpu=True)
+    nr, dim = ref_vec.shape
+    nt = tgt_vec.shape[0]
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_match_vectors_workspace_size(nr, nt, ctypes.byref(nbytes)), "match_vectors")
+    ws = WORKSPACES.get(ws_key, nbytes.value)
+    dev = ref_vec.device
+    out = dict(ref=torch.empty(nt, dtype=torch.int32, device=dev), tgt=torch.empty(nt, dtype=torch.int32, device=dev),
+               dist=torch.empty(nt, dtype=torch.float64, device=dev), count=torch.empty(1, dtype=torch.int32, device=dev))
+    rc = lib.rift2_match_vectors(_ptr(ref_vec), _ptr(ref_kp), nr, _ptr(tgt_vec), _ptr(tgt_kp), nt, dim,
+                                 _ptr(out["ref"]), _ptr(out["tgt"]), _ptr(out["dist"]), _ptr(out["count"]),
+                                 _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "rift2_match_vectors")
     return out
 
 

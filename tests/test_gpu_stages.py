@@ -104,7 +104,7 @@ def _kp_equal(got, tag, g):
 
 def _detect_gpu(eng, maps, thr, cap, margin, single):
     t = torch.as_tensor(np.asarray(maps, dtype=np.float64)).cuda()
-    out = eng.detect(t, thr, cap, margin, single_map=single)
+    out = eng.detect(t[:, 0], None if single else t[:, 1], thr, cap, margin, single_map=single)
     torch.cuda.synchronize()
     return {k: v.cpu().numpy() for k, v in out.items()}
 

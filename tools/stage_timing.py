@@ -39,8 +39,7 @@ def main():
         ev[0].record()
         f = engine.fields(x, bank)
         ev[1].record()
-        maps = torch.stack([f["mmin"], f["mmax"]], 1)
-        k = engine.detect(maps, 0.001, 5000, 48)
+        k = engine.detect(f["mmin"], f["mmax"], 0.001, 5000, 48)
         ev[2].record()
         d = engine.describe(f["mim"], k["x"], k["y"], k["count"], 6)
         ev[3].record()
