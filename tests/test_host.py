@@ -1,0 +1,115 @@
+"""CPU-side checks: the C-ABI library loads and exports every symbol
+include/rift2_b200.h declares (no compute call without a GPU), the Python
+boundary mirrors the reference's types/validation, the BASELINE generator
+is deterministic, and the product path refuses to run without CUDA."""
+
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rift2_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:int32_t|const char\*)\s+(rift2_\w+)\(", text, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2303_00319_b200 import _lib
+    if not os.path.exists(_lib.library_path()):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2303_00319_b200", "csrc"), "-j8"], check=True)
+    return _lib.load()
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2303_00319_b200 import _lib
+    names = _declared()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.EXPORTED)
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.library_path()], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}$", out, re.M), f"{n} not exported with C linkage"
+
+
+def test_version_and_errors_without_gpu(lib):
+    import ctypes
+    from paper_2303_00319_b200 import _lib
+    assert lib.rift2_version() == 100
+    # argument validation needs no GPU and maps onto the reference's errors
+    p = _lib.BankParamsC(0, 6, 3.0, 2.1, 0.55, 0.0, 2.0, 0.5, 10.0)
+    n = ctypes.c_size_t()
+    rc = lib.rift2_fields_workspace_size(1, 64, 64, ctypes.byref(p), ctypes.byref(n))
+    assert rc == 1 and b"n_scales" in lib.rift2_last_error()
+    p = _lib.BankParamsC(4, 6, 3.0, 2.1, 0.55, 0.0, 2.0, 0.5, 10.0)
+    assert lib.rift2_fields_workspace_size(1, 8, 64, ctypes.byref(p), ctypes.byref(n)) == 1
+    assert lib.rift2_fields_workspace_size(1, 64, 77, ctypes.byref(p), ctypes.byref(n)) == 2   # prime 7, 11
+    assert lib.rift2_fields_workspace_size(2, 1024, 1024, ctypes.byref(p), ctypes.byref(n)) == 0
+    assert n.value > 2 * 24 * 1024 * 1024 * 8
+    with pytest.raises(Exception):
+        _lib.check(1, "x")
+
+
+def test_bank_params_validation():
+    from paper_2303_00319_b200 import BankParams, ParameterError
+    for kw in ({"n_scales": 0}, {"n_orient": 1}, {"min_wavelength": 1.0}, {"scale_mult": 1.0},
+               {"sigma_on_f": 0.0}, {"sigma_on_f": 1.0}):
+        with pytest.raises(ParameterError):
+            BankParams(**kw)
+    assert np.allclose(BankParams().wavelengths(), [3.0, 6.3, 13.23, 27.783])
+
+
+def test_config_mirror():
+    from paper_2303_00319_b200 import ConfigError, RiftConfig, apply_overrides, parse_config_text
+    cfg = parse_config_text("scale_mult = 1.6\n# c\nsigma_on_f=0.75\nrotate_patch = off\n")
+    assert cfg.scale_mult == 1.6 and cfg.sigma_on_f == 0.75 and cfg.rotate_patch is False
+    assert apply_overrides(cfg, ["mode=ring"]).mode == "ring"
+    for bad in ("nope = 1", "mode = x", "patch_size = 95"):
+        with pytest.raises(ConfigError):
+            parse_config_text(bad)
+    assert RiftConfig().bank_params().n_orient == 6
+
+
+def test_errors_hierarchy():
+    from paper_2303_00319_b200 import ConfigError, FormatError, ParameterError, RiftError
+    for e in (ParameterError, FormatError, ConfigError):
+        assert issubclass(e, RiftError) and issubclass(e, ValueError)
+
+
+def test_generator_deterministic():
+    from paper_2303_00319_b200 import synth
+    a1, b1, t1 = synth.make_pair(128, seed=9)
+    a2, b2, t2 = synth.make_pair(128, seed=9)
+    assert np.array_equal(a1, a2) and np.array_equal(b1, b2) and t1.theta_deg == t2.theta_deg
+    assert a1.min() == 0.0 and a1.max() == 1.0
+    # ground truth maps image-1 points onto image 2 (noise-free check)
+    a = synth.blob_field(127, seed=1)
+    m = synth.similarity(127, 90.0, 1.0, (3.0, -2.0))     # quarter turn, integer shift: exact samples
+    b = synth.warp(a, m)
+    tr = synth.PairTruth(90.0, 1.0, (3.0, -2.0), False, 1.0, 0, 127, m)
+    for p in ([40.0, 50.0], [70.0, 20.0]):
+        q = tr.apply(np.array([p]))[0]
+        assert abs(b[int(round(q[1])), int(round(q[0]))] - a[int(p[1]), int(p[0])]) < 1e-12
+
+
+def test_product_path_refuses_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2303_00319_b200 import RiftError, compute_fields
+    with pytest.raises((RiftError, RuntimeError, AssertionError)):
+        compute_fields(np.zeros((64, 64)))
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2303_00319_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            assert "oracle" not in open(os.path.join(pkg, fn)).read().replace("oracle/", ""), fn
