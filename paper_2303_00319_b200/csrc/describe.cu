@@ -167,7 +167,17 @@ __global__ void __launch_bounds__(kT) k_desc_plan(const uint8_t* __restrict__ mi
   cell_counts(c, [&](int i, int j) { return (int)__ldg(&m[(size_t)(y0 + i) * c.W + x0 + j]); }, cnt);
   unsigned short* bo = base + ((size_t)b * a.kp_stride + k) * c.cells * c.O;
   for (int i = threadIdx.x; i < c.cells * c.O; i += kT) bo[i] = (unsigned short)cnt[i];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // patch histogram (ref: mim.py:58-66) = sum of the cell counts, warp-parallel
+    unsigned hs[16];
+    for (int v = 0; v < c.O; ++v) {
+      unsigned s = 0;
+      for (int q = threadIdx.x; q < c.cells; q += 32) s += cnt[q * c.O + v];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      hs[v] = s;
+    }
+    if (threadIdx.x != 0) return;
     KpPlan p{0, 0, {0, 0}};
     if (c.mode == 0) { p.ndesc = 1; p.pick[0] = 1; }
     else if (c.mode == 1) { p.ndesc = c.O; }
@@ -176,11 +186,7 @@ __global__ void __launch_bounds__(kT) k_desc_plan(const uint8_t* __restrict__ mi
       // (float64, inclusive), runner-up ties to the bin cyclically closest
       // after the peak.
       double hist[16];
-      for (int v = 0; v < c.O; ++v) {
-        unsigned s = 0;
-        for (int q = 0; q < c.cells; ++q) s += cnt[q * c.O + v];
-        hist[v] = (double)s;
-      }
+      for (int v = 0; v < c.O; ++v) hist[v] = (double)hs[v];
       int pk = 0;
       for (int v = 1; v < c.O; ++v) if (hist[v] > hist[pk]) pk = v;
       double rv = -1.0;

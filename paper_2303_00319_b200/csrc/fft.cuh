@@ -234,7 +234,16 @@ R2_DEV void fft_fast(float2 (&v)[32], float2* buf, const float2* __restrict__ tw
 }
 
 // Synchronisation objects for a group of G threads.
-struct SyncWarp { R2_DEV void operator()() const { __syncwarp(); } };
+struct SyncWarp {
+  unsigned mask;
+  R2_DEV void operator()() const { __syncwarp(mask); }
+};
+// lanes of the G-thread group (G <= 32) containing this thread
+R2_DEV unsigned group_mask(int G) {
+  if (G >= 32) return 0xffffffffu;
+  const unsigned base = (threadIdx.x & 31) / G * G;
+  return ((1u << G) - 1u) << base;
+}
 struct SyncNamed {
   int id, n;
   R2_DEV void operator()() const { named_sync(id, n); }

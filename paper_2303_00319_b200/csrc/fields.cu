@@ -5,18 +5,24 @@
 // (build_mim) with a two-pass 2-D FFT whose inter-pass planes are the only
 // per-filter HBM traffic:
 //
-//   K1 rows_fwd   real rows -> half spectrum rows (two rows per complex FFT)
-//   K2 cols       column FFT once per column, then for each of the S*O filters
-//                 multiply by the analytically generated transfer function and
-//                 inverse-FFT the column (mirror columns from Hermitian symmetry)
-//   K3a rows_amp0 inverse row FFT of the S=0 planes -> |response| + histogram
-//   K4  median    exact np.median of each scale-0 amplitude plane (radix select)
-//   K3b rows_pc   inverse row FFTs of all planes, fused phase congruency,
-//                 moments, orientation amplitude sums and MIM argmax.
+//   K1  rows_fwd  real rows -> half-spectrum rows (two rows per complex FFT)
+//   K2  cols      column FFT once per column; then, per filter and with no
+//                 CTA barrier, multiply by the analytically generated
+//                 transfer function and inverse-FFT the column (mirror
+//                 columns from Hermitian symmetry), stored from registers
+//   K3a rows_amp0 inverse row FFT of the scale-0 planes -> scale-0 responses
+//                 (kept for K3b), |response| and a radix histogram
+//   K4  median    exact np.median of each scale-0 amplitude plane
+//   K3b rows_pc   inverse row FFTs of scales 1..S-1 (scale 0 re-loaded),
+//                 fused phase congruency, moments, orientation amplitude
+//                 sums and MIM argmax.
 //
-// Layouts (all row-major, batch-major):
-//   image  [B][H][W] f32          P  [B][H][Wh] c64 (Wh = W/2+1)
-//   Q      [B][S*O][H][W] c64     amp0 [B][O][H*W] f32
+// Layouts (batch-major):
+//   image [B][H][W] f32               P   [B][H][Wh] c64 (Wh = W/2+1), row-major
+//   Q     [B][S*O][Hp/4][W][4] c64    4-row column tiles: element (y, x) at
+//                                     ((y>>2)*W + x)*4 + (y&3), Hp = H rounded up to 4
+//   R0    [B][O][H][W] c64            scale-0 responses, row-major
+//   amp0  [B][O][H*W] f32
 //   outputs M, m [B][H][W] f32, MIM [B][H][W] u8, optional a_o/pc [B][O][H][W], amax [B][H][W]
 #include "fft.cuh"
 #include "fields.h"
@@ -24,19 +30,25 @@
 namespace r2 {
 
 constexpr int kThreads = 256;
+// K2 CTA size: two warps per direct+mirror column pair keeps smem per CTA low
+// enough for three CTAs per SM
+template <int G>
+struct ColsCfg { static constexpr int T = G == 0 ? 256 : (G >= 64 ? 2 * G : 128); };
 constexpr int kHistBins = 4096;   // float bits >> 19 of a non-negative float
 constexpr int kMaxS = 8;
 constexpr int kMaxO = 16;
+constexpr float kPi = 3.14159265358979f;
+constexpr float kTwoPi = 6.28318530717959f;
 
 struct FieldsConst {
-  int B, H, W, Wh, S, O;
+  int B, H, W, Wh, Hp, S, O;
   float log_lambda[kMaxS];     // ln(lambda_s) = -ln(f0_s)
-  float inv_den_r;             // 1 / (2 ln(sigma_on_f)^2)
-  float inv_den_a;             // 1 / (2 sigma_theta^2)
+  float a2;                    // log2(e) / (2 ln(sigma_on_f)^2)
+  float b2;                    // log2(e) / (2 sigma_theta^2)
   float ang[kMaxO], cos_a[kMaxO], sin_a[kMaxO];
   float spread_cutoff, spread_gain, inv_sm1;
   float lp_lncut;              // ln(0.45)
-  float inv_hw;
+  float log2_inv_hw;           // log2(1 / (H*W)): the inverse-FFT scale folded into the exponent
   double thr_factor;           // T = median * thr_factor
   const float2* tw_w;          // W_W^j
   const float2* tw_h;          // W_H^j
@@ -45,6 +57,16 @@ struct FieldsConst {
 
 // numpy.fft.fftfreq(n)[k]
 R2_DEV float fftfreq(int k, int n) { return (float)(k < (n + 1) / 2 ? k : k - n) / (float)n; }
+
+// 4-row column-tile plane index: a 32-byte sector holds rows 4j..4j+3 of one
+// column, so a column FFT's stores fill whole sectors
+R2_DEV size_t tq(int y, int x, int W) { return ((size_t)(y >> 2) * W + x) * 4 + (y & 3); }
+
+R2_DEV float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // ------------------------------------------------------------------ K1 ---
 // Two real rows y0, y1 as one complex FFT z = r0 + i r1, then split:
@@ -70,7 +92,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_fwd(const float* __restrict__
       const int x = t + G * m;
       v[m] = make_float2(v0 ? __ldg(&im[(size_t)y0 * W + x]) : 0.f, v1 ? __ldg(&im[(size_t)y1 * W + x]) : 0.f);
     }
-    SyncWarp sw;
+    SyncWarp sw{group_mask(G)};
     SyncNamed sn{1 + g, G};
     if constexpr (G <= 32) fft_fast<G>(v, buf, c.tw_w, t, sw);
     else fft_fast<G>(v, buf, c.tw_w, t, sn);
@@ -102,58 +124,61 @@ __global__ void __launch_bounds__(kThreads) k_rows_fwd(const float* __restrict__
 }
 
 // ------------------------------------------------------------------ K2 ---
-// Transfer function of filter (s, o) at a spectrum sample (ref: loggabor.py:131-159):
-//   lowpass(r) * exp(-ln(r/f0)^2 / (2 ln(sigma)^2)) * exp(-dtheta^2 / (2 sigma_theta^2)),
-// folded into one exp; geo = (ln r, lowpass/(H*W) (0 at DC), theta, theta_mirror).
-R2_DEV float transfer(const FieldsConst& c, float4 geo, bool mirror, int s, int o) {
-  const float dr = geo.x + c.log_lambda[s];
-  float d = (mirror ? geo.w : geo.z) - c.ang[o];
-  if (d > 3.14159265358979f) d -= 6.28318530717959f;
-  if (d < -3.14159265358979f) d += 6.28318530717959f;
-  return geo.y * __expf(-(dr * dr * c.inv_den_r + d * d * c.inv_den_a));
-}
-
-R2_DEV float4 geometry(const FieldsConst& c, int ky, int kx) {
+// Spectrum geometry of column kx (ref: loggabor.py:122-159, r = hypot(fx, fy),
+// theta = atan2(fy, fx), lowpass 1 / (1 + (r/0.45)^30), DC zeroed):
+//   lnr, L2 = log2(lowpass / (H*W)) (-inf at DC), theta of the direct column.
+// The mirror column W - kx has the same r and theta_m = +-pi - theta.
+R2_DEV void geometry(const FieldsConst& c, int ky, int kx, float& lnr, float& L2, float& th) {
   const float fy = fftfreq(ky, c.H);
   const float fx = fftfreq(kx, c.W);
-  const float fxm = fftfreq(kx == 0 ? 0 : c.W - kx, c.W);
-  const float r2 = fx * fx + fy * fy;
-  float4 g;
   if (ky == 0 && kx == 0) {
-    g = make_float4(0.f, 0.f, 0.f, 0.f);
-  } else {
-    const float lnr = 0.5f * logf(r2);
-    // 1 / (1 + (r / 0.45)^30)
-    const float lp = 1.f / (1.f + expf(30.f * (lnr - c.lp_lncut)));
-    g = make_float4(lnr, lp * c.inv_hw, atan2f(fy, fx), atan2f(fy, fxm));
+    lnr = 0.f;
+    L2 = -INFINITY;
+    th = 0.f;
+    return;
   }
-  return g;
+  lnr = 0.5f * logf(fx * fx + fy * fy);
+  const float lp = 1.f / (1.f + expf(30.f * (lnr - c.lp_lncut)));
+  L2 = log2f(lp) + c.log2_inv_hw;
+  th = atan2f(fy, fx);
+}
+
+// transfer of filter (s, o) as exp2(L2 - a2 (ln r - ln f0)^2 - b2 dtheta^2)
+R2_DEV float transfer(float lnr, float L2, float th, float ll, float ang, float a2, float b2) {
+  float d = fabsf(th - ang);
+  d = d > kPi ? kTwoPi - d : d;
+  const float dr = lnr + ll;
+  return ex2(fmaf(d * d, -b2, fmaf(dr * dr, -a2, L2)));
 }
 
 template <int G>
-__global__ void __launch_bounds__(kThreads) k_cols(const float2* __restrict__ P, float2* __restrict__ Q,
+__global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k_cols(const float2* __restrict__ P, float2* __restrict__ Q,
                                                    const __grid_constant__ FieldsConst c) {
   extern __shared__ float2 sm[];
   const int H = c.H, W = c.W, Wh = c.Wh, F = c.S * c.O;
   const int b = blockIdx.y;
   const float2* Pb = P + (size_t)b * H * Wh;
+  float2* Qb = Q + (size_t)b * F * c.Hp * W;
   if constexpr (G > 0) {
     constexpr int N = 32 * G;        // == H
-    constexpr int NG = kThreads / G;
-    constexpr int CG = NG / 2;       // direct columns per CTA (plus mirrors)
+    constexpr int NG = ColsCfg<G>::T / G;
+    // A CTA owns direct columns kx0..kx0+CG-1 and their mirrors W-kx.
+    constexpr int CG = NG / 2;
+    constexpr int NS = CG;           // spectrum columns held
     constexpr int PL = padded_len(N);
-    float2* S = sm;                                        // [CG][PL]
-    float4* geo = reinterpret_cast<float4*>(sm + CG * PL); // [CG][N]
-    float2* bufs = sm + CG * PL + 2 * CG * N;              // [NG][PL]
+    float2* S = sm;                                              // [NS][PL]
+    float* glnr = reinterpret_cast<float*>(sm + NS * PL);        // [NS][N]
+    float* gL2 = glnr + NS * N;                                  // [NS][N]
+    float* gth = gL2 + NS * N;                                   // [NS][N]
+    float2* bufs = reinterpret_cast<float2*>(gth + NS * N);      // [NG][PL]
     const int g = threadIdx.x / G, t = threadIdx.x % G;
     float2* buf = bufs + g * PL;
     const int kx0 = blockIdx.x * CG;
-    SyncWarp sw;
+    SyncWarp sw{group_mask(G)};
     SyncNamed sn{1 + g, G};
-    auto gsync = [&]() { if constexpr (G <= 32) sw(); else sn(); };
     float2 v[32];
     // 1. forward column FFTs of the half spectrum
-    if (g < CG) {
+    if (g < NS) {
       const int kx = kx0 + g;
       const bool ok = kx < Wh;
 #pragma unroll
@@ -162,44 +187,53 @@ __global__ void __launch_bounds__(kThreads) k_cols(const float2* __restrict__ P,
 #pragma unroll
       for (int m = 0; m < 32; ++m) S[g * PL + pad32(t + G * m)] = v[m];
     }
-    // 2. spectrum geometry of the CG columns (shared with their mirrors)
-    for (int i = threadIdx.x; i < CG * N; i += kThreads) {
-      const int cc = i / N, ky = i % N;
-      geo[i] = geometry(c, ky, min(kx0 + cc, Wh - 1));
+    // 2. spectrum geometry of the NS columns
+    for (int i = threadIdx.x; i < NS * N; i += ColsCfg<G>::T) {
+      float lnr, L2, th;
+      geometry(c, i % N, min(kx0 + i / N, Wh - 1), lnr, L2, th);
+      glnr[i] = lnr;
+      gL2[i] = L2;
+      gth[i] = th;
     }
     __syncthreads();
-    // 3. per filter: multiply + inverse column FFT, then coalesced row-segment stores
-    const int cc = g % CG, mir = g / CG;
+    // 3. every group independently: per filter multiply + inverse column FFT,
+    //    stored straight from registers into the 4-row column-tile plane
+    const int mir = g / CG;
+    const int cc = g % CG;           // local spectrum column
     const int kx = kx0 + cc;
-    const bool valid = kx < Wh && (mir == 0 || (kx != 0 && 2 * kx != W));
+    const bool valid = mir == 0 ? kx < Wh : (kx != 0 && 2 * kx < W);
+    if (!valid) return;              // whole group idles; no CTA barrier follows
+    const int xo = mir ? W - kx : kx;
+    const float2* Sc = S + cc * PL;
+    const float* Ln = glnr + cc * N;
+    const float* Lp = gL2 + cc * N;
+    const float* Th = gth + cc * N;
+    const float a2 = c.a2, b2 = c.b2;
     for (int f = 0; f < F; ++f) {
       const int s = f / c.O, o = f % c.O;
+      const float ll = c.log_lambda[s], ang = c.ang[o];
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const int ky = t + G * m;
+        float th = Th[ky];
         float2 sv;
-        if (mir) sv = cconj(S[cc * PL + pad32(ky == 0 ? 0 : N - ky)]);
-        else sv = S[cc * PL + pad32(ky)];
-        const float gval = valid ? transfer(c, geo[cc * N + ky], mir, s, o) : 0.f;
-        v[m] = make_float2(sv.x * gval, -sv.y * gval);   // conj for the inverse
+        if (mir) {
+          sv = Sc[pad32((N - ky) & (N - 1))];       // S(-ky, kx) = conj S(ky, W - kx)
+          th = (ky < N / 2 ? kPi : -kPi) - th;
+        } else {
+          sv = Sc[pad32(ky)];
+          sv.y = -sv.y;
+        }
+        const float gv = transfer(Ln[ky], Lp[ky], th, ll, ang, a2, b2);
+        v[m] = make_float2(sv.x * gv, sv.y * gv);   // conj(spectrum * G) for the inverse
       }
       if constexpr (G <= 32) fft_fast<G>(v, buf, c.tw_h, t, sw); else fft_fast<G>(v, buf, c.tw_h, t, sn);
-      gsync();
+      float2* Qf = Qb + (size_t)f * c.Hp * W;
 #pragma unroll
-      for (int m = 0; m < 32; ++m) buf[pad32(t + G * m)] = cconj(v[m]);
-      __syncthreads();
-      float2* Qf = Q + ((size_t)b * F + f) * H * W;
-      for (int i = threadIdx.x; i < 2 * CG * N; i += kThreads) {
-        const int mm = i / (CG * N), rem = i % (CG * N);
-        const int y = rem / CG, col = rem % CG;
-        const int kxc = kx0 + col;
-        const bool ok = kxc < Wh && (mm == 0 || (kxc != 0 && 2 * kxc != W));
-        if (ok) {
-          const int xo = mm ? W - kxc : kxc;
-          Qf[(size_t)y * W + xo] = bufs[(mm * CG + col) * PL + pad32(y)];
-        }
+      for (int m = 0; m < 32; ++m) {
+        const int y = t + G * m;
+        Qf[tq(y, xo, W)] = cconj(v[m]);
       }
-      __syncthreads();
     }
   } else {
     // generic sizes: whole CTA per transform, 4 columns per CTA
@@ -220,20 +254,29 @@ __global__ void __launch_bounds__(kThreads) k_cols(const float2* __restrict__ P,
     }
     for (int f = 0; f < F; ++f) {
       const int s = f / c.O, o = f % c.O;
-      float2* Qf = Q + ((size_t)b * F + f) * H * W;
+      float2* Qf = Qb + (size_t)f * c.Hp * W;
       for (int job = 0; job < 2 * CG; ++job) {
         const int cc = job % CG, mir = job / CG;
         const int kx = kx0 + cc;
         if (!(kx < Wh && (mir == 0 || (kx != 0 && 2 * kx != W)))) continue;
         for (int ky = threadIdx.x; ky < H; ky += blockDim.x) {
-          float2 sv = mir ? cconj(S[cc * PL + pad32(ky == 0 ? 0 : H - ky)]) : S[cc * PL + pad32(ky)];
-          const float gval = transfer(c, geometry(c, ky, kx), mir, s, o);
-          buf[pad32(ky)] = make_float2(sv.x * gval, -sv.y * gval);
+          float lnr, L2, th;
+          geometry(c, ky, kx, lnr, L2, th);
+          float2 sv;
+          if (mir) {
+            sv = S[cc * PL + pad32(ky == 0 ? 0 : H - ky)];
+            th = (2 * ky < H ? kPi : -kPi) - th;
+          } else {
+            sv = S[cc * PL + pad32(ky)];
+            sv.y = -sv.y;
+          }
+          const float gv = transfer(lnr, L2, th, c.log_lambda[s], c.ang[o], c.a2, c.b2);
+          buf[pad32(ky)] = make_float2(sv.x * gv, sv.y * gv);
         }
         __syncthreads();
         fft_generic(buf, scr, H, c.plan_h, c.tw_h, threadIdx.x, blockDim.x);
         const int xo = mir ? W - kx : kx;
-        for (int y = threadIdx.x; y < H; y += blockDim.x) Qf[(size_t)y * W + xo] = cconj(buf[pad32(y)]);
+        for (int y = threadIdx.x; y < H; y += blockDim.x) Qf[tq(y, xo, W)] = cconj(buf[pad32(y)]);
         __syncthreads();
       }
     }
@@ -241,37 +284,40 @@ __global__ void __launch_bounds__(kThreads) k_cols(const float2* __restrict__ P,
 }
 
 // ----------------------------------------------------------------- K3a ---
-// Scale-0 amplitudes of orientation blockIdx.y for a block of rows, with a
-// 4096-bin histogram of their float bits (radix-select level 1).
+// Scale-0 responses of orientation blockIdx.y for a block of rows: written
+// out (for K3b) with |response| and a 4096-bin histogram of its float bits
+// (radix-select level 1 of the median).
 template <int G>
-__global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict__ Q, float* __restrict__ amp0,
-                                                        unsigned* __restrict__ hist,
+__global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict__ Q, float2* __restrict__ R0,
+                                                        float* __restrict__ amp0, unsigned* __restrict__ hist,
                                                         const __grid_constant__ FieldsConst c) {
   extern __shared__ float2 sm[];
   const int H = c.H, W = c.W, F = c.S * c.O;
   const int o = blockIdx.y, b = blockIdx.z;
-  const float2* Qp = Q + ((size_t)b * F + o) * H * W;   // filter (s=0, o)
+  const float2* Qp = Q + ((size_t)b * F + o) * c.Hp * W;   // filter (s=0, o)
   float* A = amp0 + ((size_t)b * c.O + o) * H * W;
+  float2* Rp = R0 + ((size_t)b * c.O + o) * H * W;
   unsigned* sh;
   if constexpr (G > 0) {
-    constexpr int N = 32 * G, NG = kThreads / G, PL = padded_len(N);
+    constexpr int NG = kThreads / G, PL = padded_len(32 * G);
     sh = reinterpret_cast<unsigned*>(sm + NG * PL);
     for (int i = threadIdx.x; i < kHistBins; i += kThreads) sh[i] = 0;
     __syncthreads();
     const int g = threadIdx.x / G, t = threadIdx.x % G;
     float2* buf = sm + g * PL;
     const int y = blockIdx.x * NG + g;
-    const bool ok = y < H;
-    float2 v[32];
+    if (y < H) {
+      float2 v[32];
 #pragma unroll
-    for (int m = 0; m < 32; ++m) v[m] = ok ? cconj(Qp[(size_t)y * W + t + G * m]) : make_float2(0.f, 0.f);
-    SyncWarp sw;
-    SyncNamed sn{1 + g, G};
-    if constexpr (G <= 32) fft_fast<G>(v, buf, c.tw_w, t, sw); else fft_fast<G>(v, buf, c.tw_w, t, sn);
-    if (ok) {
+      for (int m = 0; m < 32; ++m) v[m] = cconj(Qp[tq(y, t + G * m, W)]);
+      SyncWarp sw{group_mask(G)};
+      SyncNamed sn{1 + g, G};
+      if constexpr (G <= 32) fft_fast<G>(v, buf, c.tw_w, t, sw); else fft_fast<G>(v, buf, c.tw_w, t, sn);
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
-        const float a = sqrtf(v[m].x * v[m].x + v[m].y * v[m].y);
+        const float2 z = cconj(v[m]);
+        const float a = sqrtf(z.x * z.x + z.y * z.y);
+        Rp[(size_t)y * W + t + G * m] = z;
         A[(size_t)y * W + t + G * m] = a;
         atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
       }
@@ -283,12 +329,13 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
     sh = reinterpret_cast<unsigned*>(sm + 2 * PL);
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) sh[i] = 0;
     const int y = blockIdx.x;
-    for (int x = threadIdx.x; x < W; x += blockDim.x) buf[pad32(x)] = cconj(Qp[(size_t)y * W + x]);
+    for (int x = threadIdx.x; x < W; x += blockDim.x) buf[pad32(x)] = cconj(Qp[tq(y, x, W)]);
     __syncthreads();
     fft_generic(buf, scr, W, c.plan_w, c.tw_w, threadIdx.x, blockDim.x);
     for (int x = threadIdx.x; x < W; x += blockDim.x) {
-      const float2 z = buf[pad32(x)];
+      const float2 z = cconj(buf[pad32(x)]);
       const float a = sqrtf(z.x * z.x + z.y * z.y);
+      Rp[(size_t)y * W + x] = z;
       A[(size_t)y * W + x] = a;
       atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
     }
@@ -303,12 +350,11 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
 // Exact median of each amp0 plane (ref: loggabor.py:222, np.median: mean of
 // the two middle order statistics for even counts).
 struct MedInfo {
-  unsigned bin[2];     // level-1 bins of ranks n/2-1 (or n/2) and n/2
+  unsigned bin[2];     // level-1 bins of ranks (n-1)/2 and n/2
   unsigned rank[2];    // ranks inside those bins
 };
 
 __device__ void block_exclusive_scan_1024(unsigned* data, int n, unsigned* tmp) {
-  // simple single-thread-per-chunk scan: n <= 4096, blockDim 1024
   const int tid = threadIdx.x, nth = blockDim.x;
   const int per = (n + nth - 1) / nth;
   unsigned s = 0;
@@ -330,7 +376,6 @@ __device__ void block_exclusive_scan_1024(unsigned* data, int n, unsigned* tmp) 
   __syncthreads();
 }
 
-// locate the bins holding the two middle ranks
 __global__ void __launch_bounds__(1024) k_med_bins(const unsigned* __restrict__ hist, MedInfo* __restrict__ info,
                                                    unsigned n) {
   __shared__ unsigned h[kHistBins];
@@ -348,10 +393,13 @@ __global__ void __launch_bounds__(1024) k_med_bins(const unsigned* __restrict__ 
   }
 }
 
-// gather the float bits of every value falling into one of the two bins
+// gather the float bits of every value falling into one of the two bins;
+// hits are staged per CTA and appended with one global atomic per CTA pass
 __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ amp0, const MedInfo* __restrict__ info,
                                                      unsigned* __restrict__ cand, unsigned* __restrict__ cnt,
                                                      unsigned n) {
+  __shared__ unsigned s_buf[4 * 256];
+  __shared__ unsigned s_n, s_base;
   const int plane = blockIdx.y;
   const unsigned b0 = info[plane].bin[0], b1 = info[plane].bin[1];
   const float* Ap = amp0 + (size_t)plane * n;
@@ -359,6 +407,8 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
   unsigned* out = cand + (size_t)plane * n;
   const unsigned n4 = (n + 3) / 4;
   for (unsigned base = blockIdx.x * blockDim.x; base < n4; base += gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
     const unsigned i = base + threadIdx.x;
     float4 q = make_float4(-1.f, -1.f, -1.f, -1.f);
     if (4 * i + 3 < n) q = A[i];
@@ -372,9 +422,13 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
     for (int e = 0; e < 4; ++e) {
       const unsigned bits = __float_as_uint(vals[e]);
       const bool hit = vals[e] >= 0.f && ((bits >> 19) == b0 || (bits >> 19) == b1);
-      const unsigned slot = agg_inc(&cnt[plane], hit);
-      if (hit) out[slot] = bits;
+      if (hit) s_buf[atomicAdd(&s_n, 1u)] = bits;
     }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_n) s_base = atomicAdd(&cnt[plane], s_n);
+    __syncthreads();
+    for (unsigned j = threadIdx.x; j < s_n; j += blockDim.x) out[s_base + j] = s_buf[j];
+    __syncthreads();
   }
 }
 
@@ -392,8 +446,7 @@ __global__ void __launch_bounds__(1024) k_med_final(const unsigned* __restrict__
   for (int q = 0; q < 2; ++q) {
     unsigned prefix = info[plane].bin[q];   // bits >> 19
     unsigned rank = info[plane].rank[q];
-    // level 2: bits 18..9, level 3: bits 8..0
-    const int shifts[2] = {9, 0};
+    const int shifts[2] = {9, 0};           // level 2: bits 18..9, level 3: bits 8..0
     const int widths[2] = {10, 9};
     for (int lv = 0; lv < 2; ++lv) {
       const int sh = shifts[lv], nb = 1 << widths[lv];
@@ -432,119 +485,146 @@ struct PcOut {
 
 template <int G>
 struct PcShape {
-  static constexpr int PIX = G == 0 ? 16 : ((32 * G > 1024) ? (32 * G) / kThreads : 4);
+  // pixels per thread: a CTA holds (up to) two rows
+  static constexpr int PIX = G == 0 ? 16 : (G == 128 ? 16 : (G >= 4 ? G / 4 : 1));
 };
 
+// One CTA per row pair (y0, y0+1).  Stage = `ops` orientations of `rr` rows;
+// its buffers (row, orientation, scale) are filled by FFT jobs (scales >= 1)
+// and plain loads of the K3a responses (scale 0), then the per-pixel phase
+// congruency (ref: loggabor.py:193-251) consumes them.
 template <int G>
-__global__ void __launch_bounds__(kThreads) k_rows_pc(const float2* __restrict__ Q, const float* __restrict__ thr,
-                                                      PcOut out, const __grid_constant__ FieldsConst c,
-                                                      int rows, int ops) {
+__global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restrict__ Q, const float2* __restrict__ R0,
+                                                      const float* __restrict__ thr, PcOut out,
+                                                      const __grid_constant__ FieldsConst c, int rr, int ops) {
   extern __shared__ float2 sm[];
   const int H = c.H, W = c.W, S = c.S, O = c.O, F = S * O;
   const int b = blockIdx.y;
-  const int y0 = blockIdx.x * rows;
+  const int y0 = 2 * blockIdx.x;
   constexpr int PIX = PcShape<G>::PIX;
   const int PL = padded_len(W);
-  const int nb = rows * S * ops;             // shared buffers per stage
-  const int npix = rows * W;
-  float acc_a[PIX], acc_b[PIX], acc_c[PIX], best[PIX];
-  int bidx[PIX];
-#pragma unroll
-  for (int i = 0; i < PIX; ++i) { acc_a[i] = acc_b[i] = acc_c[i] = 0.f; best[i] = -1.f; bidx[i] = 1; }
+  const int nb = rr * ops * S;
   const float* thr_b = thr + (size_t)b * O;
+  const float2* Qb = Q + (size_t)b * F * c.Hp * W;
+  const float2* Rb = R0 + (size_t)b * O * H * W;
 
-  for (int o0 = 0; o0 < O; o0 += ops) {
-    const int no = min(ops, O - o0);
-    // --- FFT jobs: (row r, orientation o0+oo, scale s) -> buffer j
-    if constexpr (G > 0) {
-      constexpr int NG = kThreads / G;
-      const int g = threadIdx.x / G, t = threadIdx.x % G;
-      SyncWarp sw;
-      SyncNamed sn{1 + g, G};
-      for (int j0 = 0; j0 < nb; j0 += NG) {
-        const int j = j0 + g;
-        const int r = j / (S * ops), rem = j % (S * ops), oo = rem / S, s = rem % S;
-        const int y = y0 + r;
-        const bool ok = j < nb && oo < no && y < H;
-        float2* buf = sm + (j < nb ? j : 0) * PL;
-        float2 v[32];
-        const float2* Qp = Q + (((size_t)b * F + s * O + o0 + oo) * H + (ok ? y : 0)) * W;
+  for (int rbase = 0; rbase < 2; rbase += rr) {
+    const int npix = rr * W;
+    float acc_a[PIX], acc_b[PIX], acc_c[PIX], best[PIX];
+    int bidx[PIX];
 #pragma unroll
-        for (int m = 0; m < 32; ++m) v[m] = ok ? cconj(Qp[t + G * m]) : make_float2(0.f, 0.f);
-        float2* xbuf = (j < nb) ? buf : sm + nb * PL + g * PL;   // spare scratch for idle groups
-        if constexpr (G <= 32) fft_fast<G>(v, xbuf, c.tw_w, t, sw); else fft_fast<G>(v, xbuf, c.tw_w, t, sn);
-        if constexpr (G <= 32) sw(); else sn();
-        if (j < nb) {
+    for (int i = 0; i < PIX; ++i) { acc_a[i] = acc_b[i] = acc_c[i] = 0.f; best[i] = -1.f; bidx[i] = 1; }
+    for (int o0 = 0; o0 < O; o0 += ops) {
+      const int no = min(ops, O - o0);
+      if constexpr (G > 0) {
+        constexpr int NG = kThreads / G;
+        const int g = threadIdx.x / G, t = threadIdx.x % G;
+        SyncWarp sw{group_mask(G)};
+        SyncNamed sn{1 + g, G};
+        for (int j = g; j < nb; j += NG) {
+          const int r = j / (ops * S), rem = j % (ops * S), oo = rem / S, s = rem % S;
+          const int y = y0 + rbase + r;
+          float2* buf = sm + j * PL;
+          if (oo >= no || y >= H) continue;
+          const int o = o0 + oo;
+          if (s == 0) {
+            const float2* Rp = Rb + ((size_t)o * H + y) * W;
+            float2 v[32];
 #pragma unroll
-          for (int m = 0; m < 32; ++m) buf[pad32(t + G * m)] = cconj(v[m]);
+            for (int m = 0; m < 32; ++m) v[m] = Rp[t + G * m];
+#pragma unroll
+            for (int m = 0; m < 32; ++m) buf[pad32(t + G * m)] = v[m];
+          } else {
+            const float2* Qp = Qb + (size_t)(s * O + o) * c.Hp * W;
+            float2 v[32];
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m] = cconj(Qp[tq(y, t + G * m, W)]);
+            if constexpr (G <= 32) fft_fast<G>(v, buf, c.tw_w, t, sw); else fft_fast<G>(v, buf, c.tw_w, t, sn);
+            if constexpr (G <= 32) sw(); else sn();
+#pragma unroll
+            for (int m = 0; m < 32; ++m) buf[pad32(t + G * m)] = cconj(v[m]);
+          }
+        }
+      } else {
+        float2* scr = sm + nb * PL;
+        for (int j = 0; j < nb; ++j) {
+          const int oo = j / S, s = j % S;
+          const int y = y0 + rbase;
+          if (oo >= no || y >= H) break;
+          const int o = o0 + oo;
+          float2* buf = sm + j * PL;
+          if (s == 0) {
+            const float2* Rp = Rb + ((size_t)o * H + y) * W;
+            for (int x = threadIdx.x; x < W; x += blockDim.x) buf[pad32(x)] = Rp[x];
+          } else {
+            const float2* Qp = Qb + (size_t)(s * O + o) * c.Hp * W;
+            for (int x = threadIdx.x; x < W; x += blockDim.x) buf[pad32(x)] = cconj(Qp[tq(y, x, W)]);
+            __syncthreads();
+            fft_generic(buf, scr, W, c.plan_w, c.tw_w, threadIdx.x, blockDim.x);
+            for (int x = threadIdx.x; x < W; x += blockDim.x) buf[pad32(x)] = cconj(buf[pad32(x)]);
+          }
         }
       }
-    } else {
-      float2* scr = sm + nb * PL;
-      for (int j = 0; j < nb; ++j) {
-        const int oo = j / S, s = j % S;
-        if (oo >= no) break;
-        float2* buf = sm + j * PL;
-        const float2* Qp = Q + (((size_t)b * F + s * O + o0 + oo) * H + y0) * W;
-        for (int x = threadIdx.x; x < W; x += blockDim.x) buf[pad32(x)] = cconj(Qp[x]);
-        __syncthreads();
-        fft_generic(buf, scr, W, c.plan_w, c.tw_w, threadIdx.x, blockDim.x);
-        for (int x = threadIdx.x; x < W; x += blockDim.x) buf[pad32(x)] = cconj(buf[pad32(x)]);
+      __syncthreads();
+      // --- per-pixel phase congruency for the orientations of this stage
+#pragma unroll
+      for (int i = 0; i < PIX; ++i) {
+        const int p = threadIdx.x + kThreads * i;
+        if (p >= npix) continue;
+        const int r = p / W, x = p % W;
+        const int y = y0 + rbase + r;
+        if (y >= H) continue;
+        for (int oo = 0; oo < no; ++oo) {
+          const int o = o0 + oo;
+          const float2* bb = sm + ((r * ops + oo) * S) * PL + pad32(x);
+          float2 z[kMaxS];
+          float se = 0.f, so = 0.f, sa = 0.f, mx = 0.f;
+#pragma unroll
+          for (int s = 0; s < kMaxS; ++s) {
+            if (s < S) {
+              z[s] = bb[s * PL];
+              const float a = sqrtf(z[s].x * z[s].x + z[s].y * z[s].y);
+              se += z[s].x; so += z[s].y; sa += a; mx = fmaxf(mx, a);
+            }
+          }
+          // fast-math division / exp: relative error ~1e-7, far inside the 1e-4 budget
+          const float ixe = __frcp_rn(sqrtf(se * se + so * so) + 1e-4f);
+          const float me = se * ixe, mo = so * ixe;
+          float en = 0.f;
+#pragma unroll
+          for (int s = 0; s < kMaxS; ++s)
+            if (s < S) en += z[s].x * me + z[s].y * mo - fabsf(z[s].x * mo - z[s].y * me);
+          en = fmaxf(en - thr_b[o], 0.f);
+          const float spread = (__fdividef(sa, mx + 1e-4f) - 1.f) * c.inv_sm1;
+          const float wgt = __frcp_rn(1.f + __expf(c.spread_gain * (c.spread_cutoff - spread)));
+          const float pc = __fdividef(wgt * en, sa + 1e-4f);
+          const float pcc = pc * c.cos_a[o], pcs = pc * c.sin_a[o];
+          acc_a[i] += pcc * pcc;
+          acc_b[i] += pcc * pcs;
+          acc_c[i] += pcs * pcs;
+          if (sa > best[i]) { best[i] = sa; bidx[i] = o + 1; }
+          const size_t po = (((size_t)b * O + o) * H + y) * W + x;
+          if (out.a_o) out.a_o[po] = sa;
+          if (out.pc) out.pc[po] = pc;
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
-    // --- per-pixel phase congruency for the orientations of this stage
 #pragma unroll
     for (int i = 0; i < PIX; ++i) {
       const int p = threadIdx.x + kThreads * i;
       if (p >= npix) continue;
       const int r = p / W, x = p % W;
-      if (y0 + r >= H) continue;
-      for (int oo = 0; oo < no; ++oo) {
-        const int o = o0 + oo;
-        const float2* bb = sm + ((r * ops + oo) * S) * PL + pad32(x);
-        float se = 0.f, so = 0.f, sa = 0.f, mx = 0.f;
-        for (int s = 0; s < S; ++s) {
-          const float2 z = bb[s * PL];
-          const float a = sqrtf(z.x * z.x + z.y * z.y);
-          se += z.x; so += z.y; sa += a; mx = fmaxf(mx, a);
-        }
-        const float xe = sqrtf(se * se + so * so) + 1e-4f;
-        const float me = se / xe, mo = so / xe;
-        float en = 0.f;
-        for (int s = 0; s < S; ++s) {
-          const float2 z = bb[s * PL];
-          en += z.x * me + z.y * mo - fabsf(z.x * mo - z.y * me);
-        }
-        en = fmaxf(en - thr_b[o], 0.f);
-        const float spread = (sa / (mx + 1e-4f) - 1.f) * c.inv_sm1;
-        const float wgt = 1.f / (1.f + expf(c.spread_gain * (c.spread_cutoff - spread)));
-        const float pc = wgt * en / (sa + 1e-4f);
-        const float pcc = pc * c.cos_a[o], pcs = pc * c.sin_a[o];
-        acc_a[i] += pcc * pcc;
-        acc_b[i] += pcc * pcs;
-        acc_c[i] += pcs * pcs;
-        if (sa > best[i]) { best[i] = sa; bidx[i] = o + 1; }
-        const size_t po = (((size_t)b * O + o) * H + (y0 + r)) * W + x;
-        if (out.a_o) out.a_o[po] = sa;
-        if (out.pc) out.pc[po] = pc;
-      }
+      const int y = y0 + rbase + r;
+      if (y >= H) continue;
+      const float a = acc_a[i], bq = 2.f * acc_b[i], cq = acc_c[i];
+      const float root = sqrtf(bq * bq + (a - cq) * (a - cq));
+      const size_t po = ((size_t)b * H + y) * W + x;
+      out.mmax[po] = 0.5f * (cq + a + root);
+      out.mmin[po] = fmaxf(0.5f * (cq + a - root), 0.f);
+      out.mim[po] = (uint8_t)bidx[i];
+      if (out.amax) out.amax[po] = best[i];
     }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < PIX; ++i) {
-    const int p = threadIdx.x + kThreads * i;
-    if (p >= npix) continue;
-    const int r = p / W, x = p % W;
-    if (y0 + r >= H) continue;
-    const float a = acc_a[i], bq = 2.f * acc_b[i], cq = acc_c[i];
-    const float root = sqrtf(bq * bq + (a - cq) * (a - cq));
-    const size_t po = ((size_t)b * H + (y0 + r)) * W + x;
-    out.mmax[po] = 0.5f * (cq + a + root);
-    out.mmin[po] = fmaxf(0.5f * (cq + a - root), 0.f);
-    out.mim[po] = (uint8_t)bidx[i];
-    if (out.amax) out.amax[po] = best[i];
   }
 }
 
@@ -561,7 +641,6 @@ static bool make_plan(int n, GenericPlan& p) {
   const int order[5] = {5, 3, 8, 4, 2};
   for (int r : order) {
     while (m % r == 0 && p.n_pass < 16) {
-      if (r == 8 && m % 8 != 0) break;
       p.radix[p.n_pass++] = r;
       m /= r;
     }
@@ -570,22 +649,23 @@ static bool make_plan(int n, GenericPlan& p) {
 }
 
 struct FieldsPlan {
-  int B, H, W, Wh, S, O, F;
+  int B, H, W, Wh, Hp, S, O, F;
   int gw, gh;
-  size_t off_P, off_Q, off_amp0, off_hist, off_info, off_cand, off_cnt, off_thr, total;
+  size_t off_P, off_Q, off_R0, off_amp0, off_hist, off_info, off_cand, off_cnt, off_thr, total;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static FieldsPlan plan_fields(int B, int H, int W, int S, int O) {
   FieldsPlan p{};
-  p.B = B; p.H = H; p.W = W; p.Wh = W / 2 + 1; p.S = S; p.O = O; p.F = S * O;
+  p.B = B; p.H = H; p.W = W; p.Wh = W / 2 + 1; p.Hp = (H + 3) & ~3; p.S = S; p.O = O; p.F = S * O;
   p.gw = fast_g(W); p.gh = fast_g(H);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
   const size_t n = (size_t)H * W;
   p.off_P = take((size_t)B * H * p.Wh * sizeof(float2));
-  p.off_Q = take((size_t)B * p.F * n * sizeof(float2));
+  p.off_Q = take((size_t)B * p.F * p.Hp * W * sizeof(float2));
+  p.off_R0 = take((size_t)B * O * n * sizeof(float2));
   p.off_amp0 = take((size_t)B * O * n * sizeof(float));
   p.off_hist = take((size_t)B * O * kHistBins * sizeof(unsigned));
   p.off_info = take((size_t)B * O * sizeof(MedInfo));
@@ -602,7 +682,10 @@ size_t fields_workspace_bytes(int B, int H, int W, int S, int O) {
 
 template <class K>
 static cudaError_t set_smem(K kern, size_t bytes) {
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  return e;
 }
 
 template <int G>
@@ -628,8 +711,8 @@ static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c,
   size_t smem;
   dim3 grid;
   if constexpr (G > 0) {
-    const int N = 32 * G, NG = kThreads / G, CG = NG / 2, PL = padded_len(N);
-    smem = ((size_t)CG * PL + 2 * (size_t)CG * N + (size_t)NG * PL) * sizeof(float2);
+    const int N = 32 * G, NG = ColsCfg<G>::T / G, CG = NG / 2, PL = padded_len(N);
+    smem = ((size_t)CG * PL + (size_t)NG * PL) * sizeof(float2) + 3 * (size_t)CG * N * sizeof(float);
     grid = dim3((c.Wh + CG - 1) / CG, c.B);
   } else {
     const int PL = padded_len(c.H);
@@ -638,12 +721,13 @@ static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c,
   }
   cudaError_t e = set_smem(k_cols<G>, smem);
   if (e != cudaSuccess) return e;
-  k_cols<G><<<grid, kThreads, smem, st>>>(P, Q, c);
+  k_cols<G><<<grid, ColsCfg<G>::T, smem, st>>>(P, Q, c);
   return cudaGetLastError();
 }
 
 template <int G>
-static cudaError_t launch_amp0(const float2* Q, float* amp0, unsigned* hist, const FieldsConst& c, cudaStream_t st) {
+static cudaError_t launch_amp0(const float2* Q, float2* R0, float* amp0, unsigned* hist, const FieldsConst& c,
+                               cudaStream_t st) {
   size_t smem;
   dim3 grid;
   if constexpr (G > 0) {
@@ -656,34 +740,34 @@ static cudaError_t launch_amp0(const float2* Q, float* amp0, unsigned* hist, con
   }
   cudaError_t e = set_smem(k_rows_amp0<G>, smem);
   if (e != cudaSuccess) return e;
-  k_rows_amp0<G><<<grid, kThreads, smem, st>>>(Q, amp0, hist, c);
+  k_rows_amp0<G><<<grid, kThreads, smem, st>>>(Q, R0, amp0, hist, c);
   return cudaGetLastError();
 }
 
 template <int G>
-static cudaError_t launch_pc(const float2* Q, const float* thr, const PcOut& out, const FieldsConst& c,
-                             cudaStream_t st) {
-  int rows, ops;
+static cudaError_t launch_pc(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
+                             const FieldsConst& c, cudaStream_t st) {
+  const size_t PLb = padded_len(c.W) * sizeof(float2);
+  const size_t budget = 200 * 1024;
+  int rr, ops;
   size_t nbuf;
   if constexpr (G > 0) {
     const int NG = kThreads / G;
-    rows = NG / (c.S * c.O);
-    if (rows < 1) rows = 1;
-    if (rows > 1) ops = c.O;
-    else { ops = NG / c.S; if (ops < 1) ops = 1; if (ops > c.O) ops = c.O; }
-    // PIX bound: rows*W pixels over kThreads threads
-    while (rows > 1 && rows * c.W > kThreads * PcShape<G>::PIX) --rows;
-    const int nb = rows * c.S * ops;
-    nbuf = nb + NG;   // + spare scratch for idle groups
+    rr = (2 * c.S * PLb <= budget) ? 2 : 1;
+    ops = NG / (rr * c.S);
+    if (ops < 1) ops = 1;
+    if (ops > c.O) ops = c.O;
+    while (ops > 1 && (size_t)rr * ops * c.S * PLb > budget) --ops;
+    nbuf = (size_t)rr * ops * c.S;
   } else {
-    rows = 1; ops = 1;
+    rr = 1; ops = 1;
     nbuf = c.S + 1;
   }
-  const size_t smem = nbuf * padded_len(c.W) * sizeof(float2);
+  const size_t smem = nbuf * PLb;
   cudaError_t e = set_smem(k_rows_pc<G>, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((c.H + rows - 1) / rows, c.B);
-  k_rows_pc<G><<<grid, kThreads, smem, st>>>(Q, thr, out, c, rows, ops);
+  dim3 grid((c.H + 1) / 2, c.B);
+  k_rows_pc<G><<<grid, kThreads, smem, st>>>(Q, R0, thr, out, c, rr, ops);
   return cudaGetLastError();
 }
 
@@ -704,21 +788,22 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
                void* ws, size_t ws_bytes, cudaStream_t st) {
   const FieldsPlan p = plan_fields(B, H, W, bk.n_scales, bk.n_orient);
   if (ws_bytes < p.total) return 1;
+  const double log2e = 1.4426950408889634;
   FieldsConst c{};
-  c.B = B; c.H = H; c.W = W; c.Wh = p.Wh; c.S = bk.n_scales; c.O = bk.n_orient;
+  c.B = B; c.H = H; c.W = W; c.Wh = p.Wh; c.Hp = p.Hp; c.S = bk.n_scales; c.O = bk.n_orient;
   for (int s = 0; s < c.S; ++s) c.log_lambda[s] = (float)bk.log_lambda[s];
-  c.inv_den_r = (float)bk.inv_den_r;
-  c.inv_den_a = (float)bk.inv_den_a;
-  for (int o = 0; o < c.O; ++o) {
-    c.ang[o] = (float)bk.angle[o];
-    c.cos_a[o] = (float)bk.cos_a[o];
-    c.sin_a[o] = (float)bk.sin_a[o];
+  c.a2 = (float)(bk.inv_den_r * log2e);
+  c.b2 = (float)(bk.inv_den_a * log2e);
+  for (int q = 0; q < c.O; ++q) {
+    c.ang[q] = (float)bk.angle[q];
+    c.cos_a[q] = (float)bk.cos_a[q];
+    c.sin_a[q] = (float)bk.sin_a[q];
   }
   c.spread_cutoff = (float)bk.spread_cutoff;
   c.spread_gain = (float)bk.spread_gain;
   c.inv_sm1 = (float)(1.0 / (c.S > 1 ? c.S - 1 : 1));
   c.lp_lncut = (float)bk.lp_lncut;
-  c.inv_hw = (float)(1.0 / ((double)H * W));
+  c.log2_inv_hw = (float)(-std::log2((double)H * (double)W));
   c.thr_factor = bk.thr_factor;
   c.tw_w = twiddle_table(W);
   c.tw_h = twiddle_table(H);
@@ -729,6 +814,7 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   char* w = static_cast<char*>(ws);
   float2* P = reinterpret_cast<float2*>(w + p.off_P);
   float2* Q = reinterpret_cast<float2*>(w + p.off_Q);
+  float2* R0 = reinterpret_cast<float2*>(w + p.off_R0);
   float* amp0 = reinterpret_cast<float*>(w + p.off_amp0);
   unsigned* hist = reinterpret_cast<unsigned*>(w + p.off_hist);
   MedInfo* info = reinterpret_cast<MedInfo*>(w + p.off_info);
@@ -743,7 +829,7 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   if (e != cudaSuccess) return 3;
   R2_DISPATCH_G(p.gh, launch_cols, P, Q, c, st);
   if (e != cudaSuccess) return 3;
-  R2_DISPATCH_G(p.gw, launch_amp0, Q, amp0, hist, c, st);
+  R2_DISPATCH_G(p.gw, launch_amp0, Q, R0, amp0, hist, c, st);
   if (e != cudaSuccess) return 3;
   const unsigned n = (unsigned)((size_t)H * W);
   k_med_bins<<<B * c.O, 1024, 0, st>>>(hist, info, n);
@@ -754,7 +840,7 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   k_med_final<<<B * c.O, 1024, 0, st>>>(cand, cnt, info, thr, n, c.thr_factor);
   if (cudaGetLastError() != cudaSuccess) return 3;
   PcOut po{o.mmax, o.mmin, o.mim, o.a_o, o.pc, o.amax};
-  R2_DISPATCH_G(p.gw, launch_pc, Q, thr, po, c, st);
+  R2_DISPATCH_G(p.gw, launch_pc, Q, R0, thr, po, c, st);
   if (e != cudaSuccess) return 3;
   return 0;
 }

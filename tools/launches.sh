@@ -1,0 +1,10 @@
+#!/bin/bash
+# Per-kernel launch list of one pipeline iteration (run on the GPU box).
+# usage: tools/launches.sh TAG [pairs]
+TAG=${1:-x}; PAIRS=${2:-16}
+mkdir -p gpurun_out
+python tools/stage_timing.py --pairs $PAIRS --iters 2 > gpurun_out/plain_$TAG.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active,sm__inst_executed.sum \
+    --clock-control none -s 24 -c 24 --csv --log-file gpurun_out/launches_$TAG.csv \
+    python tools/stage_timing.py --pairs $PAIRS --iters 2 > gpurun_out/ncu_$TAG.log 2>&1
+tail -2 gpurun_out/plain_$TAG.log
