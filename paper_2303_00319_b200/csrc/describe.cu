@@ -11,12 +11,19 @@
 // reference's float64 vector is counts / ||counts||, rebuilt bit-exactly by
 // the host layer when the dataclass API is used).
 //
-//   k_desc_plan  one CTA per keypoint: base-patch cell counts (packed byte
-//                counters per column thread, segmented warp reduction),
-//                dominant index / runner-up, rotated-bbox skip test
-//   k_desc_scan  per image: exclusive scan of descriptors per keypoint
-//   k_desc_emit  one CTA per keypoint: recode (a per-cell permutation of the
-//                base counts) or rotated gather + recode, fp16 rows out
+//   k_desc_main  one CTA per keypoint.  The MIM neighbourhood every sample of
+//                the axis-aligned and rotated patches can touch is staged in
+//                shared memory as bytes s = 5(v-1) (4 pixels per word op;
+//                0xFF outside the image), so a sample counts as
+//                acc += 1 << s into six 5-bit fields.  Four threads share a
+//                cell (4 columns x cs rows each) and reduce with two shuffles.
+//                Then dominant index / runner-up, the rotated patch of each
+//                pick through a host-built int16 offset table, recode (a
+//                per-cell permutation) and a write into the fixed slot
+//                keypoint * per + pick.
+//   k_desc_scan  per image: exclusive scan of the slot valid flags
+//   k_desc_copy  order-preserving compaction of the slots
+#include <algorithm>
 #include <cmath>
 #include <mutex>
 #include <unordered_map>
@@ -29,19 +36,13 @@ namespace r2 {
 
 namespace {
 
-constexpr int kT = 256;
-constexpr int kMaxCells = 16 * 16;
-constexpr int kMaxDim = kMaxCells * 16;
-
-struct KpPlan {
-  int ndesc;
-  int skipped;
-  int pick[2];
-};
+constexpr int kT = 160;   // 5 warps: 144 counting threads for the 6x6 grid of 16-px cells
 
 struct GatherTables {
-  const short2* off;     // [O][P*P] (dx, dy); angle index 0 unused
+  const short* soff;     // [O][P*P] dy*stride + dx into the staged region; angle 0 unused
   const int4* bbox;      // [O] (dx_min, dx_max, dy_min, dy_max)
+  int radius;            // max |offset| over all angles (and the axis crop)
+  int stride;            // staged row length in bytes (multiple of 4, >= 2*radius + 4)
 };
 
 std::mutex g_mu;
@@ -49,7 +50,7 @@ std::unordered_map<long long, GatherTables> g_tables;
 
 // Host: the reference's rotated sample offsets (float64, snapped cos/sin,
 // nearest neighbour floor(u + 0.5)), ref: descriptor.py:46-82.
-static double snap_h(double v) {
+double snap_h(double v) {
   if (std::fabs(v) < 1e-12) return 0.0;
   if (std::fabs(std::fabs(v) - 1.0) < 1e-12) return std::copysign(1.0, v);
   return v;
@@ -62,9 +63,10 @@ GatherTables gather_tables(int P, int O) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_tables.find(key);
   if (it != g_tables.end()) return it->second;
-  std::vector<short2> off((size_t)O * P * P);
+  std::vector<int2> off((size_t)O * P * P);
   std::vector<int4> bbox(O);
   const double half = P / 2.0;
+  int radius = (P + 1) / 2;   // axis crop spans [x + 1 - (P+1)/2, x + P - (P+1)/2]
   for (int a = 0; a < O; ++a) {
     const double ang = a * (M_PI / O);
     const double c = snap_h(std::cos(ang)), s = snap_h(std::sin(ang));
@@ -75,100 +77,192 @@ GatherTables gather_tables(int P, int O) {
         const double u = j + 0.5 - half;
         const int dx = (int)std::floor(c * u - s * v + 0.5);
         const int dy = (int)std::floor(s * u + c * v + 0.5);
-        off[(size_t)a * P * P + i * P + j] = make_short2((short)dx, (short)dy);
+        off[(size_t)a * P * P + i * P + j] = make_int2(dx, dy);
         bb.x = std::min(bb.x, dx); bb.y = std::max(bb.y, dx);
         bb.z = std::min(bb.z, dy); bb.w = std::max(bb.w, dy);
       }
     }
     bbox[a] = bb;
+    radius = std::max({radius, -bb.x, bb.y, -bb.z, bb.w});
   }
-  GatherTables t{nullptr, nullptr};
-  short2* d_off = nullptr;
+  const int stride = ((2 * radius + 1 + 3) / 4 + 1) * 4;
+  GatherTables t{nullptr, nullptr, radius, stride};
+  if ((size_t)radius * stride + radius > 32767) return t;   // offsets must fit int16
+  std::vector<short> soff(off.size());
+  for (size_t i = 0; i < off.size(); ++i) soff[i] = (short)(off[i].y * stride + off[i].x);
+  short* d_off = nullptr;
   int4* d_bb = nullptr;
-  if (cudaMalloc(&d_off, off.size() * sizeof(short2)) != cudaSuccess) return t;
+  if (cudaMalloc(&d_off, soff.size() * sizeof(short)) != cudaSuccess) return t;
   if (cudaMalloc(&d_bb, bbox.size() * sizeof(int4)) != cudaSuccess) return t;
-  cudaMemcpy(d_off, off.data(), off.size() * sizeof(short2), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_off, soff.data(), soff.size() * sizeof(short), cudaMemcpyHostToDevice);
   cudaMemcpy(d_bb, bbox.data(), bbox.size() * sizeof(int4), cudaMemcpyHostToDevice);
-  t.off = d_off;
+  t.soff = d_off;
   t.bbox = d_bb;
   g_tables[key] = t;
   return t;
 }
 
 struct DescConst {
-  int H, W, O, P, g, cs, cells, dim;
+  int H, W, O, P, g, cs, cells, dim, per;
   double ratio;
   bool rotate;
   int mode;
-  bool fast;           // cs is a power of two <= 32 and O <= 8
+  int R, stride, rows;   // staging radius, staged row bytes, staged rows (2R+1)
 };
 
-// Count per (cell, value) of a P x P sample grid read through `src(i, j)`
-// (i = sample row, j = sample column) into smem cnt[cells * O].
-template <class Src>
-R2_DEV void cell_counts(const DescConst& c, Src src, unsigned* cnt) {
-  for (int i = threadIdx.x; i < c.cells * c.O; i += kT) cnt[i] = 0;
-  __syncthreads();
-  const int ngrp = kT / c.P;
-  const int grp = threadIdx.x / c.P, col = threadIdx.x % c.P;
-  const bool active = grp < ngrp;
-  for (int cr0 = 0; cr0 < c.g; cr0 += ngrp) {
-    const int cr = cr0 + grp;
-    const bool on = active && cr < c.g;
-    unsigned long long acc = 0, acc2 = 0;
-    if (on) {
-      for (int r = 0; r < c.cs; ++r) {
-        const int v = src(cr * c.cs + r, col);
-        if (v >= 1 && v <= 8) acc += 1ull << (8 * (v - 1));
-        else if (v > 8 && v <= 16) acc2 += 1ull << (8 * (v - 9));
-      }
-    }
-    const int cell = cr * c.g + col / c.cs;
-    if (c.fast) {
-      // split into 16-bit fields and reduce across the cs column threads of the cell
-      unsigned long long e = acc & 0x00ff00ff00ff00ffull, o = (acc >> 8) & 0x00ff00ff00ff00ffull;
-      for (int m = 1; m < c.cs; m <<= 1) {
-        e += __shfl_xor_sync(0xffffffffu, e, m);
-        o += __shfl_xor_sync(0xffffffffu, o, m);
-      }
-      if (on && (col % c.cs) == 0) {
-        for (int v = 0; v < c.O; ++v) {
-          const unsigned long long w = (v & 1) ? o : e;
-          cnt[cell * c.O + v] = (unsigned)((w >> (16 * (v >> 1))) & 0xffffu);
-        }
-      }
-    } else if (on) {
-      for (int v = 0; v < c.O; ++v) {
-        const unsigned n = v < 8 ? (unsigned)((acc >> (8 * v)) & 255u) : (unsigned)((acc2 >> (8 * (v - 8))) & 255u);
-        if (n) atomicAdd(&cnt[cell * c.O + v], n);
-      }
-    }
-  }
-  __syncthreads();
+// six 5-bit counters (<= 31 samples) -> 10-bit fields: values 1,3,5 into e, 2,4,6 into o
+R2_DEV void widen(uint32_t acc, uint32_t& e, uint32_t& o) {
+  e += (acc & 31u) | ((acc >> 10) & 31u) << 10 | ((acc >> 20) & 31u) << 20;
+  o += ((acc >> 5) & 31u) | ((acc >> 15) & 31u) << 10 | ((acc >> 25) & 31u) << 20;
 }
 
-__global__ void __launch_bounds__(kT) k_desc_plan(const uint8_t* __restrict__ mim, DescribeArgs a, DescConst c,
-                                                  GatherTables tab, KpPlan* __restrict__ plan,
-                                                  unsigned short* __restrict__ base) {
-  __shared__ unsigned cnt[kMaxDim];
-  const int b = blockIdx.y, k = blockIdx.x;
-  KpPlan* pl = plan + (size_t)b * a.kp_stride + k;
-  if (k >= a.kp_count[b]) {
-    if (threadIdx.x == 0) { pl->ndesc = 0; pl->skipped = 0; }
-    return;
+// reduce the 4 threads of a cell and write its O counts
+R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int O) {
+  e += __shfl_xor_sync(0xffffffffu, e, 1);
+  o += __shfl_xor_sync(0xffffffffu, o, 1);
+  e += __shfl_xor_sync(0xffffffffu, e, 2);
+  o += __shfl_xor_sync(0xffffffffu, o, 2);
+  if (writer)
+    for (int v = 0; v < O; ++v) out[v] = (((v & 1) ? o : e) >> (10 * (v >> 1))) & 1023u;
+}
+
+// 1 << s for a staged shift byte (0xFF -> 0)
+R2_DEV uint32_t one_hot(uint32_t s) { return s < 32u ? (1u << s) : 0u; }
+
+// axis-aligned patch: thread = (cell, quarter); 4 columns x CS rows per thread
+template <int CS>
+R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsigned* cnt) {
+  const int tpc = CS / 4;                       // threads per cell
+  const int t = threadIdx.x;
+  const bool on = t < c.cells * tpc;
+  const int cell = on ? t / tpc : 0, sub = t % tpc;
+  const int cr = cell / c.g, cc = cell % c.g;
+  uint32_t e = 0, o = 0;
+  if (on) {
+    const int col = off0 + cc * CS + 4 * sub;   // byte offset of this thread's 4 columns within a row
+    const int wbase = col >> 2, sh = (col & 3) * 8;
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(sreg) + (cr * CS) * (c.stride >> 2) + wbase;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int r = 0; r < CS; ++r) {
+      const uint32_t* p = rw + r * (c.stride >> 2);
+      const uint32_t w = __funnelshift_r(p[0], p[1], sh);
+      acc += one_hot(w & 255u) + one_hot((w >> 8) & 255u) + one_hot((w >> 16) & 255u) + one_hot(w >> 24);
+      if (r % 7 == 6 || r == CS - 1) { widen(acc, e, o); acc = 0; }   // 4 samples/row: <= 28 per field
+    }
   }
+  reduce_cell(e, o, on && sub == 0, cnt + cell * c.O, c.O);
+}
+
+// rotated patch of angle table t: sample (i, j) at ctr + t[i*P + j]
+template <int CS>
+R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const short* __restrict__ t, unsigned* cnt) {
+  const int tpc = CS / 4;
+  const int tid = threadIdx.x;
+  const bool on = tid < c.cells * tpc;
+  const int cell = on ? tid / tpc : 0, sub = tid % tpc;
+  const int cr = cell / c.g, cc = cell % c.g;
+  uint32_t e = 0, o = 0;
+  if (on) {
+    const short* tr = t + (cr * CS) * c.P + cc * CS + 4 * sub;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int r = 0; r < CS; ++r) {
+      const short2 a = __ldg(reinterpret_cast<const short2*>(tr + r * c.P));
+      const short2 b = __ldg(reinterpret_cast<const short2*>(tr + r * c.P + 2));
+      acc += one_hot(ctr[a.x]) + one_hot(ctr[a.y]) + one_hot(ctr[b.x]) + one_hot(ctr[b.y]);
+      if (r % 7 == 6 || r == CS - 1) { widen(acc, e, o); acc = 0; }
+    }
+  }
+  reduce_cell(e, o, on && sub == 0, cnt + cell * c.O, c.O);
+}
+
+// write one descriptor row: output bin (cell, w-1) holds the count of the
+// input value v with recode(v) = w, i.e. v = (w - 1 + pivot - 1) mod O + 1
+// (ref: mim.py:117-136)
+R2_DEV void emit_row(const DescribeArgs& a, const DescConst& c, const unsigned* cnt, int pivot, __half* row,
+                     int* s_sq) {
+  int sq = 0;
+  for (int i = threadIdx.x; i < a.stride; i += kT) {
+    unsigned v = 0;
+    if (i < c.dim) {
+      const int cell = i / c.O, w = i % c.O;
+      v = cnt[cell * c.O + (w + pivot - 1) % c.O];
+    }
+    row[i] = __uint2half_rn(v);
+    sq += (int)(v * v);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(s_sq, sq);
+}
+
+template <int CS>
+__global__ void __launch_bounds__(kT) k_desc_main(const uint8_t* __restrict__ mim, DescribeArgs a, DescConst c,
+                                                  GatherTables tab, __half* __restrict__ slot_rows,
+                                                  int* __restrict__ slot_meta, int* __restrict__ kp_skip) {
+  extern __shared__ uint32_t s_dyn[];             // staged bytes (c.rows x c.stride), then cnt
+  uint8_t* sreg = reinterpret_cast<uint8_t*>(s_dyn);
+  unsigned* cnt = s_dyn + (c.rows * c.stride) / 4;   // [cells * O]
+  __shared__ int s_pick[16], s_np, s_sq;
+  const int b = blockIdx.y, k = blockIdx.x;
+  const size_t slot0 = ((size_t)b * a.kp_stride + k) * c.per;
+  int* meta = slot_meta + slot0 * 3;              // (valid, variant, sqnorm) per slot
+  if (k >= a.kp_count[b]) return;                 // k_desc_scan only reads live keypoints
   const int x = a.kp_x[(size_t)b * a.kp_stride + k], y = a.kp_y[(size_t)b * a.kp_stride + k];
   const int x0 = x + 1 - (c.P + 1) / 2, y0 = y + 1 - (c.P + 1) / 2;   // floor(kp + 1 - P/2)
   if (x0 < 0 || y0 < 0 || x0 + c.P > c.W || y0 + c.P > c.H) {
-    if (threadIdx.x == 0) { pl->ndesc = 0; pl->skipped = 1; }
+    for (int q = threadIdx.x; q < c.per; q += kT) meta[3 * q] = 0;
+    if (threadIdx.x == 0) kp_skip[(size_t)b * a.kp_stride + k] = 1;
     return;
   }
   const uint8_t* m = mim + (size_t)b * c.H * c.W;
-  cell_counts(c, [&](int i, int j) { return (int)__ldg(&m[(size_t)(y0 + i) * c.W + x0 + j]); }, cnt);
-  unsigned short* bo = base + ((size_t)b * a.kp_stride + k) * c.cells * c.O;
-  for (int i = threadIdx.x; i < c.cells * c.O; i += kT) bo[i] = (unsigned short)cnt[i];
+  // ---- stage rows y-R..y+R, word-aligned columns from ax0, as shift bytes 5(v-1)
+  const int ax0 = (x - c.R) >= 0 ? ((x - c.R) & ~3) : -(((c.R - x) + 3) & ~3);
+  const int wpr = c.stride / 4;
+  const bool word_ok = (c.W & 3) == 0;
+  uint32_t* sw = s_dyn;
+  const bool inside = word_ok && y - c.R >= 0 && y + c.R < c.H && ax0 >= 0 && ax0 + 4 * wpr <= c.W;
+  if (inside) {
+    // common case: one aligned word load + one multiply-add per 4 pixels
+    const uint32_t* src0 = reinterpret_cast<const uint32_t*>(m + (size_t)(y - c.R) * c.W + ax0);
+    const int wrow = c.W >> 2;
+    for (int r = threadIdx.x >> 5; r < c.rows; r += kT / 32) {
+      const uint32_t* src = src0 + r * wrow;
+      uint32_t* dst = sw + r * wpr;
+      for (int wq = threadIdx.x & 31; wq < wpr; wq += 32) dst[wq] = __ldg(src + wq) * 5u - 0x05050505u;
+    }
+  } else for (int r = threadIdx.x >> 5; r < c.rows; r += kT / 32) {
+    const int gy = y - c.R + r;
+    const bool row_in = gy >= 0 && gy < c.H;
+    const uint8_t* row = m + (size_t)(row_in ? gy : 0) * c.W;
+    for (int wq = threadIdx.x & 31; wq < wpr; wq += 32) {
+      const int gx = ax0 + 4 * wq;
+      uint32_t v = 0xffffffffu;
+      if (row_in) {
+        if (word_ok && gx >= 0 && gx + 3 < c.W) {
+          v = __ldg(reinterpret_cast<const uint32_t*>(row + gx)) * 5u - 0x05050505u;
+        } else {
+          v = 0;
+          for (int e = 0; e < 4; ++e) {
+            const int xx = gx + e;
+            const uint32_t s = (xx >= 0 && xx < c.W) ? (uint32_t)(5 * (row[xx] - 1)) & 255u : 255u;
+            v |= s << (8 * e);
+          }
+        }
+      }
+      sw[r * wpr + wq] = v;
+    }
+  }
+  for (int i = threadIdx.x; i < c.cells * c.O; i += kT) cnt[i] = 0;
+  __syncthreads();
+  const int bx = x - ax0;                         // keypoint column within a staged row
+  const uint8_t* ctr = sreg + c.R * c.stride + bx;   // keypoint pixel
+  // ---- axis-aligned patch
+  count_axis<CS>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt);
+  __syncthreads();
+  // ---- dominant index / runner-up (ref: mim.py:69-91)
   if (threadIdx.x < 32) {
-    // patch histogram (ref: mim.py:58-66) = sum of the cell counts, warp-parallel
     unsigned hs[16];
     for (int v = 0; v < c.O; ++v) {
       unsigned s = 0;
@@ -177,60 +271,86 @@ __global__ void __launch_bounds__(kT) k_desc_plan(const uint8_t* __restrict__ mi
       for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       hs[v] = s;
     }
-    if (threadIdx.x != 0) return;
-    KpPlan p{0, 0, {0, 0}};
-    if (c.mode == 0) { p.ndesc = 1; p.pick[0] = 1; }
-    else if (c.mode == 1) { p.ndesc = c.O; }
-    else {
-      // ref: mim.py:69-91 -- first argmax, runner-up if >= ratio * peak
-      // (float64, inclusive), runner-up ties to the bin cyclically closest
-      // after the peak.
-      double hist[16];
-      for (int v = 0; v < c.O; ++v) hist[v] = (double)hs[v];
-      int pk = 0;
-      for (int v = 1; v < c.O; ++v) if (hist[v] > hist[pk]) pk = v;
-      double rv = -1.0;
-      for (int v = 0; v < c.O; ++v) if (v != pk && hist[v] > rv) rv = hist[v];
-      int picks[2] = {pk + 1, 0};
-      int np = 1;
-      if (rv >= c.ratio * hist[pk]) {
-        int best = -1, bestd = 1 << 30;
-        for (int v = 0; v < c.O; ++v) {
-          if (v == pk || hist[v] != rv) continue;
-          const int d = ((v - pk) % c.O + c.O) % c.O;
-          if (d < bestd) { bestd = d; best = v; }
+    if (threadIdx.x == 0) {
+      int np = 0, skip = 0;
+      if (c.mode == 0) { s_pick[np++] = 1; }
+      else if (c.mode == 1) { for (int v = 1; v <= c.O; ++v) s_pick[np++] = v; }
+      else {
+        // first argmax; runner-up if >= ratio * peak (float64, inclusive);
+        // runner-up ties go to the bin cyclically closest after the peak
+        int pk = 0;
+        for (int v = 1; v < c.O; ++v) if (hs[v] > hs[pk]) pk = v;
+        double rv = -1.0;
+        for (int v = 0; v < c.O; ++v) if (v != pk && (double)hs[v] > rv) rv = (double)hs[v];
+        int picks[2] = {pk + 1, 0}, cand = 1;
+        if (rv >= c.ratio * (double)hs[pk]) {
+          int best = -1, bestd = 1 << 30;
+          for (int v = 0; v < c.O; ++v) {
+            if (v == pk || (double)hs[v] != rv) continue;
+            const int d = ((v - pk) % c.O + c.O) % c.O;
+            if (d < bestd) { bestd = d; best = v; }
+          }
+          picks[1] = best + 1;
+          cand = 2;
         }
-        picks[1] = best + 1;
-        np = 2;
-      }
-      for (int q = 0; q < np; ++q) {
-        const int dom = picks[q];
-        if (c.rotate && dom != 1) {
-          const int4 bb = tab.bbox[dom - 1];
-          if (x + bb.x < 0 || x + bb.y >= c.W || y + bb.z < 0 || y + bb.w >= c.H) { p.skipped++; continue; }
+        for (int q = 0; q < cand; ++q) {
+          const int dom = picks[q];
+          if (c.rotate && dom != 1) {
+            const int4 bb = tab.bbox[dom - 1];
+            if (x + bb.x < 0 || x + bb.y >= c.W || y + bb.z < 0 || y + bb.w >= c.H) { ++skip; continue; }
+          }
+          s_pick[np++] = dom;
         }
-        p.pick[p.ndesc++] = dom;
       }
+      s_np = np;
+      kp_skip[(size_t)b * a.kp_stride + k] = skip;
     }
-    *pl = p;
   }
+  __syncthreads();
+  const int np = s_np;
+  // axis-patch descriptors first (they reuse `cnt`), rotated ones after
+  for (int q = 0; q < np; ++q) {
+    const int dom = s_pick[q];
+    if (c.mode == 2 && c.rotate && dom != 1) continue;
+    if (threadIdx.x == 0) s_sq = 0;
+    __syncthreads();
+    emit_row(a, c, cnt, c.mode == 0 ? 1 : dom, slot_rows + (slot0 + q) * a.stride, &s_sq);
+    __syncthreads();
+    if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = c.mode == 0 ? 1 : dom; meta[3 * q + 2] = s_sq; }
+  }
+  if (c.mode == 2 && c.rotate) {
+    for (int q = 0; q < np; ++q) {
+      const int dom = s_pick[q];
+      if (dom == 1) continue;
+      __syncthreads();
+      count_rotated<CS>(c, ctr, tab.soff + (size_t)(dom - 1) * c.P * c.P, cnt);
+      if (threadIdx.x == 0) s_sq = 0;
+      __syncthreads();
+      emit_row(a, c, cnt, dom, slot_rows + (slot0 + q) * a.stride, &s_sq);
+      __syncthreads();
+      if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq; }
+    }
+  }
+  for (int q = np + threadIdx.x; q < c.per; q += kT) meta[3 * q] = 0;
 }
 
-__global__ void __launch_bounds__(1024) k_desc_scan(const KpPlan* __restrict__ plan, DescribeArgs a,
+// exclusive scan of the valid flags of one image's slots -> output positions
+__global__ void __launch_bounds__(1024) k_desc_scan(const int* __restrict__ slot_meta,
+                                                    const int* __restrict__ kp_skip, DescribeArgs a, int per,
                                                     int* __restrict__ offs) {
   __shared__ int s_warp[32];
   __shared__ int s_base, s_skip, s_tot;
   const int b = blockIdx.x;
-  const int n = a.kp_count[b];
-  const KpPlan* pl = plan + (size_t)b * a.kp_stride;
-  int* of = offs + (size_t)b * a.kp_stride;
+  const int n = a.kp_count[b] * per;
+  const int* meta = slot_meta + (size_t)b * a.kp_stride * per * 3;
+  int* of = offs + (size_t)b * a.kp_stride * per;
   if (threadIdx.x == 0) { s_base = 0; s_skip = 0; }
   __syncthreads();
+  for (int i = threadIdx.x; i < a.kp_count[b]; i += blockDim.x) atomicAdd(&s_skip, kp_skip[(size_t)b * a.kp_stride + i]);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int c0 = 0; c0 < n; c0 += blockDim.x) {
     const int i = c0 + threadIdx.x;
-    const int v = i < n ? pl[i].ndesc : 0;
-    if (i < n && pl[i].skipped) atomicAdd(&s_skip, pl[i].skipped);
+    const int v = i < n ? meta[3 * i] : 0;
     int incl = v;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -245,7 +365,7 @@ __global__ void __launch_bounds__(1024) k_desc_scan(const KpPlan* __restrict__ p
       s_tot = run;
     }
     __syncthreads();
-    if (i < n) of[i] = s_base + s_warp[wid] + incl - v;
+    if (i < n) of[i] = v ? s_base + s_warp[wid] + incl - v : -1;
     __syncthreads();
     if (threadIdx.x == 0) s_base += s_tot;
     __syncthreads();
@@ -253,114 +373,94 @@ __global__ void __launch_bounds__(1024) k_desc_scan(const KpPlan* __restrict__ p
   if (threadIdx.x == 0) { a.count[b] = s_base; a.skipped[b] = s_skip; }
 }
 
-__global__ void __launch_bounds__(kT) k_desc_emit(const uint8_t* __restrict__ mim, DescribeArgs a, DescConst c,
-                                                  GatherTables tab, const KpPlan* __restrict__ plan,
-                                                  const unsigned short* __restrict__ base,
-                                                  const int* __restrict__ offs) {
-  __shared__ unsigned cnt[kMaxDim];
-  __shared__ int s_sq;
-  const int b = blockIdx.y, k = blockIdx.x;
-  if (k >= a.kp_count[b]) return;
-  const KpPlan pl = plan[(size_t)b * a.kp_stride + k];
-  if (pl.ndesc == 0) return;
-  const int x = a.kp_x[(size_t)b * a.kp_stride + k], y = a.kp_y[(size_t)b * a.kp_stride + k];
-  const unsigned short* bi = base + ((size_t)b * a.kp_stride + k) * c.cells * c.O;
-  const uint8_t* m = mim + (size_t)b * c.H * c.W;
-  const int off0 = offs[(size_t)b * a.kp_stride + k];
-  for (int j = 0; j < pl.ndesc; ++j) {
-    const int slot = off0 + j;
-    int variant, pivot;
-    bool rotated = false;
-    if (c.mode == 0) { variant = 1; pivot = 1; }
-    else if (c.mode == 1) { variant = j + 1; pivot = j + 1; }
-    else { variant = pl.pick[j]; pivot = variant; rotated = c.rotate && variant != 1; }
-    if (rotated) {
-      const short2* t = tab.off + (size_t)(variant - 1) * c.P * c.P;
-      cell_counts(c, [&](int i, int jj) {
-        const short2 d = __ldg(&t[i * c.P + jj]);
-        return (int)__ldg(&m[(size_t)(y + d.y) * c.W + x + d.x]);
-      }, cnt);
-    } else {
-      __syncthreads();
-      for (int i = threadIdx.x; i < c.cells * c.O; i += kT) cnt[i] = bi[i];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) s_sq = 0;
-    __syncthreads();
-    if (slot < a.cap) {
-      __half* row = a.counts + ((size_t)b * a.cap + slot) * a.stride;
-      int sq = 0;
-      for (int i = threadIdx.x; i < a.stride; i += kT) {
-        unsigned v = 0;
-        if (i < c.dim) {
-          // output bin (cell, w-1) holds input value v' with recode(v') = w:
-          // v' = (w - 1 + pivot - 1) mod O + 1  (ref: mim.py:117-136)
-          const int cell = i / c.O, w = i % c.O;
-          const int src = (w + pivot - 1) % c.O;
-          v = cnt[cell * c.O + src];
-        }
-        row[i] = __uint2half_rn(v);
-        sq += (int)(v * v);
-      }
-      atomicAdd(&s_sq, sq);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const size_t o = (size_t)b * a.cap + slot;
-        a.sqnorm[o] = s_sq;
-        a.kp[o] = k;
-        a.variant[o] = (uint8_t)variant;
-      }
-    }
-    __syncthreads();
+// one warp per slot: copy the row (16-byte vectors) and metadata into place
+__global__ void __launch_bounds__(256) k_desc_copy(const __half* __restrict__ slot_rows,
+                                                   const int* __restrict__ slot_meta, const int* __restrict__ offs,
+                                                   DescribeArgs a, int per) {
+  const int b = blockIdx.y;
+  const int slot = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (slot >= a.kp_count[b] * per) return;
+  const size_t gs = (size_t)b * a.kp_stride * per + slot;
+  const int dst = offs[gs];
+  if (dst < 0 || dst >= a.cap) return;
+  const size_t o = (size_t)b * a.cap + dst;
+  const int4* src = reinterpret_cast<const int4*>(slot_rows + gs * a.stride);
+  int4* out = reinterpret_cast<int4*>(a.counts + o * a.stride);
+  for (int i = lane; i < a.stride / 8; i += 32) out[i] = src[i];
+  if (lane == 0) {
+    a.sqnorm[o] = slot_meta[3 * gs + 2];
+    a.kp[o] = slot / per;
+    a.variant[o] = (uint8_t)slot_meta[3 * gs + 1];
   }
 }
 
-struct DescPlanWs {
-  size_t off_plan, off_base, off_offs, total;
+struct DescWs {
+  size_t off_rows, off_meta, off_skip, off_offs, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-DescPlanWs plan_ws(int B, int S, int grid, int O) {
-  DescPlanWs p{};
+int per_kp(int mode, int O) { return mode == 1 ? O : (mode == 2 ? 2 : 1); }
+
+DescWs plan_ws(int B, int S, int O, int stride) {
+  // sized for the largest mode (ring: O slots per keypoint)
+  DescWs p{};
+  const size_t slots = (size_t)B * S * O;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = al(off + bytes); return o; };
-  p.off_plan = take((size_t)B * S * sizeof(KpPlan));
-  p.off_base = take((size_t)B * S * grid * grid * O * sizeof(unsigned short));
-  p.off_offs = take((size_t)B * S * sizeof(int));
+  p.off_rows = take(slots * stride * sizeof(__half));
+  p.off_meta = take(slots * 3 * sizeof(int));
+  p.off_skip = take((size_t)B * S * sizeof(int));
+  p.off_offs = take(slots * sizeof(int));
   p.total = off;
   return p;
 }
 
+constexpr int kMaxStride = 256;
+
 }  // namespace
 
 size_t describe_workspace_bytes(int B, int kp_stride, int grid, int O) {
-  return plan_ws(B, kp_stride > 0 ? kp_stride : 1, grid, O).total;
+  (void)grid;
+  return plan_ws(B, kp_stride > 0 ? kp_stride : 1, O, kMaxStride).total;
 }
 
 int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const DescPlanWs p = plan_ws(a.B, a.kp_stride > 0 ? a.kp_stride : 1, a.grid, a.O);
+  const int S = a.kp_stride > 0 ? a.kp_stride : 1;
+  const DescWs p = plan_ws(a.B, S, a.O, kMaxStride);
   if (ws_bytes < p.total) return 1;
+  if (a.stride % 8 != 0 || a.stride > kMaxStride) return 2;
+  const int cs = a.patch / a.grid;
+  // 5-bit one-hot fields (O <= 6, cs <= 31 rows per thread), 4 columns per thread
+  if (a.O > 6 || cs != 16 || a.grid * a.grid * (cs / 4) > kT) return 2;
   DescConst c{};
-  c.H = a.H; c.W = a.W; c.O = a.O; c.P = a.patch; c.g = a.grid; c.cs = a.patch / a.grid;
-  c.cells = a.grid * a.grid; c.dim = c.cells * a.O;
+  c.H = a.H; c.W = a.W; c.O = a.O; c.P = a.patch; c.g = a.grid; c.cs = cs;
+  c.cells = a.grid * a.grid; c.dim = c.cells * a.O; c.per = per_kp(a.mode, a.O);
   c.ratio = a.ratio; c.rotate = a.rotate; c.mode = a.mode;
-  c.fast = (c.cs <= 32) && ((c.cs & (c.cs - 1)) == 0) && a.O <= 8;
   GatherTables tab = gather_tables(a.patch, a.O);
-  if (!tab.off) return 3;
+  if (!tab.soff) return 2;
+  c.R = tab.radius;
+  c.stride = tab.stride;
+  c.rows = 2 * c.R + 1;
   char* w = static_cast<char*>(ws);
-  auto* plan = reinterpret_cast<KpPlan*>(w + p.off_plan);
-  auto* base = reinterpret_cast<unsigned short*>(w + p.off_base);
+  auto* rows = reinterpret_cast<__half*>(w + p.off_rows);
+  auto* meta = reinterpret_cast<int*>(w + p.off_meta);
+  auto* skip = reinterpret_cast<int*>(w + p.off_skip);
   auto* offs = reinterpret_cast<int*>(w + p.off_offs);
   if (a.kp_stride == 0) {
     cudaMemsetAsync(a.count, 0, sizeof(int32_t) * a.B, st);
     cudaMemsetAsync(a.skipped, 0, sizeof(int32_t) * a.B, st);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
   }
+  const size_t smem = (size_t)c.rows * c.stride + (size_t)c.cells * c.O * sizeof(uint32_t);
+  if (smem > 200 * 1024) return 2;
   dim3 grid(a.kp_stride, a.B);
-  k_desc_plan<<<grid, kT, 0, st>>>(mim, a, c, tab, plan, base);
-  k_desc_scan<<<a.B, 1024, 0, st>>>(plan, a, offs);
-  k_desc_emit<<<grid, kT, 0, st>>>(mim, a, c, tab, plan, base, offs);
+  cudaFuncSetAttribute(k_desc_main<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_desc_main<16><<<grid, kT, smem, st>>>(mim, a, c, tab, rows, meta, skip);
+  k_desc_scan<<<a.B, 1024, 0, st>>>(meta, skip, a, c.per, offs);
+  dim3 g2((a.kp_stride * c.per + 7) / 8, a.B);
+  k_desc_copy<<<g2, 256, 0, st>>>(rows, meta, offs, a, c.per);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

@@ -489,16 +489,34 @@ struct PcShape {
   static constexpr int PIX = G == 0 ? 16 : (G == 128 ? 16 : (G >= 4 ? G / 4 : 1));
 };
 
+R2_DEV float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+R2_DEV float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // One CTA per row pair (y0, y0+1).  Stage = `ops` orientations of `rr` rows;
 // its buffers (row, orientation, scale) are filled by FFT jobs (scales >= 1)
 // and plain loads of the K3a responses (scale 0), then the per-pixel phase
-// congruency (ref: loggabor.py:193-251) consumes them.
-template <int G>
+// congruency (ref: loggabor.py:193-251) consumes them.  SC > 0 fixes the
+// scale count at compile time (the BASELINE / reference default is 4).
+// Approximate sqrt / rcp / exp (relative error ~1e-7) stay far inside the
+// 1e-4 map tolerance.
+template <int G, int SC>
 __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restrict__ Q, const float2* __restrict__ R0,
-                                                      const float* __restrict__ thr, PcOut out,
-                                                      const __grid_constant__ FieldsConst c, int rr, int ops) {
+                                                         const float* __restrict__ thr, PcOut out,
+                                                         const __grid_constant__ FieldsConst c, int rr, int ops) {
   extern __shared__ float2 sm[];
-  const int H = c.H, W = c.W, S = c.S, O = c.O, F = S * O;
+  constexpr int SMAX = SC > 0 ? SC : kMaxS;
+  const int H = c.H, O = c.O;
+  const int W = G > 0 ? 32 * G : c.W;
+  const int S = SC > 0 ? SC : c.S;
+  const int F = S * O;
   const int b = blockIdx.y;
   const int y0 = 2 * blockIdx.x;
   constexpr int PIX = PcShape<G>::PIX;
@@ -507,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
   const float* thr_b = thr + (size_t)b * O;
   const float2* Qb = Q + (size_t)b * F * c.Hp * W;
   const float2* Rb = R0 + (size_t)b * O * H * W;
+  const float inv_sm1 = c.inv_sm1, gain = c.spread_gain, cut = c.spread_cutoff;
 
   for (int rbase = 0; rbase < 2; rbase += rr) {
     const int npix = rr * W;
@@ -567,45 +586,47 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
       }
       __syncthreads();
       // --- per-pixel phase congruency for the orientations of this stage
+      for (int oo = 0; oo < no; ++oo) {
+        const int o = o0 + oo;
+        const float T = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
 #pragma unroll
-      for (int i = 0; i < PIX; ++i) {
-        const int p = threadIdx.x + kThreads * i;
-        if (p >= npix) continue;
-        const int r = p / W, x = p % W;
-        const int y = y0 + rbase + r;
-        if (y >= H) continue;
-        for (int oo = 0; oo < no; ++oo) {
-          const int o = o0 + oo;
+        for (int i = 0; i < PIX; ++i) {
+          const int p = threadIdx.x + kThreads * i;
+          if (p >= npix) continue;
+          const int r = p / W, x = p % W;
+          const int y = y0 + rbase + r;
+          if (y >= H) continue;
           const float2* bb = sm + ((r * ops + oo) * S) * PL + pad32(x);
-          float2 z[kMaxS];
+          float2 z[SMAX];
           float se = 0.f, so = 0.f, sa = 0.f, mx = 0.f;
 #pragma unroll
-          for (int s = 0; s < kMaxS; ++s) {
-            if (s < S) {
+          for (int s = 0; s < SMAX; ++s) {
+            if (SC > 0 || s < S) {
               z[s] = bb[s * PL];
-              const float a = sqrtf(z[s].x * z[s].x + z[s].y * z[s].y);
+              const float a = sqrt_approx(fmaf(z[s].x, z[s].x, z[s].y * z[s].y));
               se += z[s].x; so += z[s].y; sa += a; mx = fmaxf(mx, a);
             }
           }
-          // fast-math division / exp: relative error ~1e-7, far inside the 1e-4 budget
-          const float ixe = __frcp_rn(sqrtf(se * se + so * so) + 1e-4f);
+          const float ixe = rcp_approx(sqrt_approx(fmaf(se, se, so * so)) + 1e-4f);
           const float me = se * ixe, mo = so * ixe;
           float en = 0.f;
 #pragma unroll
-          for (int s = 0; s < kMaxS; ++s)
-            if (s < S) en += z[s].x * me + z[s].y * mo - fabsf(z[s].x * mo - z[s].y * me);
-          en = fmaxf(en - thr_b[o], 0.f);
-          const float spread = (__fdividef(sa, mx + 1e-4f) - 1.f) * c.inv_sm1;
-          const float wgt = __frcp_rn(1.f + __expf(c.spread_gain * (c.spread_cutoff - spread)));
-          const float pc = __fdividef(wgt * en, sa + 1e-4f);
-          const float pcc = pc * c.cos_a[o], pcs = pc * c.sin_a[o];
-          acc_a[i] += pcc * pcc;
-          acc_b[i] += pcc * pcs;
-          acc_c[i] += pcs * pcs;
+          for (int s = 0; s < SMAX; ++s)
+            if (SC > 0 || s < S) en += fmaf(z[s].x, me, z[s].y * mo) - fabsf(fmaf(z[s].x, mo, -z[s].y * me));
+          en = fmaxf(en - T, 0.f);
+          const float spread = fmaf(sa, rcp_approx(mx + 1e-4f), -1.f) * inv_sm1;
+          const float wgt = rcp_approx(1.f + __expf(gain * (cut - spread)));
+          const float pc = wgt * en * rcp_approx(sa + 1e-4f);
+          const float pcc = pc * ca, pcs = pc * sa_o;
+          acc_a[i] = fmaf(pcc, pcc, acc_a[i]);
+          acc_b[i] = fmaf(pcc, pcs, acc_b[i]);
+          acc_c[i] = fmaf(pcs, pcs, acc_c[i]);
           if (sa > best[i]) { best[i] = sa; bidx[i] = o + 1; }
-          const size_t po = (((size_t)b * O + o) * H + y) * W + x;
-          if (out.a_o) out.a_o[po] = sa;
-          if (out.pc) out.pc[po] = pc;
+          if (out.a_o || out.pc) {
+            const size_t po = (((size_t)b * O + o) * H + y) * W + x;
+            if (out.a_o) out.a_o[po] = sa;
+            if (out.pc) out.pc[po] = pc;
+          }
         }
       }
       __syncthreads();
@@ -744,9 +765,9 @@ static cudaError_t launch_amp0(const float2* Q, float2* R0, float* amp0, unsigne
   return cudaGetLastError();
 }
 
-template <int G>
-static cudaError_t launch_pc(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
-                             const FieldsConst& c, cudaStream_t st) {
+template <int G, int SC>
+static cudaError_t launch_pc_s(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
+                               const FieldsConst& c, cudaStream_t st) {
   const size_t PLb = padded_len(c.W) * sizeof(float2);
   const size_t budget = 200 * 1024;
   int rr, ops;
@@ -764,11 +785,18 @@ static cudaError_t launch_pc(const float2* Q, const float2* R0, const float* thr
     nbuf = c.S + 1;
   }
   const size_t smem = nbuf * PLb;
-  cudaError_t e = set_smem(k_rows_pc<G>, smem);
+  cudaError_t e = set_smem(k_rows_pc<G, SC>, smem);
   if (e != cudaSuccess) return e;
   dim3 grid((c.H + 1) / 2, c.B);
-  k_rows_pc<G><<<grid, kThreads, smem, st>>>(Q, R0, thr, out, c, rr, ops);
+  k_rows_pc<G, SC><<<grid, kThreads, smem, st>>>(Q, R0, thr, out, c, rr, ops);
   return cudaGetLastError();
+}
+
+template <int G>
+static cudaError_t launch_pc(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
+                             const FieldsConst& c, cudaStream_t st) {
+  if (c.S == 4 && G >= 8 && G <= 64) return launch_pc_s<G, 4>(Q, R0, thr, out, c, st);
+  return launch_pc_s<G, 0>(Q, R0, thr, out, c, st);
 }
 
 #define R2_DISPATCH_G(g, FN, ...)                       \
