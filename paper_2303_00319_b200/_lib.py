@@ -12,7 +12,8 @@ import threading
 
 from .errors import ParameterError, RiftError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "librift2_b200.so")
+_LIB_PATH = os.environ.get("RIFT2_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "librift2_b200.so")
 
 _c_int = ctypes.c_int32
 _c_p = ctypes.c_void_p

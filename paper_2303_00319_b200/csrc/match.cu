@@ -34,11 +34,25 @@ constexpr int BM = 128;            // target rows per CTA (UMMA M)
 constexpr int BN = 128;            // reference columns per tile (UMMA N)
 constexpr int BK = 64;             // fp16 elements per 128-byte swizzle atom
 constexpr int KBOX = 4;            // K boxes of 64 -> 256 >= 224
-constexpr int TILE_BYTES = BM * BK * 2;        // 16 KB per box
-constexpr int OPER_BYTES = KBOX * TILE_BYTES;  // 64 KB per operand tile
+constexpr int A_BOX = BM * BK * 2;             // 16 KB per K box
+constexpr int B_BOX = BN * BK * 2;             // 8 KB per K box
+constexpr int A_BYTES = KBOX * A_BOX;          // 64 KB, resident
+constexpr int B_BYTES = KBOX * B_BOX;          // 32 KB per stage
 constexpr int STAGES = 2;
-constexpr int GEMM_THREADS = 192;
-constexpr int SMEM_GEMM = OPER_BYTES * (1 + STAGES) + 1024 + 256;
+constexpr int NACC = 4;                        // TMEM accumulator buffers
+constexpr int TMEM_COLS = NACC * BN;
+constexpr int NEPI = BN / 32 * 4;             // epilogue warps: 4 lane quarters x BN/32 column blocks
+constexpr int GEMM_THREADS = 64 + NEPI * 32;  // producer, MMA, epilogue warps
+constexpr int BAR_OFF = A_BYTES + STAGES * B_BYTES;
+constexpr int SMEM_GEMM = BAR_OFF + 256 + NEPI * 64 * 4 + 4 * (NEPI / 4 - 1) * BM * 4 + 1024;
+
+#ifdef R2_GEMM_TRACE
+// development trace: clock64 stamps of the pipeline roles of CTA (0, 0)
+__device__ unsigned long long g_trace[8][512];
+#define R2_TR(ev, i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (i) < 512) g_trace[ev][i] = clock64(); } while (0)
+#else
+#define R2_TR(ev, i) do {} while (0)
+#endif
 
 struct Part {
   int D;      // integer dot product
@@ -59,10 +73,12 @@ R2_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 R2_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread sleeps in hardware
+// instead of spinning and stealing issue slots from the epilogue warps
 R2_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
       "@!p bra WAIT_%=;\n}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 R2_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -133,20 +149,55 @@ struct GemmParams {
   Part* part;   // [n_pairs][cap][splits]
 };
 
+// screening factor 1/|c_r| (0 for an empty descriptor); same formula everywhere
+R2_DEV float inv_norm(int q) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)q));
+  return q > 0 ? r : 0.f;
+}
+
+// exact running-best update with one candidate column (ties keep the earlier column)
+R2_DEV void take_exact(float D, int qq, float sj, int col, float& best, float& bestD, int& bestq, int& bestcol) {
+  if (bestcol < 0 || sj > best * (1.f + 1e-5f)) {
+    best = sj; bestD = D; bestcol = col; bestq = qq;
+  } else if (sj >= best * (1.f - 1e-5f)) {
+    if (cmp_exact(D, qq, bestD, bestq) > 0) { best = sj; bestD = D; bestcol = col; bestq = qq; }
+  }
+}
+
+// fold a pending chunk (raw dot products rv of columns c0..c0+31, screening
+// maximum rcm) into the exact best, columns in increasing order
+R2_DEV void resolve_chunk(const float (&rv)[32], int c0, float rcm, int n_r, const int* __restrict__ sq,
+                          float& best, float& bestD, int& bestq, int& bestcol) {
+  const float lo = fmaxf(rcm, best) * (1.f - 1e-5f);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int col = c0 + j;
+    if (col < n_r) {
+      const int qq = __ldg(&sq[col]);
+      const float sj = rv[j] * inv_norm(qq);
+      if (sj >= lo) take_exact(rv[j], qq, sj, col, best, bestD, bestq, bestcol);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-k_match_gemm(const __grid_constant__ CUtensorMap tmap, GemmParams p) {
+k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-B alignment for SWIZZLE_128B, as an offset so the pointer keeps its shared address space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + OPER_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OPER_BYTES * (1 + STAGES));
+  uint8_t* sB = smem + A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* a_full = bars + 2 * STAGES;
-  uint64_t* t_full = a_full + 1;         // [2]
-  uint64_t* t_empty = t_full + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
-  float* s_inv = reinterpret_cast<float*>(tmem_slot + 4);   // [4 warps][BN]   (placed after bars)
+  uint64_t* t_full = a_full + 1;         // [NACC]
+  uint64_t* t_empty = t_full + NACC;     // [NACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + NACC);
+  float* s_inv = reinterpret_cast<float*>(smem + BAR_OFF + 256);   // [NEPI warps][2][32], 16-B aligned
+  float* s_mrg_f = s_inv + NEPI * 64;                              // [2][NB-1][BM] best / D of blocks 1..
+  int* s_mrg_i = reinterpret_cast<int*>(s_mrg_f + 2 * (NEPI / 4 - 1) * BM);   // [2][NB-1][BM] q / column
 
   const int pair = blockIdx.y;
   const int split = blockIdx.x % p.splits;
@@ -175,12 +226,14 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmap, GemmParams p) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(a_full, 1);
-    for (int s = 0; s < 2; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 4); }
+    for (int s = 0; s < NACC; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], NEPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tmapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tmapB) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" :: "r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(tmem_slot)), "n"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -191,15 +244,17 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmap, GemmParams p) {
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer
-      mbar_expect_tx(a_full, OPER_BYTES);
-      for (int kb = 0; kb < KBOX; ++kb) tma_load_2d(sA + kb * TILE_BYTES, &tmap, kb * BK, rowA, a_full);
+      mbar_expect_tx(a_full, A_BYTES);
+      for (int kb = 0; kb < KBOX; ++kb) tma_load_2d(sA + kb * A_BOX, &tmapA, kb * BK, rowA, a_full);
       for (int i = 0; i < ntiles; ++i) {
         const int s = i % STAGES;
+        R2_TR(0, i);
         mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-        mbar_expect_tx(&full[s], OPER_BYTES);
+        R2_TR(1, i);
+        mbar_expect_tx(&full[s], B_BYTES);
         const int rowB = rowB0 + (nt0 + i) * BN;
         for (int kb = 0; kb < KBOX; ++kb)
-          tma_load_2d(sB + s * OPER_BYTES + kb * TILE_BYTES, &tmap, kb * BK, rowB, &full[s]);
+          tma_load_2d(sB + s * B_BYTES + kb * B_BOX, &tmapB, kb * BK, rowB, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -208,87 +263,150 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmap, GemmParams p) {
       mbar_wait(a_full, 0);
       const uint32_t a_base = smem_u32(sA);
       for (int i = 0; i < ntiles; ++i) {
-        const int s = i % STAGES, acc = i & 1;
+        const int s = i % STAGES, acc = i % NACC;
+        R2_TR(2, i);
         mbar_wait(&full[s], (i / STAGES) & 1);
-        mbar_wait(&t_empty[acc], ((i >> 1) & 1) ^ 1);
+        R2_TR(3, i);
+        mbar_wait(&t_empty[acc], ((i / NACC) & 1) ^ 1);
+        R2_TR(4, i);
         tc_fence_after();
-        const uint32_t b_base = smem_u32(sB + s * OPER_BYTES);
+        const uint32_t b_base = smem_u32(sB + s * B_BYTES);
         const uint32_t d = tmem + acc * BN;
 #pragma unroll
         for (int ks = 0; ks < 14; ++ks) {
-          const uint32_t off = (ks >> 2) * TILE_BYTES + (ks & 3) * 32;
-          mma_f16(d, smem_desc(a_base + off), smem_desc(b_base + off), ks > 0 ? 1u : 0u);
+          const uint32_t ka = (ks >> 2) * A_BOX + (ks & 3) * 32;
+          const uint32_t kb = (ks >> 2) * B_BOX + (ks & 3) * 32;
+          mma_f16(d, smem_desc(a_base + ka), smem_desc(b_base + kb), ks > 0 ? 1u : 0u);
         }
         mma_commit(&empty[s]);
         mma_commit(&t_full[acc]);
+        R2_TR(5, i);
       }
     }
   } else {
-    // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
-    const int q = warp & 3;
+    // ---- epilogue warps 2..17: TMEM lane quarter = warp % 4, 32-column block = (warp-2) / 4
+    //
+    // Per row (lane) the warp keeps an exactly-resolved best E = (bestD, bestq,
+    // bestcol, best) and at most one *pending* chunk R: the 32 raw dot products
+    // rv[] of the chunk whose screening maximum r_cm is the largest seen so far.
+    // Screening scores s = D * rsqrt(q) carry < 2e-7 relative error, so with a
+    // 1e-5 window a chunk is either (a) strictly below every candidate (skip),
+    // (b) strictly above all of them (it replaces R and E: a copy, no exact
+    // work), or (c) a near tie: only then is R resolved exactly into E before
+    // the new chunk becomes R.  R is resolved once more after the last tile.
+    // Record events are rare per row (~ln n) but frequent per warp, so (b)
+    // is kept branch-light; exact work happens only for (c) and at the end.
+    constexpr int NB = NEPI / 4;                    // column blocks per tile (BN / 32)
+    const int e = warp - 2;
+    const int q = warp & 3, h = e >> 2;
     const int row_loc = q * 32 + lane;
     const int row = mt * BM + row_loc;
-    float* inv = s_inv + (warp - 2) * BN;
+    float* inv_buf = s_inv + e * 64;                // two 32-float buffers (current / next tile)
+    const int* sq = p.sqnorm + (size_t)rb * p.cap;
     float best = -1.f, bestD = 0.f;
     int bestq = 1, bestcol = -1;
-    for (int i = 0; i < ntiles; ++i) {
-      const int acc = i & 1;
-      const int col0 = (nt0 + i) * BN;
-      // stage 1/|c_r| of this tile's columns (per warp)
-      for (int j = lane; j < BN; j += 32) {
-        const int c = col0 + j;
-        inv[j] = c < n_r ? rsqrtf((float)__ldg(&p.sqnorm[(size_t)rb * p.cap + c])) : 0.f;
-      }
-      __syncwarp();
-      mbar_wait(&t_full[acc], (i >> 1) & 1);
-      tc_fence_after();
-      const int nvalid = min(BN, n_r - col0);
-#pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, v);
-        if (ch * 32 >= nvalid) continue;
-        float cm = -2.f;
+    float rv[32];
+    float r_cm = -1.f;
+    int r_c0 = -1;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float s = (ch * 32 + j < nvalid) ? v[j] * inv[ch * 32 + j] : -2.f;
-          cm = fmaxf(cm, s);
+    for (int j = 0; j < 32; ++j) rv[j] = 0.f;
+    int q_nxt;
+    {
+      const int c = nt0 * BN + h * 32 + lane;
+      q_nxt = c < n_r ? __ldg(&sq[c]) : 0;          // first tile's squared norms
+    }
+    // iteration i == ntiles is virtual: it only resolves the pending chunk
+    // (one call site for the exact path keeps the code and register use small)
+    for (int i = 0;; ++i) {
+      const bool last = i == ntiles;
+      const int acc = i % NACC;
+      const int c0 = (nt0 + i) * BN + h * 32;
+      float v[32];
+      bool rec = false, near = last;
+      float cm = 0.f;
+      if (!last) {
+        float* ic = inv_buf + (i & 1) * 32;
+        ic[lane] = inv_norm(q_nxt);
+        {
+          const int c = c0 + BN + lane;
+          q_nxt = (i + 1 < ntiles && c < n_r) ? __ldg(&sq[c]) : 0;   // next tile, in flight
         }
-        if (cm >= best * (1.f - 1e-5f)) {
-          for (int j = 0; j < 32; ++j) {
-            const int jj = ch * 32 + j;
-            if (jj >= nvalid) break;
-            const float s = v[j] * inv[jj];
-            if (s > best * (1.f + 1e-5f) || bestcol < 0) {
-              best = s; bestD = v[j]; bestcol = col0 + jj;
-              bestq = __ldg(&p.sqnorm[(size_t)rb * p.cap + bestcol]);
-            } else if (s >= best * (1.f - 1e-5f)) {
-              const int qq = __ldg(&p.sqnorm[(size_t)rb * p.cap + col0 + jj]);
-              if (cmp_exact(v[j], qq, bestD, bestq) > 0) {
-                best = s; bestD = v[j]; bestcol = col0 + jj; bestq = qq;
-              }
-            }
+        __syncwarp();
+        if (e == 0 && lane == 0) R2_TR(6, i);
+        mbar_wait(&t_full[acc], (i / NACC) & 1);
+        if (e == 0 && lane == 0) R2_TR(7, i);
+        tc_fence_after();
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + h * 32, v);
+        // the chunk is in registers: hand the accumulator back to the MMA warp now
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[acc]);
+        if (c0 < n_r) {                               // warp-uniform
+          // screening maximum; invalid tail columns carry inv = 0 (score 0)
+          const float4* iv = reinterpret_cast<const float4*>(ic);
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 f = iv[q4];
+            const float2 a = __fmul2_rn(make_float2(v[4 * q4 + 0], v[4 * q4 + 1]), make_float2(f.x, f.y));
+            const float2 b = __fmul2_rn(make_float2(v[4 * q4 + 2], v[4 * q4 + 3]), make_float2(f.z, f.w));
+            cm = fmaxf(fmaxf(cm, a.x), a.y);
+            cm = fmaxf(fmaxf(cm, b.x), b.y);
           }
+          const float T = fmaxf(r_cm, best);
+          rec = cm > T * (1.f + 1e-5f);               // for T < 0 (nothing yet) always true
+          near = !rec && cm >= T * (1.f - 1e-5f);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[acc]);
+      if (__any_sync(0xffffffffu, rec || near)) {
+        if (near && r_c0 >= 0)
+          resolve_chunk(rv, r_c0, r_cm, n_r, sq, best, bestD, bestq, bestcol);
+        if (last) break;
+        if (rec) { best = -1.f; bestD = 0.f; bestq = 1; bestcol = -1; }
+        const bool take = rec || near;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) rv[j] = take ? v[j] : rv[j];
+        r_cm = take ? cm : r_cm;
+        r_c0 = take ? c0 : r_c0;
+      }
     }
-    if (row < n_t) {
-      Part r;
-      r.D = (int)bestD;
-      r.q = bestq;
-      r.kp = bestcol >= 0 ? __ldg(&p.kp[(size_t)rb * p.cap + bestcol]) : -1;
-      r.s = best;
-      out[(size_t)row * p.splits + split] = r;
+    // merge the NB column blocks of each row (exact; ties -> smaller column = smaller kp id)
+    if (h > 0) {
+      const int sidx = (h - 1) * BM + row_loc;
+      s_mrg_f[sidx] = best;
+      s_mrg_f[(NB - 1) * BM + sidx] = bestD;
+      s_mrg_i[sidx] = bestq;
+      s_mrg_i[(NB - 1) * BM + sidx] = bestcol;
+    }
+    named_sync(1, NEPI * 32);
+    if (h == 0) {
+      for (int o = 0; o < NB - 1; ++o) {
+        const int sidx = o * BM + row_loc;
+        const float ob = s_mrg_f[sidx], oD = s_mrg_f[(NB - 1) * BM + sidx];
+        const int oq = s_mrg_i[sidx], oc = s_mrg_i[(NB - 1) * BM + sidx];
+        if (oc < 0) continue;
+        bool take;
+        if (bestcol < 0) take = true;
+        else {
+          const int r = cmp_exact(oD, oq, bestD, bestq);
+          take = r > 0 || (r == 0 && oc < bestcol);
+        }
+        if (take) { best = ob; bestD = oD; bestq = oq; bestcol = oc; }
+      }
+      if (row < n_t) {
+        Part r;
+        r.D = (int)bestD;
+        r.q = bestq;
+        r.kp = bestcol >= 0 ? __ldg(&p.kp[(size_t)rb * p.cap + bestcol]) : -1;
+        r.s = best;
+        out[(size_t)row * p.splits + split] = r;
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" :: "r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(TMEM_COLS));
   }
 }
 
@@ -584,23 +702,38 @@ int match_run(const MatchArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
 
   auto encode = get_encode();
   if (!encode) return 3;
-  CUtensorMap tmap;
+  // one descriptor-array tensor map per box shape: A = 128 target rows, B = 64 reference rows
+  CUtensorMap tmapA, tmapB;
   cuuint64_t dims[2] = {(cuuint64_t)a.stride, (cuuint64_t)n_blocks * a.cap};
   cuuint64_t strides[1] = {(cuuint64_t)a.stride * 2};
-  cuuint32_t box[2] = {BK, BM};
+  cuuint32_t boxA[2] = {BK, BM}, boxB[2] = {BK, BN};
   cuuint32_t estr[2] = {1, 1};
-  CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a.counts), dims, strides,
-                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult cr = encode(&tmapA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a.counts), dims, strides,
+                       boxA, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return 3;
+  cr = encode(&tmapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a.counts), dims, strides, boxB, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return 3;
 
   const int m_tiles = (a.cap + BM - 1) / BM;
-  int splits = (2 * 148 + a.n_pairs * m_tiles - 1) / (a.n_pairs * m_tiles);
+  // split the reference range only as far as needed to put one CTA on every SM:
+  // a CTA that sees few column tiles keeps a weak running best and pays the
+  // exact-candidate path far more often (~32/(i+1) columns per tile i)
+  const int n_tiles_cap = (a.cap + BN - 1) / BN;
+  const int ctas = m_tiles * a.n_pairs;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  int splits = (n_sm + ctas - 1) / ctas;
+  const int max_split = n_tiles_cap / 4 > 1 ? n_tiles_cap / 4 : 1;
+  splits = splits > max_split ? max_split : splits;
   splits = splits < 1 ? 1 : (splits > kMaxSplits ? kMaxSplits : splits);
   GemmParams gp{a.sqnorm, a.kp, a.count, a.ref_block, a.tgt_block, a.cap, splits, part};
-  cudaFuncSetAttribute(k_match_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_GEMM + 4 * BN * 4);
+  cudaFuncSetAttribute(k_match_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_GEMM);
   dim3 grid(m_tiles * splits, a.n_pairs);
-  k_match_gemm<<<grid, GEMM_THREADS, SMEM_GEMM + 4 * BN * 4, st>>>(tmap, gp);
+  k_match_gemm<<<grid, GEMM_THREADS, SMEM_GEMM, st>>>(tmapA, tmapB, gp);
   k_match_index<<<a.n_pairs, 1024, 0, st>>>(a, iw);
   {
     dim3 g2((a.cap + 7) / 8, a.n_pairs);
@@ -654,3 +787,9 @@ int match_vectors_run(const double* R, const int* rkp, int nr, const double* T, 
 }
 
 }  // namespace r2
+
+#ifdef R2_GEMM_TRACE
+extern "C" int rift2_debug_gemm_trace(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, r2::g_trace, sizeof(r2::g_trace)) == cudaSuccess ? 0 : 3;
+}
+#endif
