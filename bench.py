@@ -96,21 +96,104 @@ def cpu_workers():
     return max(1, min(n, 16))
 
 
+UNITS = ("fields(ref)", "fields(tgt)", "features(ref)", "features(tgt)", "match")
+
+
+def _unit_worker(conn, size, seed0, stride):
+    """Persistent CPU worker for --impl reference: holds one pair's state and
+    runs one pipeline unit per request (test infrastructure: the oracle)."""
+    from oracle import rift2_oracle as O
+    from paper_2303_00319_b200 import synth
+    bank = O.Bank(**BASE_PARAMS)
+    pair, st = 0, {}
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            return
+        if msg == "gen":
+            st = {"img": synth.make_pair(size, seed0 + pair * stride)[:2]}
+            conn.send(0.0)
+            continue
+        t0 = time.perf_counter()
+        if msg in (0, 1):
+            st[f"f{msg}"] = O.fields(st["img"][msg], bank, workers=1)
+        elif msg in (2, 3):
+            f = st[f"f{msg - 2}"]
+            kp = O.detect_keypoints(f["moment_min"], f["moment_max"], 0.001, 5000, 96)
+            c, k, _, _ = O.describe_rift2(f["mim"], kp)
+            st[f"d{msg - 2}"] = (c / np.linalg.norm(c, axis=1, keepdims=True), k)
+        else:
+            (rv, rk), (tv, tk) = st["d0"], st["d1"]
+            O.match_nn(rv, rk, tv, tk)
+            pair += 1
+        conn.send(time.perf_counter() - t0)
+
+
+class UnitPool:
+    def __init__(self, n, size):
+        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "RIFT2_THREADS"):
+            os.environ[k] = "1"
+        ctx = mp.get_context("spawn")
+        self.conns, self.procs = [], []
+        for w in range(n):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_unit_worker, args=(b, size, w, n), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        self.unit = 0
+
+    def step(self):
+        """One step = the next unit on every worker; returns the wall time."""
+        if self.unit == 0:
+            for c in self.conns:                  # generation is outside the timed step
+                c.send("gen")
+            for c in self.conns:
+                c.recv()
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send(self.unit)
+        for c in self.conns:
+            c.recv()
+        wall = time.perf_counter() - t0
+        u, self.unit = self.unit, (self.unit + 1) % len(UNITS)
+        return u, wall
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.procs:
+            p.join(timeout=30)
+
+
 def run_reference(args, rank, world):
+    """The reference's CPU path (the oracle port, pinned to the reference by
+    golden vectors) on all host cores.  A step is one fifth of a pair on
+    every worker (UNITS, round robin) so the run stays within minutes;
+    pairs/s = workers / sum over units of the mean unit wall time."""
     if rank != 0:
         return
     n = cpu_workers()
-    for _ in range(min(args.warmup, 1)):
-        cpu_sample(args.size, n)
-    rates, walls = [], []
-    for s in range(args.steps):
-        r, w, _ = cpu_sample(args.size, n, seed0=s * n)
-        rates.append(r)
-        walls.append(w)
-    value = sum(n for _ in rates) / sum(walls)
-    sample = f"{n} pairs per step ({n} worker processes x 1 pair, {args.size}^2, full oracle pipeline)"
+    pool = UnitPool(n, args.size)
+    try:
+        for _ in range(args.warmup):
+            pool.step()
+        steps = max(args.steps, len(UNITS))
+        by_unit = {u: [] for u in range(len(UNITS))}
+        walls = []
+        for _ in range(steps):
+            u, w = pool.step()
+            by_unit[u].append(w)
+            walls.append(w)
+    finally:
+        pool.close()
+    per_pair = sum(statistics.mean(v) for v in by_unit.values())
+    value = n / per_pair
+    sample = (f"{n} worker processes x 1 thread; each step runs one of {len(UNITS)} units of a {args.size}^2 "
+              f"pair ({', '.join(UNITS)}) on every worker; {steps} steps; pairs/s = workers / sum of mean unit "
+              f"walls ({per_pair:.1f} s per pair per worker)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
-            "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * statistics.mean(walls),
+            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload(args, world),
             "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": n, "kind": "port", "sample": sample},
@@ -170,6 +253,37 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def rank_seed0(rank, pairs):
+    """First generator seed of this rank's pairs: ranks own disjoint, contiguous
+    seed ranges (configs[2]: the 128-pair batch split over the GPUs)."""
+    return rank * pairs
+
+
+def max_over_ranks(values, world, device):
+    """Element-wise max of per-rank timings (the slowest rank defines a step)."""
+    import torch
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def traffic():
+    """Filter-bank DRAM bytes per pass from the newest committed ncu launch
+    list (profiles/rNN_launches.json, written by tools/profile_summary.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_launches.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as fh:
+            p = json.load(fh)
+        return float(p["filter_bank"]["dram_bytes_per_pass"]), os.path.relpath(files[-1], ROOT)
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -177,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     cfg = RiftConfig(**BASE_PARAMS)
-    imgs, _ = synth.make_batch(args.pairs, args.size, seed0=rank * args.pairs)
+    imgs, _ = synth.make_batch(args.pairs, args.size, seed0=rank_seed0(rank, args.pairs))
     pipe = BatchPipeline(args.pairs, args.size, args.size, cfg)
     pipe.load(imgs)
     pipe.capture()
@@ -205,37 +319,28 @@ def run_ours(args, rank, world, local_rank):
     total_ms = ev[0][0].elapsed_time(ev[K - 1][2])
     fields_ms = sum(ev[i][0].elapsed_time(ev[i][1]) for i in range(K)) / K
 
-    # e2e: public API with host buffers (pinned H2D of the step's images, D2H of the matches)
+    # e2e: public API with host buffers -- every step uploads its images from
+    # pinned host memory (copy stream, double-buffered against the previous
+    # step's compute) and reads the match arrays back
     host_in = torch.from_numpy(imgs).pin_memory()
     out_keys = ("ref", "tgt", "dist", "count")
     host_out = {k: torch.empty(pipe.m[k].shape, dtype=pipe.m[k].dtype).pin_memory() for k in out_keys}
     h2d = host_in.numel() * 4
     d2h = sum(pipe.m[k].numel() * pipe.m[k].element_size() for k in out_keys)
-    for _ in range(2):
-        pipe.images.copy_(host_in, non_blocking=True)
-        pipe.step()
-        for k in out_keys:
-            host_out[k].copy_(pipe.m[k], non_blocking=True)
+    pipe.run_from_host(host_in, 2, host_out)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     KE = max(3, K // 3)
     e0.record()
-    for _ in range(KE):
-        pipe.images.copy_(host_in, non_blocking=True)
-        pipe.step()
-        for k in out_keys:
-            host_out[k].copy_(pipe.m[k], non_blocking=True)
+    pipe.run_from_host(host_in, KE, host_out)
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     clocks = clk.stop()
 
-    t = torch.tensor([total_ms, e2e_ms, fields_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, e2e_ms, fields_ms = t.tolist()
+    total_ms, e2e_ms, fields_ms = max_over_ranks([total_ms, e2e_ms, fields_ms], world, "cuda")
     if rank != 0:
         return
     pairs = args.pairs * world * K
@@ -244,6 +349,9 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_src = peaks()
     bytes_launch = BYTES_PER_PX * args.size * args.size * 2 * args.pairs
     achieved = bytes_launch / (fields_ms / 1e3) / 1e9
+    tr, tr_src = traffic()
+    if tr is not None and (args.pairs, args.size) != (16, 1024):
+        tr = tr * (args.pairs * args.size * args.size) / (16 * 1024 * 1024)   # profile is per 16 pairs of 1024^2
     counts = pipe.m["count"].cpu().numpy()
     line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
@@ -253,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": pipe.KERNELS_PER_STEP * K,
             "roofline": {"bound": "hbm", "kernel": "filter bank (rows_fwd+cols+rows_amp0+median+rows_pc)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "bytes_per_launch": bytes_launch, "launch_ms": fields_ms,
+                         "traffic": tr, "traffic_source": tr_src, "bytes_per_launch": bytes_launch, "launch_ms": fields_ms,
                          "share_of_step": fields_ms / (total_ms / K), "peak_source": peak_src},
             "clocks": clocks,
             "matches_per_pair": float(np.mean(counts))}

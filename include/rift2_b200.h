@@ -133,7 +133,9 @@ int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_
  *   out_ref, out_tgt [n_pairs][tgt_kp_capacity] int32 out (keypoint ids)
  *   out_dist         [n_pairs][tgt_kp_capacity] float64 out
  *   out_count        [n_pairs] int32 out (= number of target keypoints
- *                    with a descriptor)
+ *                    with a descriptor, at most tgt_kp_capacity; 0 when the
+ *                    pair's reference set is empty -- the dataclass API
+ *                    raises ParameterError there, ref: matcher.py:105-106)
  * Pairs are sorted by (dist, ref, tgt) as the reference returns them.
  * Ranking is exact: candidates are compared on integer dot products and
  * squared norms, ties resolve to the smallest reference keypoint id. */

@@ -53,6 +53,8 @@ class BatchPipeline:
         self.tb = self.rb + 1
         self.dim = self.cfg.grid * self.cfg.grid * self.cfg.n_orient
         self.graphs = None
+        self._alt = None
+        self._copy_stream = None
 
     # ---- stages (eager) --------------------------------------------------
     def run_fields(self):
@@ -76,20 +78,32 @@ class BatchPipeline:
 
     # ---- graphs ------------------------------------------------------------
     def capture(self):
-        """Warm up (allocates workspaces and cached tables), then capture."""
+        """Warm up (allocates workspaces and cached tables), then capture.
+
+        Three graphs: the filter bank on each of two image buffers (so a
+        host upload can fill one while the other is being read) and the
+        detect + describe + match group."""
         self.run()
         torch.cuda.synchronize()
+        if self._alt is None:
+            self._alt = torch.zeros_like(self.images)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        g_a, g_b, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
-            with torch.cuda.graph(g1, stream=s):
+            with torch.cuda.graph(g_a, stream=s):
                 self.run_fields()
+            self.images, self._alt = self._alt, self.images
+            try:
+                with torch.cuda.graph(g_b, stream=s):
+                    self.run_fields()
+            finally:
+                self.images, self._alt = self._alt, self.images
             with torch.cuda.graph(g2, stream=s):
                 self.run_features()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        self.graphs = (g1, g2)
+        self.graphs = (g_a, g2, g_b)
         return self
 
     def replay_fields(self):
@@ -104,6 +118,44 @@ class BatchPipeline:
         else:
             self.graphs[0].replay()
             self.graphs[1].replay()
+
+    def run_from_host(self, host_images, steps: int, host_out: dict | None = None):
+        """End-to-end steps from host memory: step i uploads host_images[i %
+        len] (pinned (B, H, W) float32 tensors) on a copy stream into one of
+        two device buffers while the previous step computes, runs the whole
+        pipeline on the current stream, and copies the match arrays back into
+        `host_out` (pinned tensors shaped like `self.m`).  Enqueues only; the
+        caller synchronises."""
+        if self.graphs is None:
+            self.capture()
+        if not isinstance(host_images, (list, tuple)):
+            host_images = [host_images]
+        cs = torch.cuda.current_stream()
+        xs = self._copy_stream = self._copy_stream or torch.cuda.Stream()
+        bufs = (self.images, self._alt)
+        fields_graph = (self.graphs[0], self.graphs[2])
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        done = [torch.cuda.Event(), torch.cuda.Event()]
+        xs.wait_stream(cs)
+        with torch.cuda.stream(xs):
+            bufs[0].copy_(host_images[0], non_blocking=True)
+            ready[0].record(xs)
+        for i in range(steps):
+            b = i % 2
+            if i + 1 < steps:
+                with torch.cuda.stream(xs):
+                    if i >= 1:
+                        xs.wait_event(done[1 - b])           # step i-1 finished reading that buffer
+                    bufs[1 - b].copy_(host_images[(i + 1) % len(host_images)], non_blocking=True)
+                    ready[1 - b].record(xs)
+            cs.wait_event(ready[b])
+            fields_graph[b].replay()
+            done[b].record(cs)
+            self.graphs[1].replay()
+            if host_out is not None:
+                for k, t in host_out.items():
+                    t.copy_(self.m[k], non_blocking=True)
+        cs.wait_stream(xs)
 
     # ---- results -----------------------------------------------------------
     def matches_host(self):

@@ -7,12 +7,16 @@
 //
 //   k_match_gemm  D = C_tgt . C_ref^T on fp16 counts (exact: counts <= 256,
 //                 dots < 2^24) with tcgen05.mma (M=128 tgt rows, N=128 ref
-//                 columns, K=224 in 14 steps) into a double-buffered TMEM
-//                 accumulator; operands staged by TMA (128B swizzle); one
-//                 warp produces, one warp issues MMA, four epilogue warps
-//                 tcgen05.ld the tile and keep a running exact argmax per
-//                 target row (fp32 screen, integer D^2 q comparison inside a
-//                 1e-5 window, ties to the smallest reference keypoint id).
+//                 columns, K=224 in 14 steps) into NACC=4 TMEM accumulators;
+//                 A (the CTA's target rows) resident in smem, B double
+//                 buffered, both staged by TMA (128B swizzle).  Warp 0
+//                 produces, warp 1 issues MMA, 16 epilogue warps (4 TMEM lane
+//                 quarters x 4 32-column blocks) tcgen05.ld their chunk and
+//                 keep an exact running argmax per target row: an fp32
+//                 screen (FMUL2 + FMNMX3), a pending-chunk copy on a new
+//                 maximum, and integer D^2 q comparisons only for near ties
+//                 (1e-5 window) and once at the end; ties go to the smallest
+//                 reference column (= keypoint id order).
 //   k_match_index per pair: target variant groups, reference keypoint ranges
 //   k_match_combine per target keypoint: best over its variants and over the
 //                 column splits (exact 128-bit comparison), then the exact
@@ -35,9 +39,9 @@ constexpr int BN = 128;            // reference columns per tile (UMMA N)
 constexpr int BK = 64;             // fp16 elements per 128-byte swizzle atom
 constexpr int KBOX = 4;            // K boxes of 64 -> 256 >= 224
 constexpr int A_BOX = BM * BK * 2;             // 16 KB per K box
-constexpr int B_BOX = BN * BK * 2;             // 8 KB per K box
+constexpr int B_BOX = BN * BK * 2;             // 16 KB per K box
 constexpr int A_BYTES = KBOX * A_BOX;          // 64 KB, resident
-constexpr int B_BYTES = KBOX * B_BOX;          // 32 KB per stage
+constexpr int B_BYTES = KBOX * B_BOX;          // 64 KB per stage
 constexpr int STAGES = 2;
 constexpr int NACC = 4;                        // TMEM accumulator buffers
 constexpr int TMEM_COLS = NACC * BN;
@@ -453,7 +457,9 @@ __global__ void __launch_bounds__(1024) k_match_index(MatchArgs a, IdxWs w) {
     if (threadIdx.x == 0) s_base += s_tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) { w.ng[pair] = s_base; gs[s_base] = n_t; }
+  // an empty reference set matches nothing (the dataclass API raises instead,
+  // ref: matcher.py:105-106; a batch slot simply reports 0 matches)
+  if (threadIdx.x == 0) { w.ng[pair] = n_r > 0 ? s_base : 0; gs[s_base] = n_t; }
 }
 
 // a beats b across target variants: Da^2 q_rb q_tb > Db^2 q_ra q_ta (128-bit)
@@ -535,7 +541,7 @@ __global__ void __launch_bounds__(1024) k_match_sort(MatchArgs a, IdxWs w, K128*
     a.out_ref[o] = (int32_t)(k[i].lo >> 32);
     a.out_tgt[o] = (int32_t)(k[i].lo & 0xffffffffull);
   }
-  if (threadIdx.x == 0) a.out_count[pair] = ng;
+  if (threadIdx.x == 0) a.out_count[pair] = n;
 }
 
 // ------------------------------------------------ generic float64 vectors

@@ -192,7 +192,7 @@ def _match_gpu(eng, ref_counts, ref_kp, tgt_counts, tgt_kp):
                 count=torch.tensor([len(ref_kp), len(tgt_kp)], dtype=torch.int32).cuda())
     rb = torch.tensor([0], dtype=torch.int32).cuda()
     tb = torch.tensor([1], dtype=torch.int32).cuda()
-    out = eng.match(desc, 216, rb, tb, int(tgt_kp.max()) + 1)
+    out = eng.match(desc, 216, rb, tb, int(tgt_kp.max()) + 1 if len(tgt_kp) else 1)
     torch.cuda.synchronize()
     n = int(out["count"][0])
     return (out["ref"][0][:n].cpu().numpy(), out["tgt"][0][:n].cpu().numpy(),
