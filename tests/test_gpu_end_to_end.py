@@ -1,0 +1,84 @@
+"""End-to-end agreement of the whole GPU pipeline with the CPU oracle.
+
+north_star: "the match set overlaps >= 99%" and (configs[4], the rotation
+sweep) "per-theta agreement of dominant index and match sets with the CPU
+oracle".  The GPU runs its own fp32 filter bank, so keypoints can differ
+where two FAST responses are within fp32 noise; matches are therefore
+compared as coordinate pairs ((x_ref, y_ref), (x_tgt, y_tgt)).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import rift2_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+BASE = dict(scale_mult=1.6, sigma_on_f=0.75)
+
+
+@pytest.fixture(scope="module")
+def r2():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2303_00319_b200 as r2
+    return r2
+
+
+def _oracle_side(img, max_points):
+    f = O.fields(img, O.Bank(**BASE), workers=8)
+    kp = O.detect_keypoints(f["moment_min"], f["moment_max"], 0.001, max_points, 96)
+    c, k, v, _ = O.describe_rift2(f["mim"], kp)
+    return kp, c, k, v
+
+
+def _oracle_matches(a, b, max_points):
+    (rkp, rc, rk, rv), (tkp, tc, tk, tv) = _oracle_side(a, max_points), _oracle_side(b, max_points)
+    pairs, _ = O.match_nn(rc / np.linalg.norm(rc, axis=1, keepdims=True), rk,
+                          tc / np.linalg.norm(tc, axis=1, keepdims=True), tk)
+    m = {((int(rkp["x"][r]), int(rkp["y"][r])), (int(tkp["x"][t]), int(tkp["y"][t]))) for r, t, _ in pairs}
+    dom = {(int(rkp["x"][k]), int(rkp["y"][k])): int(v) for k, v in zip(rk[::-1], rv[::-1])}   # first variant
+    return m, dom
+
+
+def _gpu_matches(r2, a, b, max_points):
+    cfg = r2.RiftConfig(max_keypoints=max_points, **BASE)
+    res = r2.match_pair(a, b, cfg)
+    rkp, tkp = res.ref.keypoints, res.tgt.keypoints
+    m = {((int(rkp[r].x), int(rkp[r].y)), (int(tkp[t].x), int(tkp[t].y))) for r, t, _ in res.matches.pairs}
+    dom = {}
+    descs = getattr(res.ref.descriptors, "descriptors", res.ref.descriptors)
+    for d in reversed(list(descs)):
+        k = rkp[d.keypoint_id]
+        dom[(int(k.x), int(k.y))] = int(d.variant)
+    return m, dom
+
+
+def _overlap(got, want):
+    return len(got & want) / max(len(want), 1)
+
+
+def test_pair512_match_set_overlap(r2):
+    from paper_2303_00319_b200 import synth
+    a, b, _ = synth.make_pair(512, seed=2)
+    want, dw = _oracle_matches(a.astype(np.float64), b.astype(np.float64), 5000)
+    got, dg = _gpu_matches(r2, a.astype(np.float64), b.astype(np.float64), 5000)
+    assert len(want) > 100
+    assert _overlap(got, want) >= 0.99
+    common = set(dw) & set(dg)
+    assert np.mean([dw[k] == dg[k] for k in common]) >= 0.99
+
+
+@pytest.mark.parametrize("theta", [0.0, 15.0, 90.0, 165.0, 270.0, 345.0])
+def test_rotation_sweep_agreement(r2, theta):
+    from paper_2303_00319_b200 import synth
+    # configs[4]: 512^2, theta in 15-degree steps, scale jitter [0.9, 1.1]
+    a, b, _ = synth.make_pair(512, seed=int(theta) + 1, theta_deg=theta, scale_jitter=0.1)
+    want, dw = _oracle_matches(a.astype(np.float64), b.astype(np.float64), 5000)
+    got, dg = _gpu_matches(r2, a.astype(np.float64), b.astype(np.float64), 5000)
+    print(f"theta {theta}: oracle {len(want)} matches, overlap {_overlap(got, want):.4f}")
+    assert _overlap(got, want) >= 0.99
+    common = set(dw) & set(dg)
+    assert len(common) >= 0.99 * len(dw)
+    assert np.mean([dw[k] == dg[k] for k in common]) >= 0.99
