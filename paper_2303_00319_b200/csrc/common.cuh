@@ -8,13 +8,40 @@
 namespace r2 {
 
 // ---- complex float2 arithmetic -------------------------------------------
+// sm_100 packed fp32x2 instructions (FADD2 / FMUL2 / FFMA2, with operand
+// swap and broadcast modifiers) do a complex add in one instruction and a
+// complex multiply in two, halving the FP issue slots of the FFT kernels,
+// which are issue/latency bound rather than FP-pipe bound.
+#ifndef R2_PACKED
+#define R2_PACKED 1
+#endif
+#if R2_PACKED
+R2_DEV float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+R2_DEV float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+R2_DEV float2 cmul(float2 a, float2 b) {
+  // (a.x b.x - a.y b.y, a.y b.x + a.x b.y)
+  return __ffma2_rn(make_float2(a.y, a.x), make_float2(-b.y, b.y), __fmul2_rn(a, make_float2(b.x, b.x)));
+}
+// a * (c - i s) for constants c, s: (c a.x + s a.y, c a.y - s a.x)
+R2_DEV float2 cmul_cs(float2 a, float c, float s) {
+  return __ffma2_rn(make_float2(a.y, a.x), make_float2(s, -s), __fmul2_rn(a, make_float2(c, c)));
+}
+#else
 R2_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 R2_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 R2_DEV float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
+R2_DEV float2 cmul_cs(float2 a, float c, float s) {
+  return make_float2(fmaf(c, a.x, s * a.y), fmaf(c, a.y, -s * a.x));
+}
+#endif
 R2_DEV float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+#if R2_PACKED
+R2_DEV float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+#else
 R2_DEV float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+#endif
 // multiply by -i (forward-transform quarter turn)
 R2_DEV float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
 

@@ -78,26 +78,43 @@ __global__ void __launch_bounds__(256) k_minmax(const T* __restrict__ mins, cons
   }
 }
 
+R2_DEV float min3(float a, float b, float c) { return fminf(fminf(a, b), c); }   // FMNMX3
+R2_DEV float max3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+R2_DEV double min3(double a, double b, double c) { return fmin(fmin(a, b), c); }
+R2_DEV double max3(double a, double b, double c) { return fmax(fmax(a, b), c); }
+
 // Largest threshold at which some 9-arc of the ring is brighter (A) /
 // darker (B) than the centre, on raw values: A = max_k min_{j<9} v[k+j],
-// B = min_k max_{j<9} v[k+j].
+// B = min_k max_{j<9} v[k+j].  Windows of 3, then 3 windows of 3.
 template <class T>
 R2_DEV void arc_extrema(const T (&v)[16], T& A, T& B) {
-  T m2[16], M2[16];
+  T m3[16], M3[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) { m2[k] = min(v[k], v[(k + 1) & 15]); M2[k] = max(v[k], v[(k + 1) & 15]); }
-  T m4[16], M4[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) { m4[k] = min(m2[k], m2[(k + 2) & 15]); M4[k] = max(M2[k], M2[(k + 2) & 15]); }
-  T a = min(min(m4[0], m4[4]), v[8]);
-  T b = max(max(M4[0], M4[4]), v[8]);
-#pragma unroll
-  for (int k = 1; k < 16; ++k) {
-    a = max(a, min(min(m4[k], m4[(k + 4) & 15]), v[(k + 8) & 15]));
-    b = min(b, max(max(M4[k], M4[(k + 4) & 15]), v[(k + 8) & 15]));
+  for (int k = 0; k < 16; ++k) {
+    m3[k] = min3(v[k], v[(k + 1) & 15], v[(k + 2) & 15]);
+    M3[k] = max3(v[k], v[(k + 1) & 15], v[(k + 2) & 15]);
   }
-  A = a;
-  B = b;
+  T m9[16], M9[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    m9[k] = min3(m3[k], m3[(k + 3) & 15], m3[(k + 6) & 15]);
+    M9[k] = max3(M3[k], M3[(k + 3) & 15], M3[(k + 6) & 15]);
+  }
+  T a = max3(m9[0], m9[1], m9[2]), b = min3(M9[0], M9[1], M9[2]);
+#pragma unroll
+  for (int k = 3; k < 15; k += 2) { a = max3(a, m9[k], m9[k + 1]); b = min3(b, M9[k], M9[k + 1]); }
+  A = fmax(a, m9[15]);
+  B = fmin(b, M9[15]);
+}
+
+// (x - lo) / span in float64, correctly rounded, from y = RN(1 / span):
+// q = RN(d y), r = d - span q (exact by fma), RN(q + r y) = RN(d / span)
+// (Markstein's theorem; d >= 0, span > 0, no under/overflow in this range).
+R2_DEV double div_span(double x, double lo, double span, double y) {
+  const double d = x - lo;
+  const double q = d * y;
+  const double r = fma(-q, span, d);
+  return fma(r, y, q);
 }
 
 template <class T>
@@ -114,14 +131,21 @@ __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, co
   const double hi = ord_val(mm[2 * plane + 1]);
   const double span = hi - lo;
   if (!(span > 0)) return;   // normalised map is all zeros: no keypoints
+  const double rspan = 1.0 / span;
   const int ty0 = blockIdx.y * kTile, tx0 = blockIdx.x * kTile;
-  for (int i = threadIdx.x; i < kIn * kIn; i += blockDim.x) {
-    const int yy = ty0 - kHalo + i / kIn, xx = tx0 - kHalo + i % kIn;
-    sv[i / kIn][i % kIn] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? p[(size_t)yy * W + xx] : T(0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < kIn; r += 8) {
+    const int yy = ty0 - kHalo + r;
+    const bool row_in = yy >= 0 && yy < H;
+    const T* prow = p + (size_t)(row_in ? yy : 0) * W;
+    for (int cx = lane; cx < kIn; cx += 32) {
+      const int xx = tx0 - kHalo + cx;
+      sv[r][cx] = (row_in && xx >= 0 && xx < W) ? prow[xx] : T(0);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kSc * kSc; i += blockDim.x) {
-    const int sy = i / kSc, sx = i % kSc;
+    const int sy = i / kSc, sx = i - sy * kSc;
     const int y = ty0 - 1 + sy, x = tx0 - 1 + sx;
     double s;
     if (y < 0 || y >= H || x < 0 || x >= W) {
@@ -135,27 +159,34 @@ __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, co
       for (int k = 0; k < 16; ++k) v[k] = sv[cy + c_ring_dy[k]][cx + c_ring_dx[k]];
       T A, B;
       arc_extrema(v, A, B);
-      const double nc = ((double)sv[cy][cx] - lo) / span;
-      const double na = ((double)A - lo) / span;
-      const double nb = ((double)B - lo) / span;
-      s = fmax(fmax(na - nc, nc - nb), 0.0);
+      const T c = sv[cy][cx];
+      // ref: max(max(na - nc, nc - nb), 0) with n = (v - lo) / span; the
+      // normalisation is monotone, so a side whose raw extreme does not
+      // beat the centre contributes <= 0 and is skipped
+      s = 0.0;
+      if (A > c || B < c) {
+        const double nc = div_span((double)c, lo, span, rspan);
+        if (A > c) s = fmax(s, div_span((double)A, lo, span, rspan) - nc);
+        if (B < c) s = fmax(s, nc - div_span((double)B, lo, span, rspan));
+      }
     }
     ss[sy][sx] = s;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
-    const int ly = i / kTile, lx = i % kTile;
+    const int ly = i >> 5, lx = i & 31;
     const int y = ty0 + ly, x = tx0 + lx;
     bool keep = false;
     double s = 0.0;
     if (y < H && x < W) {
       s = ss[ly + 1][lx + 1];
-      keep = s > thr;
+      keep = s > thr && x >= margin && x <= W - 1 - margin && y >= margin && y <= H - 1 - margin;
+      if (keep) {
 #pragma unroll
-      for (int dy = 0; dy < 3; ++dy)
+        for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-        for (int dx = 0; dx < 3; ++dx) keep = keep && s >= ss[ly + dy][lx + dx];
-      keep = keep && x >= margin && x <= W - 1 - margin && y >= margin && y <= H - 1 - margin;
+          for (int dx = 0; dx < 3; ++dx) keep = keep && s >= ss[ly + dy][lx + dx];
+      }
     }
     const unsigned slot = agg_inc(&cnt[plane], keep);
     if (keep && slot < cap) {

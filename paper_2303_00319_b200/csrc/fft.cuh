@@ -52,10 +52,10 @@ R2_DEV float2 tw32(float2 a) {
     constexpr float h = 7.071067812e-01f;
     constexpr float cc = W32::c[j] > 0 ? h : -h;
     constexpr float ss = W32::s[j] > 0 ? h : -h;
-    return make_float2(cc * a.x + ss * a.y, cc * a.y - ss * a.x);
+    return cmul_cs(a, cc, ss);
   } else {
     constexpr float cc = W32::c[j], ss = W32::s[j];
-    return make_float2(fmaf(cc, a.x, ss * a.y), fmaf(cc, a.y, -ss * a.x));
+    return cmul_cs(a, cc, ss);
   }
 }
 
