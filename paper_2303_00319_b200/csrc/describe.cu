@@ -24,6 +24,7 @@
 //   k_desc_scan  per image: exclusive scan of the slot valid flags
 //   k_desc_copy  order-preserving compaction of the slots
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <unordered_map>
@@ -31,6 +32,7 @@
 
 #include "common.cuh"
 #include "describe.h"
+#include "tma.cuh"
 
 namespace r2 {
 
@@ -85,7 +87,10 @@ GatherTables gather_tables(int P, int O) {
     bbox[a] = bb;
     radius = std::max({radius, -bb.x, bb.y, -bb.z, bb.w});
   }
-  const int stride = ((2 * radius + 1 + 3) / 4 + 1) * 4;
+  // staged row pitch: 2R+1 bytes from a 16-aligned start (+15; TMA box x
+  // coordinates must be 16-byte aligned), one spare word for the funnel-shift
+  // reads (+4), rounded to 16 bytes for the TMA box
+  const int stride = ((2 * radius + 1 + 15 + 4 + 15) / 16) * 16;
   GatherTables t{nullptr, nullptr, radius, stride};
   if ((size_t)radius * stride + radius > 32767) return t;   // offsets must fit int16
   std::vector<short> soff(off.size());
@@ -108,6 +113,7 @@ struct DescConst {
   bool rotate;
   int mode;
   int R, stride, rows;   // staging radius, staged row bytes, staged rows (2R+1)
+  int tma;               // stage the neighbourhood with one TMA box load
 };
 
 // six 5-bit counters (<= 31 samples) -> 10-bit fields: values 1,3,5 into e, 2,4,6 into o
@@ -126,8 +132,14 @@ R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int 
     for (int v = 0; v < O; ++v) out[v] = (((v & 1) ? o : e) >> (10 * (v >> 1))) & 1023u;
 }
 
-// 1 << s for a staged shift byte (0xFF -> 0)
-R2_DEV uint32_t one_hot(uint32_t s) { return s < 32u ? (1u << s) : 0u; }
+// 1 << s for a staged shift byte; PTX shl clamps shifts >= 32 to a zero
+// result, so out-of-image bytes (0xFF, or the garbage of a zero-filled TMA
+// word) count nothing -- and they are never sampled by an emitted descriptor
+R2_DEV uint32_t one_hot(uint32_t s) {
+  uint32_t r;
+  asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(s));
+  return r;
+}
 
 // axis-aligned patch: thread = (cell, quarter); 4 columns x CS rows per thread
 template <int CS>
@@ -198,10 +210,13 @@ R2_DEV void emit_row(const DescribeArgs& a, const DescConst& c, const unsigned* 
 }
 
 template <int CS>
-__global__ void __launch_bounds__(kT) k_desc_main(const uint8_t* __restrict__ mim, DescribeArgs a, DescConst c,
-                                                  GatherTables tab, __half* __restrict__ slot_rows,
+__global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ mim, DescribeArgs a,
+                                                  DescConst c, GatherTables tab, __half* __restrict__ slot_rows,
                                                   int* __restrict__ slot_meta, int* __restrict__ kp_skip) {
-  extern __shared__ uint32_t s_dyn[];             // staged bytes (c.rows x c.stride), then cnt
+  extern __shared__ __align__(128) uint32_t s_raw[];
+  __shared__ uint64_t s_bar;
+  // staged bytes (c.rows x c.stride, 128-byte aligned for the TMA box), then cnt
+  uint32_t* s_dyn = s_raw + ((128u - (smem_u32(s_raw) & 127u)) & 127u) / 4;
   uint8_t* sreg = reinterpret_cast<uint8_t*>(s_dyn);
   unsigned* cnt = s_dyn + (c.rows * c.stride) / 4;   // [cells * O]
   __shared__ int s_pick[16], s_np, s_sq;
@@ -218,12 +233,36 @@ __global__ void __launch_bounds__(kT) k_desc_main(const uint8_t* __restrict__ mi
   }
   const uint8_t* m = mim + (size_t)b * c.H * c.W;
   // ---- stage rows y-R..y+R, word-aligned columns from ax0, as shift bytes 5(v-1)
-  const int ax0 = (x - c.R) >= 0 ? ((x - c.R) & ~3) : -(((c.R - x) + 3) & ~3);
+  const int ax0 = (x - c.R) & (c.tma ? ~15 : ~3);   // floor to 16 (TMA) / 4 bytes
   const int wpr = c.stride / 4;
   const bool word_ok = (c.W & 3) == 0;
   uint32_t* sw = s_dyn;
   const bool inside = word_ok && y - c.R >= 0 && y + c.R < c.H && ax0 >= 0 && ax0 + 4 * wpr <= c.W;
-  if (inside) {
+  if (c.tma) {
+    // one TMA box (zero fill left/right of the image, neighbouring images'
+    // rows above/below; W % 16 == 0 and a 16-aligned start, so out-of-image
+    // bytes form whole words and the per-word transform cannot borrow into
+    // an image byte), then an in-place shift-byte transform
+    if (threadIdx.x == 0) {
+      asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap) : "memory");
+      mbar_init(&s_bar, 1);
+      mbar_fence_init();
+      mbar_expect_tx(&s_bar, (uint32_t)(c.rows * c.stride));
+      tma_load_2d(sw, &tmap, ax0, b * c.H + y - c.R, &s_bar);
+    }
+    for (int i = threadIdx.x; i < c.cells * c.O; i += kT) cnt[i] = 0;
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+    uint4* q4 = reinterpret_cast<uint4*>(sw);
+    for (int i = threadIdx.x; i < c.rows * c.stride / 16; i += kT) {
+      uint4 w = q4[i];
+      w.x = w.x * 5u - 0x05050505u;
+      w.y = w.y * 5u - 0x05050505u;
+      w.z = w.z * 5u - 0x05050505u;
+      w.w = w.w * 5u - 0x05050505u;
+      q4[i] = w;
+    }
+  } else if (inside) {
     // common case: one aligned word load + one multiply-add per 4 pixels
     const uint32_t* src0 = reinterpret_cast<const uint32_t*>(m + (size_t)(y - c.R) * c.W + ax0);
     const int wrow = c.W >> 2;
@@ -254,7 +293,8 @@ __global__ void __launch_bounds__(kT) k_desc_main(const uint8_t* __restrict__ mi
       sw[r * wpr + wq] = v;
     }
   }
-  for (int i = threadIdx.x; i < c.cells * c.O; i += kT) cnt[i] = 0;
+  if (!c.tma)
+    for (int i = threadIdx.x; i < c.cells * c.O; i += kT) cnt[i] = 0;
   __syncthreads();
   const int bx = x - ax0;                         // keypoint column within a staged row
   const uint8_t* ctr = sreg + c.R * c.stride + bx;   // keypoint pixel
@@ -451,17 +491,32 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
   if (a.kp_stride == 0) {
     cudaMemsetAsync(a.count, 0, sizeof(int32_t) * a.B, st);
     cudaMemsetAsync(a.skipped, 0, sizeof(int32_t) * a.B, st);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
   }
-  const size_t smem = (size_t)c.rows * c.stride + (size_t)c.cells * c.O * sizeof(uint32_t);
+  const size_t smem = (size_t)c.rows * c.stride + (size_t)c.cells * c.O * sizeof(uint32_t) + 128;
   if (smem > 200 * 1024) return 2;
   dim3 grid(a.kp_stride, a.B);
+  CUtensorMap tmap{};
+  c.tma = 0;
+  auto enc = get_encode();
+  if (enc && c.W % 16 == 0 && c.stride <= 256 && c.rows <= 256 && ((uintptr_t)mim & 15) == 0) {
+    // 2-D view (W, B*H): rows outside one image read its neighbour (or zeros
+    // at the ends) -- never sampled by an emitted descriptor, see above
+    cuuint64_t dims[2] = {(cuuint64_t)c.W, (cuuint64_t)c.H * a.B};
+    cuuint64_t strides[1] = {(cuuint64_t)c.W};
+    cuuint32_t box[2] = {(cuuint32_t)c.stride, (cuuint32_t)c.rows};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(mim), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      c.tma = 1;
+  }
   cudaFuncSetAttribute(k_desc_main<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_desc_main<16><<<grid, kT, smem, st>>>(mim, a, c, tab, rows, meta, skip);
+  k_desc_main<16><<<grid, kT, smem, st>>>(tmap, mim, a, c, tab, rows, meta, skip);
   k_desc_scan<<<a.B, 1024, 0, st>>>(meta, skip, a, c.per, offs);
   dim3 g2((a.kp_stride * c.per + 7) / 8, a.B);
   k_desc_copy<<<g2, 256, 0, st>>>(rows, meta, offs, a, c.per);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace r2

@@ -470,7 +470,7 @@ int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, siz
   const int planes = a.B * nm;
   if (a.max_points == 0) {
     cudaMemsetAsync(a.kp_count, 0, sizeof(int32_t) * a.B, st);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
   }
   k_init<<<(planes + 255) / 256, 256, 0, st>>>(mm, cnt, planes);
   const size_t n = (size_t)a.H * a.W;
@@ -492,7 +492,7 @@ int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, siz
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_merge_suppress, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_merge_suppress<<<a.B, 1024, smem, st>>>(sorted, nsel, merged, hk, hv, p.tsz, nbr, a.W, a);
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace

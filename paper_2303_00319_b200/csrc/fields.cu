@@ -724,7 +724,7 @@ static cudaError_t launch_rows_fwd(const float* img, float2* P, const FieldsCons
   cudaError_t e = set_smem(k_rows_fwd<G>, smem);
   if (e != cudaSuccess) return e;
   k_rows_fwd<G><<<grid, kThreads, smem, st>>>(img, P, c);
-  return cudaGetLastError();
+  return cudaPeekAtLastError();
 }
 
 template <int G>
@@ -743,7 +743,7 @@ static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c,
   cudaError_t e = set_smem(k_cols<G>, smem);
   if (e != cudaSuccess) return e;
   k_cols<G><<<grid, ColsCfg<G>::T, smem, st>>>(P, Q, c);
-  return cudaGetLastError();
+  return cudaPeekAtLastError();
 }
 
 template <int G>
@@ -762,7 +762,7 @@ static cudaError_t launch_amp0(const float2* Q, float2* R0, float* amp0, unsigne
   cudaError_t e = set_smem(k_rows_amp0<G>, smem);
   if (e != cudaSuccess) return e;
   k_rows_amp0<G><<<grid, kThreads, smem, st>>>(Q, R0, amp0, hist, c);
-  return cudaGetLastError();
+  return cudaPeekAtLastError();
 }
 
 template <int G, int SC>
@@ -789,7 +789,7 @@ static cudaError_t launch_pc_s(const float2* Q, const float2* R0, const float* t
   if (e != cudaSuccess) return e;
   dim3 grid((c.H + 1) / 2, c.B);
   k_rows_pc<G, SC><<<grid, kThreads, smem, st>>>(Q, R0, thr, out, c, rr, ops);
-  return cudaGetLastError();
+  return cudaPeekAtLastError();
 }
 
 template <int G>
@@ -866,7 +866,7 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
     k_med_collect<<<grid, 256, 0, st>>>(amp0, info, cand, cnt, n);
   }
   k_med_final<<<B * c.O, 1024, 0, st>>>(cand, cnt, info, thr, n, c.thr_factor);
-  if (cudaGetLastError() != cudaSuccess) return 3;
+  if (cudaPeekAtLastError() != cudaSuccess) return 3;
   PcOut po{o.mmax, o.mmin, o.mim, o.a_o, o.pc, o.amax};
   R2_DISPATCH_G(p.gw, launch_pc, Q, R0, thr, po, c, st);
   if (e != cudaSuccess) return 3;

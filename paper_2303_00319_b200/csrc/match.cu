@@ -29,6 +29,7 @@
 
 #include "match.h"
 #include "sort.cuh"
+#include "tma.cuh"
 
 namespace r2 {
 
@@ -66,30 +67,6 @@ struct Part {
 };
 
 // ------------------------------------------------------------ PTX helpers
-R2_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-R2_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
-}
-R2_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-R2_DEV void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
-}
-// try_wait with a suspend-time hint: the waiting thread sleeps in hardware
-// instead of spinning and stealing issue slots from the epilogue warps
-R2_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-      "@!p bra WAIT_%=;\n}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-R2_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      :: "r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)) : "memory");
-}
 R2_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 R2_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -231,7 +208,7 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(a_full, 1);
     for (int s = 0; s < NACC; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], NEPI); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_fence_init();
     asm volatile("prefetch.tensormap [%0];" :: "l"(&tmapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" :: "l"(&tmapB) : "memory");
   }
@@ -651,19 +628,6 @@ __global__ void __launch_bounds__(1024) k_vec_sort(K128* __restrict__ keys, K128
 }
 
 // ------------------------------------------------------------ host
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q;
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  });
-  return fn;
-}
-
 constexpr int kMaxSplits = 8;
 
 struct MatchWs {
@@ -748,7 +712,7 @@ int match_run(const MatchArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   const size_t sort_smem = kSortChunk * sizeof(K128);
   cudaFuncSetAttribute(k_match_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
   k_match_sort<<<a.n_pairs, 1024, sort_smem, st>>>(a, iw, keys, tmp);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace r2
@@ -789,7 +753,7 @@ int match_vectors_run(const double* R, const int* rkp, int nr, const double* T, 
   const size_t sort_smem = kSortChunk * sizeof(K128);
   cudaFuncSetAttribute(k_vec_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
   k_vec_sort<<<1, 1024, sort_smem, st>>>(keys, tmp, ntg, out_ref, out_tgt, out_dist, out_count);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace r2
