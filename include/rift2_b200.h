@@ -147,6 +147,41 @@ int32_t rift2_match(const void* desc_counts, const int32_t* desc_sqnorm, const i
                     int32_t tgt_kp_capacity, int32_t* out_ref, int32_t* out_tgt, double* out_dist,
                     int32_t* out_count, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- stage 4, row-sharded across processes ------
+ * For one huge pair split over G GPUs: rank r matches ALL target
+ * descriptors against its slice of the reference descriptors
+ * (rift2_match_partial), the G partial arrays are all-gathered, and every
+ * rank (or one) combines them exactly (rift2_match_finish) -- the same
+ * result as rift2_match on the whole reference set, bit for bit.
+ *
+ * rift2_match_partial: arguments as rift2_match; out_parts
+ *   [n_pairs][desc_capacity] records, one per target descriptor row: the
+ *   exact best reference candidate of this call (ref_kp = -1 when none).
+ *   Reference keypoint ids are taken from desc_kp, so a slice must carry
+ *   global keypoint ids.  No workspace.
+ * rift2_match_finish: parts [n_parts][n_pairs][desc_capacity] (the gathered
+ *   partial arrays, any order of ranks); the descriptor arrays must hold the
+ *   FULL reference and target sets (for variant grouping and the float64
+ *   distance of each winner); outputs and workspace as rift2_match
+ *   (rift2_match_workspace_size). */
+typedef struct rift2_match_part {
+  int32_t dot;          /* integer dot product of the count vectors */
+  int32_t ref_sqnorm;   /* sum of squared reference counts */
+  int32_t ref_kp;       /* reference keypoint id, -1 = none */
+  float score;          /* dot / |ref| (screening only) */
+} rift2_match_part;
+
+int32_t rift2_match_partial(const void* desc_counts, const int32_t* desc_sqnorm, const int32_t* desc_kp,
+                            const int32_t* desc_count, int32_t n_blocks, int32_t desc_stride, int32_t desc_capacity,
+                            int32_t dim, int32_t n_pairs, const int32_t* ref_block, const int32_t* tgt_block,
+                            rift2_match_part* out_parts, void* stream);
+int32_t rift2_match_finish(const rift2_match_part* parts, int32_t n_parts, const void* desc_counts,
+                           const int32_t* desc_sqnorm, const int32_t* desc_kp, const int32_t* desc_count,
+                           int32_t n_blocks, int32_t desc_stride, int32_t desc_capacity, int32_t dim, int32_t n_pairs,
+                           const int32_t* ref_block, const int32_t* tgt_block, int32_t tgt_kp_capacity,
+                           int32_t* out_ref, int32_t* out_tgt, double* out_dist, int32_t* out_count, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* Generic variant of stage 4 for arbitrary float64 descriptor vectors (not
  * integer histograms), e.g. unit vectors built by the caller: the
  * reference's own key |r|^2 - 2 r.t in float64 (ref: matcher.py:125-135).

@@ -49,6 +49,10 @@ _SIGNATURES = {
     "rift2_match_workspace_size": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
     "rift2_match": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p,
                              _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "rift2_match_partial": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p,
+                                     _c_p, _c_p]),
+    "rift2_match_finish": (_c_int, [_c_p, _c_int, _c_p, _c_p, _c_p, _c_p, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                    _c_p, _c_p, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "rift2_match_vectors_workspace_size": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_sz)]),
     "rift2_match_vectors": (_c_int, [_c_p, _c_p, _c_int, _c_p, _c_p, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p,
                                      _c_p, _c_sz, _c_p]),

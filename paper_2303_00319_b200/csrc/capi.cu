@@ -263,6 +263,46 @@ int32_t rift2_match(const void* desc_counts, const int32_t* desc_sqnorm, const i
   return map_internal(rc, "rift2_match");
 }
 
+static int32_t match_args_check(int32_t n_pairs, int32_t n_blocks, int32_t desc_capacity, int32_t dim,
+                                int32_t desc_stride) {
+  if (n_pairs < 1 || n_blocks < 1 || desc_capacity < 1 || dim < 1 || dim > desc_stride || desc_stride % 8 != 0)
+    return fail(RIFT2_BAD_ARGUMENT, "bad match dimensions");
+  if (desc_stride != 224 && desc_stride != 256) return fail(RIFT2_UNSUPPORTED, "desc_stride must be 224 or 256");
+  return RIFT2_OK;
+}
+
+static_assert(sizeof(rift2_match_part) == 16, "rift2_match_part is the kernel's 16-byte partial record");
+
+int32_t rift2_match_partial(const void* desc_counts, const int32_t* desc_sqnorm, const int32_t* desc_kp,
+                            const int32_t* desc_count, int32_t n_blocks, int32_t desc_stride, int32_t desc_capacity,
+                            int32_t dim, int32_t n_pairs, const int32_t* ref_block, const int32_t* tgt_block,
+                            rift2_match_part* out_parts, void* stream) {
+  if (int32_t rc = match_args_check(n_pairs, n_blocks, desc_capacity, dim, desc_stride)) return rc;
+  if (!desc_counts || !desc_sqnorm || !desc_kp || !desc_count || !ref_block || !tgt_block || !out_parts)
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  r2::MatchArgs a{static_cast<const __half*>(desc_counts), desc_sqnorm, desc_kp, desc_count, desc_stride,
+                  desc_capacity, dim, n_pairs, n_blocks, ref_block, tgt_block, 0, nullptr, nullptr, nullptr, nullptr};
+  return map_internal(r2::match_partial_run(a, out_parts, static_cast<cudaStream_t>(stream)), "rift2_match_partial");
+}
+
+int32_t rift2_match_finish(const rift2_match_part* parts, int32_t n_parts, const void* desc_counts,
+                           const int32_t* desc_sqnorm, const int32_t* desc_kp, const int32_t* desc_count,
+                           int32_t n_blocks, int32_t desc_stride, int32_t desc_capacity, int32_t dim, int32_t n_pairs,
+                           const int32_t* ref_block, const int32_t* tgt_block, int32_t tgt_kp_capacity,
+                           int32_t* out_ref, int32_t* out_tgt, double* out_dist, int32_t* out_count, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  if (int32_t rc = match_args_check(n_pairs, n_blocks, desc_capacity, dim, desc_stride)) return rc;
+  if (n_parts < 1) return fail(RIFT2_BAD_ARGUMENT, "n_parts must be >= 1");
+  if (!parts || !desc_counts || !desc_sqnorm || !desc_kp || !desc_count || !ref_block || !tgt_block || !out_ref ||
+      !out_tgt || !out_dist || !out_count || !workspace)
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  r2::MatchArgs a{static_cast<const __half*>(desc_counts), desc_sqnorm, desc_kp, desc_count, desc_stride,
+                  desc_capacity, dim, n_pairs, n_blocks, ref_block, tgt_block, tgt_kp_capacity, out_ref, out_tgt,
+                  out_dist, out_count};
+  return map_internal(r2::match_finish_run(a, parts, n_parts, workspace, workspace_bytes,
+                                           static_cast<cudaStream_t>(stream)), "rift2_match_finish");
+}
+
 int32_t rift2_match_vectors_workspace_size(int32_t n_ref, int32_t n_tgt, size_t* bytes) {
   if (n_ref < 1 || n_tgt < 1 || !bytes) return fail(RIFT2_BAD_ARGUMENT, "descriptor lists must be nonempty");
   *bytes = r2::match_vectors_workspace_bytes(n_ref, n_tgt);

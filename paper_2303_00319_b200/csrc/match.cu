@@ -448,8 +448,14 @@ R2_DEV int cmp_cross(const Part& a, int qta, const Part& b, int qtb) {
   return l > r ? 1 : (l < r ? -1 : 0);
 }
 
+// Part of (pair, target row t, split s) at pair * pair_stride + t * row_stride + s * split_stride:
+// the GEMM's own [pair][row][split] layout, or [part][pair][row] as gathered from G ranks
+struct PartLayout {
+  size_t pair_stride, row_stride, split_stride;
+};
+
 __global__ void __launch_bounds__(256) k_match_combine(MatchArgs a, IdxWs w, const Part* __restrict__ part,
-                                                       int splits, K128* __restrict__ keys) {
+                                                       int splits, PartLayout lay, K128* __restrict__ keys) {
   const int pair = blockIdx.y;
   const int warp_g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -458,14 +464,14 @@ __global__ void __launch_bounds__(256) k_match_combine(MatchArgs a, IdxWs w, con
   const int tb = a.tgt_block[pair], rb = a.ref_block[pair];
   const int* gs = w.gstart + (size_t)pair * (a.cap + 1);
   const int t0 = gs[warp_g], t1 = gs[warp_g + 1];
-  const Part* pp = part + (size_t)pair * a.cap * splits;
+  const Part* pp = part + (size_t)pair * lay.pair_stride;
   // best candidate over variants x splits (all lanes compute the same; cheap)
   Part best{0, 1, -1, -1.f};
   int best_qt = 1;
   for (int t = t0; t < t1; ++t) {
     const int qt = a.sqnorm[(size_t)tb * a.cap + t];
     for (int s = 0; s < splits; ++s) {
-      const Part c = pp[(size_t)t * splits + s];
+      const Part c = pp[(size_t)t * lay.row_stride + (size_t)s * lay.split_stride];
       if (c.kp < 0) continue;
       if (best.kp < 0) { best = c; best_qt = qt; continue; }
       const int r = cmp_cross(c, qt, best, best_qt);
@@ -658,60 +664,94 @@ size_t match_workspace_bytes(int n_pairs, int cap, int tgt_kp_cap) {
   return plan_match(n_pairs, cap > 0 ? cap : 1).total;
 }
 
-int match_run(const MatchArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int n_blocks = a.n_blocks;
-  const MatchWs p = plan_match(a.n_pairs, a.cap);
-  if (ws_bytes < p.total) return 1;
-  if (a.stride != 224 && a.stride != 256) return 2;   // TMA boxes cover K <= 256
-  char* w = static_cast<char*>(ws);
-  Part* part = reinterpret_cast<Part*>(w + p.off_part);
-  IdxWs iw{reinterpret_cast<int*>(w + p.off_gstart), reinterpret_cast<int*>(w + p.off_ng),
-           reinterpret_cast<int*>(w + p.off_rstart), reinterpret_cast<int*>(w + p.off_rend)};
-  K128* keys = reinterpret_cast<K128*>(w + p.off_keys);
-  K128* tmp = reinterpret_cast<K128*>(w + p.off_tmp);
+namespace {
 
+// Launch k_match_gemm: per target row the exact best reference candidate of
+// each column split, into part[pair][cap][splits].  splits <= 0: chosen to
+// fill the SMs.  Returns the split count used (negative on error).
+int gemm_launch(const MatchArgs& a, Part* part, int splits, cudaStream_t st) {
+  if (a.stride != 224 && a.stride != 256) return -2;   // TMA boxes cover K <= 256
   auto encode = get_encode();
-  if (!encode) return 3;
-  // one descriptor-array tensor map per box shape: A = 128 target rows, B = 64 reference rows
+  if (!encode) return -3;
+  // one descriptor-array tensor map per box shape: A = 128 target rows, B = 128 reference rows
   CUtensorMap tmapA, tmapB;
-  cuuint64_t dims[2] = {(cuuint64_t)a.stride, (cuuint64_t)n_blocks * a.cap};
+  cuuint64_t dims[2] = {(cuuint64_t)a.stride, (cuuint64_t)a.n_blocks * a.cap};
   cuuint64_t strides[1] = {(cuuint64_t)a.stride * 2};
   cuuint32_t boxA[2] = {BK, BM}, boxB[2] = {BK, BN};
   cuuint32_t estr[2] = {1, 1};
   CUresult cr = encode(&tmapA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a.counts), dims, strides,
                        boxA, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return 3;
+  if (cr != CUDA_SUCCESS) return -3;
   cr = encode(&tmapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(a.counts), dims, strides, boxB, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return 3;
+  if (cr != CUDA_SUCCESS) return -3;
 
   const int m_tiles = (a.cap + BM - 1) / BM;
-  // split the reference range only as far as needed to put one CTA on every SM:
-  // a CTA that sees few column tiles keeps a weak running best and pays the
-  // exact-candidate path far more often (~32/(i+1) columns per tile i)
-  const int n_tiles_cap = (a.cap + BN - 1) / BN;
-  const int ctas = m_tiles * a.n_pairs;
-  int dev = 0, n_sm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  int splits = (n_sm + ctas - 1) / ctas;
-  const int max_split = n_tiles_cap / 4 > 1 ? n_tiles_cap / 4 : 1;
-  splits = splits > max_split ? max_split : splits;
-  splits = splits < 1 ? 1 : (splits > kMaxSplits ? kMaxSplits : splits);
+  if (splits <= 0) {
+    // split the reference range only as far as needed to put one CTA on every SM:
+    // a CTA that sees few column tiles keeps a weak running best and pays the
+    // exact-candidate path far more often (~32/(i+1) columns per tile i)
+    const int n_tiles_cap = (a.cap + BN - 1) / BN;
+    const int ctas = m_tiles * a.n_pairs;
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    splits = (n_sm + ctas - 1) / ctas;
+    const int max_split = n_tiles_cap / 4 > 1 ? n_tiles_cap / 4 : 1;
+    splits = splits > max_split ? max_split : splits;
+    splits = splits < 1 ? 1 : (splits > kMaxSplits ? kMaxSplits : splits);
+  }
   GemmParams gp{a.sqnorm, a.kp, a.count, a.ref_block, a.tgt_block, a.cap, splits, part};
   cudaFuncSetAttribute(k_match_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_GEMM);
   dim3 grid(m_tiles * splits, a.n_pairs);
   k_match_gemm<<<grid, GEMM_THREADS, SMEM_GEMM, st>>>(tmapA, tmapB, gp);
+  return splits;
+}
+
+// variant groups, exact combine over the parts, winner distances, (dist, ref, tgt) order
+void finish_launch(const MatchArgs& a, const Part* part, int n_parts, PartLayout lay, const MatchWs& p, char* w,
+                   cudaStream_t st) {
+  IdxWs iw{reinterpret_cast<int*>(w + p.off_gstart), reinterpret_cast<int*>(w + p.off_ng),
+           reinterpret_cast<int*>(w + p.off_rstart), reinterpret_cast<int*>(w + p.off_rend)};
+  K128* keys = reinterpret_cast<K128*>(w + p.off_keys);
+  K128* tmp = reinterpret_cast<K128*>(w + p.off_tmp);
   k_match_index<<<a.n_pairs, 1024, 0, st>>>(a, iw);
   {
     dim3 g2((a.cap + 7) / 8, a.n_pairs);
-    k_match_combine<<<g2, 256, 0, st>>>(a, iw, part, splits, keys);
+    k_match_combine<<<g2, 256, 0, st>>>(a, iw, part, n_parts, lay, keys);
   }
   const size_t sort_smem = kSortChunk * sizeof(K128);
   cudaFuncSetAttribute(k_match_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
   k_match_sort<<<a.n_pairs, 1024, sort_smem, st>>>(a, iw, keys, tmp);
+}
+
+}  // namespace
+
+int match_run(const MatchArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const MatchWs p = plan_match(a.n_pairs, a.cap);
+  if (ws_bytes < p.total) return 1;
+  char* w = static_cast<char*>(ws);
+  Part* part = reinterpret_cast<Part*>(w + p.off_part);
+  const int splits = gemm_launch(a, part, 0, st);
+  if (splits < 0) return -splits;
+  finish_launch(a, part, splits, PartLayout{(size_t)a.cap * splits, (size_t)splits, 1}, p, w, st);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
+
+int match_partial_run(const MatchArgs& a, void* parts, cudaStream_t st) {
+  const int r = gemm_launch(a, static_cast<Part*>(parts), 1, st);
+  if (r < 0) return -r;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
+
+int match_finish_run(const MatchArgs& a, const void* parts, int n_parts, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  const MatchWs p = plan_match(a.n_pairs, a.cap);
+  if (ws_bytes < p.total) return 1;
+  finish_launch(a, static_cast<const Part*>(parts), n_parts,
+                PartLayout{(size_t)a.cap, 1, (size_t)a.n_pairs * a.cap}, p, static_cast<char*>(ws), st);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
 

@@ -24,6 +24,11 @@ struct MatchArgs {
 
 size_t match_workspace_bytes(int n_pairs, int cap, int tgt_kp_cap);
 int match_run(const MatchArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
+// row-sharded matching: GEMM partials [n_pairs][cap] of 16-byte records, and the
+// exact combine of n_parts gathered partial arrays ([n_parts][n_pairs][cap])
+int match_partial_run(const MatchArgs& a, void* parts, cudaStream_t st);
+int match_finish_run(const MatchArgs& a, const void* parts, int n_parts, void* ws, size_t ws_bytes,
+                     cudaStream_t st);
 
 // generic float64 descriptor vectors (rows grouped by keypoint id)
 size_t match_vectors_workspace_bytes(int nr, int nt);

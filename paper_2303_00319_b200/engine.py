@@ -189,3 +189,52 @@ def match(desc: dict, dim: int, ref_block: torch.Tensor, tgt_block: torch.Tensor
                          _ptr(out["tgt"]), _ptr(out["dist"]), _ptr(out["count"]), _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "rift2_match")
     return out
+
+
+def match_partial(desc: dict, dim: int, ref_block: torch.Tensor, tgt_block: torch.Tensor, out=None):
+    """Row-sharded matching, step 1 (rift2_match_partial): per target
+    descriptor row the exact best candidate among this call's reference
+    descriptors -> int32 tensor (P, cap, 4) of (dot, ref_sqnorm, ref_kp,
+    score bits)."""
+    lib = _lib.load(require_gpu=True)
+    counts = desc["counts"]
+    n_blocks, cap, stride = counts.shape
+    P = ref_block.numel()
+    if out is None:
+        out = torch.empty((P, cap, 4), dtype=torch.int32, device=counts.device)
+    rc = lib.rift2_match_partial(_ptr(counts), _ptr(desc["sqnorm"]), _ptr(desc["kp"]), _ptr(desc["count"]),
+                                 n_blocks, stride, cap, int(dim), P, _ptr(ref_block), _ptr(tgt_block), _ptr(out),
+                                 _stream())
+    _lib.check(rc, "rift2_match_partial")
+    return out
+
+
+def match_finish(parts: torch.Tensor, desc: dict, dim: int, ref_block: torch.Tensor, tgt_block: torch.Tensor,
+                 tgt_kp_cap: int, ws_key: str = "match_finish", out=None):
+    """Row-sharded matching, step 2 (rift2_match_finish): exact combine of
+    the gathered partials parts (G, P, cap, 4) over the FULL descriptor
+    sets -> dict(ref, tgt, dist, count) as match()."""
+    lib = _lib.load(require_gpu=True)
+    counts = desc["counts"]
+    n_blocks, cap, stride = counts.shape
+    P = ref_block.numel()
+    G = parts.shape[0]
+    if parts.shape != (G, P, cap, 4) or parts.dtype != torch.int32:
+        raise ParameterError(f"parts must be int32 ({G}, {P}, {cap}, 4), got {tuple(parts.shape)}")
+    parts = parts.contiguous()
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_match_workspace_size(P, cap, tgt_kp_cap, ctypes.byref(nbytes)), "match_finish")
+    ws = WORKSPACES.get(ws_key, nbytes.value)
+    dev = counts.device
+    kc = max(int(tgt_kp_cap), 1)
+    if out is None:
+        out = dict(ref=torch.empty((P, kc), dtype=torch.int32, device=dev),
+                   tgt=torch.empty((P, kc), dtype=torch.int32, device=dev),
+                   dist=torch.empty((P, kc), dtype=torch.float64, device=dev),
+                   count=torch.empty((P,), dtype=torch.int32, device=dev))
+    rc = lib.rift2_match_finish(_ptr(parts), G, _ptr(counts), _ptr(desc["sqnorm"]), _ptr(desc["kp"]),
+                                _ptr(desc["count"]), n_blocks, stride, cap, int(dim), P, _ptr(ref_block),
+                                _ptr(tgt_block), kc, _ptr(out["ref"]), _ptr(out["tgt"]), _ptr(out["dist"]),
+                                _ptr(out["count"]), _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "rift2_match_finish")
+    return out
