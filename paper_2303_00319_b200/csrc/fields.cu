@@ -151,6 +151,52 @@ R2_DEV float transfer(float lnr, float L2, float th, float ll, float ang, float 
   return ex2(fmaf(d * d, -b2, fmaf(dr * dr, -a2, L2)));
 }
 
+// Per-filter multiply + inverse column FFT + store for one column (direct or
+// mirror), G >= 32.  One instruction stream serves both kinds of warp (two
+// unrolled copies thrash the instruction cache); the differences are
+// per-thread constants: with t < G and G a multiple of 32 every padded
+// spectrum index is a base plus a signed compile-time multiple of m, the
+// mirror angle is +-pi - theta with the sign fixed per unrolled element
+// (ky < N/2 <=> m < 16), and the imaginary part takes a sign.  The spectrum
+// buffer holds the periodic copy S[N] = S[0], so the mirror index needs no wrap.
+template <int G, class Sync>
+R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float* Ln, const float* Lp, const float* Th,
+                         float2* buf, float2* Qb, int xo, int t, bool mir, Sync& sync) {
+  constexpr int N = 32 * G;
+  constexpr int PS = G + G / 32;                          // padded stride of one m step
+  const int W = c.W, F = c.S * c.O;
+  const float2* sp = Sc + (mir ? (N + N / 32) - t - ((t + 31) >> 5) : t + (t >> 5));
+  const int sstep = mir ? -PS : PS;
+  const float tsg = mir ? -1.f : 1.f;                     // theta_m = +-pi - theta
+  const float tpi = mir ? kPi : 0.f;
+  const float ysg = mir ? 1.f : -1.f;                     // conj for the direct column
+  const float a2 = c.a2, b2 = c.b2;
+  float2 v[32];
+  for (int f = 0; f < F; ++f) {
+    const int s = f / c.O, o = f % c.O;
+    const float ll = c.log_lambda[s], ang = c.ang[o];
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      const int ky = t + G * m;
+      const float2 sv = sp[sstep * m];
+      const float th = fmaf(tsg, Th[ky], m < 16 ? tpi : -tpi);
+      const float gv = transfer(Ln[ky], Lp[ky], th, ll, ang, a2, b2);
+      // conj(spectrum * G) for the inverse; the mirror reads S(-ky, kx) = conj S(ky, W - kx)
+      v[m] = __fmul2_rn(sv, make_float2(gv, gv * ysg));
+    }
+    fft_fast<G>(v, buf, c.tw_h, t, sync);
+    // y = t + G m: tile row (t >> 2) + (G / 4) m, lane t & 3.  W is re-read
+    // opaquely each filter so the compiler does not hoist 32 64-bit store
+    // addresses across the loop (register spills)
+    int wv;
+    asm volatile("mov.b32 %0, %1;" : "=r"(wv) : "r"(W));
+    float2* q = Qb + (size_t)f * c.Hp * wv + ((size_t)(t >> 2) * wv + xo) * 4 + (t & 3);
+    const size_t step = (size_t)G * wv;           // (G / 4) tile rows of 4 W elements
+#pragma unroll
+    for (int m = 0; m < 32; ++m) q[m * step] = cconj(v[m]);
+  }
+}
+
 template <int G>
 __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k_cols(const float2* __restrict__ P, float2* __restrict__ Q,
                                                    const __grid_constant__ FieldsConst c) {
@@ -186,6 +232,7 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
       if constexpr (G <= 32) fft_fast<G>(v, buf, c.tw_h, t, sw); else fft_fast<G>(v, buf, c.tw_h, t, sn);
 #pragma unroll
       for (int m = 0; m < 32; ++m) S[g * PL + pad32(t + G * m)] = v[m];
+      if (t == 0) S[g * PL + pad32(N)] = v[0];         // periodic copy for the mirror index
     }
     // 2. spectrum geometry of the NS columns
     for (int i = threadIdx.x; i < NS * N; i += ColsCfg<G>::T) {
@@ -208,6 +255,11 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     const float* Ln = glnr + cc * N;
     const float* Lp = gL2 + cc * N;
     const float* Th = gth + cc * N;
+    if constexpr (G >= 32) {
+      if constexpr (G <= 32) cols_filters<G>(c, Sc, Ln, Lp, Th, buf, Qb, xo, t, mir != 0, sw);
+      else cols_filters<G>(c, Sc, Ln, Lp, Th, buf, Qb, xo, t, mir != 0, sn);
+      return;
+    } else {
     const float a2 = c.a2, b2 = c.b2;
     for (int f = 0; f < F; ++f) {
       const int s = f / c.O, o = f % c.O;
@@ -227,13 +279,14 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
         const float gv = transfer(Ln[ky], Lp[ky], th, ll, ang, a2, b2);
         v[m] = make_float2(sv.x * gv, sv.y * gv);   // conj(spectrum * G) for the inverse
       }
-      if constexpr (G <= 32) fft_fast<G>(v, buf, c.tw_h, t, sw); else fft_fast<G>(v, buf, c.tw_h, t, sn);
+      fft_fast<G>(v, buf, c.tw_h, t, sw);
       float2* Qf = Qb + (size_t)f * c.Hp * W;
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const int y = t + G * m;
         Qf[tq(y, xo, W)] = cconj(v[m]);
       }
+    }
     }
   } else {
     // generic sizes: whole CTA per transform, 4 columns per CTA
