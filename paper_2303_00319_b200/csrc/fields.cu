@@ -151,6 +151,15 @@ R2_DEV float transfer(float lnr, float L2, float th, float ll, float ang, float 
   return ex2(fmaf(d * d, -b2, fmaf(dr * dr, -a2, L2)));
 }
 
+// transfer of filter (s, o) without the radius-only factor lowpass / (H*W),
+// which the fast column pass folds into the spectrum once per column
+R2_DEV float transfer_s(float lnr, float th, float ll, float ang, float a2, float b2) {
+  float d = fabsf(th - ang);
+  d = d > kPi ? kTwoPi - d : d;
+  const float dr = lnr + ll;
+  return ex2(fmaf(d * d, -b2, -a2 * (dr * dr)));
+}
+
 // Per-filter multiply + inverse column FFT + store for one column (direct or
 // mirror), G >= 32.  One instruction stream serves both kinds of warp (two
 // unrolled copies thrash the instruction cache); the differences are
@@ -160,7 +169,7 @@ R2_DEV float transfer(float lnr, float L2, float th, float ll, float ang, float 
 // (ky < N/2 <=> m < 16), and the imaginary part takes a sign.  The spectrum
 // buffer holds the periodic copy S[N] = S[0], so the mirror index needs no wrap.
 template <int G, class Sync>
-R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float* Ln, const float* Lp, const float* Th,
+R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float* Ln, const float* Th,
                          float2* buf, float2* Qb, int xo, int t, bool mir, Sync& sync) {
   constexpr int N = 32 * G;
   constexpr int PS = G + G / 32;                          // padded stride of one m step
@@ -180,7 +189,7 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float* Ln
       const int ky = t + G * m;
       const float2 sv = sp[sstep * m];
       const float th = fmaf(tsg, Th[ky], m < 16 ? tpi : -tpi);
-      const float gv = transfer(Ln[ky], Lp[ky], th, ll, ang, a2, b2);
+      const float gv = transfer_s(Ln[ky], th, ll, ang, a2, b2);
       // conj(spectrum * G) for the inverse; the mirror reads S(-ky, kx) = conj S(ky, W - kx)
       v[m] = __fmul2_rn(sv, make_float2(gv, gv * ysg));
     }
@@ -214,8 +223,7 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     constexpr int PL = padded_len(N);
     float2* S = sm;                                              // [NS][PL]
     float* glnr = reinterpret_cast<float*>(sm + NS * PL);        // [NS][N]
-    float* gL2 = glnr + NS * N;                                  // [NS][N]
-    float* gth = gL2 + NS * N;                                   // [NS][N]
+    float* gth = glnr + NS * N;                                  // [NS][N]
     float2* bufs = reinterpret_cast<float2*>(gth + NS * N);      // [NG][PL]
     const int g = threadIdx.x / G, t = threadIdx.x % G;
     float2* buf = bufs + g * PL;
@@ -232,15 +240,20 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
       if constexpr (G <= 32) fft_fast<G>(v, buf, c.tw_h, t, sw); else fft_fast<G>(v, buf, c.tw_h, t, sn);
 #pragma unroll
       for (int m = 0; m < 32; ++m) S[g * PL + pad32(t + G * m)] = v[m];
-      if (t == 0) S[g * PL + pad32(N)] = v[0];         // periodic copy for the mirror index
     }
+    __syncthreads();
     // 2. spectrum geometry of the NS columns
     for (int i = threadIdx.x; i < NS * N; i += ColsCfg<G>::T) {
       float lnr, L2, th;
       geometry(c, i % N, min(kx0 + i / N, Wh - 1), lnr, L2, th);
       glnr[i] = lnr;
-      gL2[i] = L2;
       gth[i] = th;
+      // the radius-only factor lowpass / (H*W) goes into the spectrum (the
+      // mirror column has the same radius); 0 at DC
+      const int cc = i / N, ky = i % N;
+      const float2 sv = cscale(S[cc * PL + pad32(ky)], ex2(L2));
+      S[cc * PL + pad32(ky)] = sv;
+      if (ky == 0) S[cc * PL + pad32(N)] = sv;   // periodic copy for the mirror index
     }
     __syncthreads();
     // 3. every group independently: per filter multiply + inverse column FFT,
@@ -253,11 +266,10 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     const int xo = mir ? W - kx : kx;
     const float2* Sc = S + cc * PL;
     const float* Ln = glnr + cc * N;
-    const float* Lp = gL2 + cc * N;
     const float* Th = gth + cc * N;
     if constexpr (G >= 32) {
-      if constexpr (G <= 32) cols_filters<G>(c, Sc, Ln, Lp, Th, buf, Qb, xo, t, mir != 0, sw);
-      else cols_filters<G>(c, Sc, Ln, Lp, Th, buf, Qb, xo, t, mir != 0, sn);
+      if constexpr (G <= 32) cols_filters<G>(c, Sc, Ln, Th, buf, Qb, xo, t, mir != 0, sw);
+      else cols_filters<G>(c, Sc, Ln, Th, buf, Qb, xo, t, mir != 0, sn);
       return;
     } else {
     const float a2 = c.a2, b2 = c.b2;
@@ -276,7 +288,7 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
           sv = Sc[pad32(ky)];
           sv.y = -sv.y;
         }
-        const float gv = transfer(Ln[ky], Lp[ky], th, ll, ang, a2, b2);
+        const float gv = transfer_s(Ln[ky], th, ll, ang, a2, b2);
         v[m] = make_float2(sv.x * gv, sv.y * gv);   // conj(spectrum * G) for the inverse
       }
       fft_fast<G>(v, buf, c.tw_h, t, sw);
@@ -786,7 +798,7 @@ static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c,
   dim3 grid;
   if constexpr (G > 0) {
     const int N = 32 * G, NG = ColsCfg<G>::T / G, CG = NG / 2, PL = padded_len(N);
-    smem = ((size_t)CG * PL + (size_t)NG * PL) * sizeof(float2) + 3 * (size_t)CG * N * sizeof(float);
+    smem = ((size_t)CG * PL + (size_t)NG * PL) * sizeof(float2) + 2 * (size_t)CG * N * sizeof(float);
     grid = dim3((c.Wh + CG - 1) / CG, c.B);
   } else {
     const int PL = padded_len(c.H);
