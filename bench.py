@@ -300,24 +300,32 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     clk = Clocks(local_rank)
     clk.start()
     time.sleep(0.3)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # headline: K whole steps (the captured step graph; the second half's
+    # filter bank overlaps the first half's detect / describe / match)
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record()
+    for _ in range(K):
+        pipe.step()
+    e_end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = e_start.elapsed_time(e_end)
+    # roofline: the filter bank (both halves, alone on the stream), K launches
+    # of its graph timed with CUDA events on the stream it runs on
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     for i in range(K):
         ev[i][0].record()
         pipe.replay_fields()
         ev[i][1].record()
-        pipe.replay_features()
-        ev[i][2].record()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    total_ms = ev[0][0].elapsed_time(ev[K - 1][2])
-    fields_ms = sum(ev[i][0].elapsed_time(ev[i][1]) for i in range(K)) / K
+    fields_ms = sum(a.elapsed_time(b) for a, b in ev) / K
 
     # e2e: public API with host buffers -- every step uploads its images from
     # pinned host memory (copy stream, double-buffered against the previous
@@ -362,7 +370,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "kernel": "filter bank (rows_fwd+cols+rows_amp0+median+rows_pc)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": tr, "traffic_source": tr_src, "bytes_per_launch": bytes_launch, "launch_ms": fields_ms,
-                         "share_of_step": fields_ms / (total_ms / K), "peak_source": peak_src},
+                         "share_of_step": fields_ms / (total_ms / K), "peak_source": peak_src,
+                         "note": "filter bank timed alone; in the step it overlaps the other half's features"},
             "clocks": clocks,
             "matches_per_pair": float(np.mean(counts))}
     if world == 1 and not args.no_cpu_baseline:

@@ -57,67 +57,111 @@ class BatchPipeline:
         self._copy_stream = None
 
     # ---- stages (eager) --------------------------------------------------
-    def run_fields(self):
-        engine.fields(self.images, self.bank, out=self.f, ws_key="b_fields")
+    # The batch is processed as (up to) two halves of pairs with their own
+    # workspaces.  In the captured step the second half's filter bank runs
+    # while the first half's detect / describe / match (whose per-image
+    # kernels leave most SMs idle) runs on a second stream.
+    def _halves(self):
+        if self.P < 2:
+            return [(0, self.P)]
+        h = self.P // 2
+        return [(0, h), (h, self.P)]
+
+    def run_fields_half(self, i: int, images=None):
+        p0, p1 = self._halves()[i]
+        img = self.images if images is None else images
+        f = {k: v[2 * p0:2 * p1] for k, v in self.f.items()}
+        engine.fields(img[2 * p0:2 * p1], self.bank, out=f, ws_key=f"b_fields{i}")
+
+    def run_features_half(self, i: int):
+        p0, p1 = self._halves()[i]
+        c = self.cfg
+        sl = slice(2 * p0, 2 * p1)
+        k = {n: v[sl] for n, v in self.k.items()}
+        d = {n: v[sl] for n, v in self.d.items()}
+        m = {n: v[p0:p1] for n, v in self.m.items()}
+        n = p1 - p0
+        engine.detect(self.f["mmin"][sl], self.f["mmax"][sl], c.fast_threshold, self.K, c.patch_size // 2,
+                      ws_key=f"b_detect{i}", out=k)
+        engine.describe(self.f["mim"][sl], k["x"], k["y"], k["count"], c.n_orient, c.patch_size,
+                        c.grid, c.dominant_ratio, c.rotate_patch, "rift2", capacity=2 * self.K,
+                        ws_key=f"b_describe{i}", out=d)
+        engine.match(d, self.dim, self.rb[:n], self.tb[:n], self.K, ws_key=f"b_match{i}", out=m)
+
+    def run_fields(self, images=None):
+        for i in range(len(self._halves())):
+            self.run_fields_half(i, images)
 
     def run_features(self):
-        c = self.cfg
-        engine.detect(self.f["mmin"], self.f["mmax"], c.fast_threshold, self.K, c.patch_size // 2,
-                      ws_key="b_detect", out=self.k)
-        engine.describe(self.f["mim"], self.k["x"], self.k["y"], self.k["count"], c.n_orient, c.patch_size,
-                        c.grid, c.dominant_ratio, c.rotate_patch, "rift2", capacity=2 * self.K,
-                        ws_key="b_describe", out=self.d)
-        engine.match(self.d, self.dim, self.rb, self.tb, self.K, ws_key="b_match", out=self.m)
+        for i in range(len(self._halves())):
+            self.run_features_half(i)
 
     def run(self):
         self.run_fields()
         self.run_features()
 
-    # number of our kernels one step launches (fields 7 + detect 5 + describe 3 + match 4)
-    KERNELS_PER_STEP = 19
+    def _run_overlapped(self, images, side: torch.cuda.Stream):
+        """Enqueue one step: F0, then F1 on this stream while D0 runs on `side`, then D1."""
+        main = torch.cuda.current_stream()
+        nh = len(self._halves())
+        self.run_fields_half(0, images)
+        if nh == 1:
+            self.run_features_half(0)
+            return
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self.run_features_half(0)
+        self.run_fields_half(1, images)
+        self.run_features_half(1)
+        main.wait_stream(side)
+
+    @property
+    def KERNELS_PER_STEP(self):
+        # our kernels per step: per half, fields 7 + detect 5 + describe 3 + match 4
+        return 19 * len(self._halves())
 
     # ---- graphs ------------------------------------------------------------
     def capture(self):
         """Warm up (allocates workspaces and cached tables), then capture.
 
-        Three graphs: the filter bank on each of two image buffers (so a
-        host upload can fill one while the other is being read) and the
-        detect + describe + match group."""
+        Graphs: the overlapped whole step on each of two image buffers (a
+        host upload can fill one while the other is being read), plus the
+        filter bank alone (both halves, one stream) and the feature stages
+        alone, used by bench.py to time the filter bank by itself."""
         self.run()
         torch.cuda.synchronize()
         if self._alt is None:
             self._alt = torch.zeros_like(self.images)
         s = torch.cuda.Stream()
+        side = self._side = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        g_a, g_b, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        g_a, g_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        g_f, g_d = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             with torch.cuda.graph(g_a, stream=s):
+                self._run_overlapped(self.images, side)
+            with torch.cuda.graph(g_b, stream=s):
+                self._run_overlapped(self._alt, side)
+            with torch.cuda.graph(g_f, stream=s):
                 self.run_fields()
-            self.images, self._alt = self._alt, self.images
-            try:
-                with torch.cuda.graph(g_b, stream=s):
-                    self.run_fields()
-            finally:
-                self.images, self._alt = self._alt, self.images
-            with torch.cuda.graph(g2, stream=s):
+            with torch.cuda.graph(g_d, stream=s):
                 self.run_features()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        self.graphs = (g_a, g2, g_b)
+        self.graphs = {"step": (g_a, g_b), "fields": g_f, "features": g_d}
         return self
 
     def replay_fields(self):
-        self.graphs[0].replay()
+        self.graphs["fields"].replay()
 
     def replay_features(self):
-        self.graphs[1].replay()
+        self.graphs["features"].replay()
 
     def step(self):
         if self.graphs is None:
             self.run()
         else:
-            self.graphs[0].replay()
-            self.graphs[1].replay()
+            self.graphs["step"][0].replay()
 
     def run_from_host(self, host_images, steps: int, host_out: dict | None = None):
         """End-to-end steps from host memory: step i uploads host_images[i %
@@ -133,7 +177,7 @@ class BatchPipeline:
         cs = torch.cuda.current_stream()
         xs = self._copy_stream = self._copy_stream or torch.cuda.Stream()
         bufs = (self.images, self._alt)
-        fields_graph = (self.graphs[0], self.graphs[2])
+        step_graph = self.graphs["step"]
         ready = [torch.cuda.Event(), torch.cuda.Event()]
         done = [torch.cuda.Event(), torch.cuda.Event()]
         xs.wait_stream(cs)
@@ -149,9 +193,8 @@ class BatchPipeline:
                     bufs[1 - b].copy_(host_images[(i + 1) % len(host_images)], non_blocking=True)
                     ready[1 - b].record(xs)
             cs.wait_event(ready[b])
-            fields_graph[b].replay()
+            step_graph[b].replay()
             done[b].record(cs)
-            self.graphs[1].replay()
             if host_out is not None:
                 for k, t in host_out.items():
                     t.copy_(self.m[k], non_blocking=True)

@@ -44,7 +44,8 @@ struct GatherTables {
   const short* soff;     // [O][P*P] dy*stride + dx into the staged region; angle 0 unused
   const int4* bbox;      // [O] (dx_min, dx_max, dy_min, dy_max)
   int radius;            // max |offset| over all angles (and the axis crop)
-  int stride;            // staged row length in bytes (multiple of 4, >= 2*radius + 4)
+  int stride;            // staged row length in bytes (multiple of 16)
+  int4 hbbox[8];         // host copy of bbox
 };
 
 std::mutex g_mu;
@@ -91,7 +92,8 @@ GatherTables gather_tables(int P, int O) {
   // coordinates must be 16-byte aligned), one spare word for the funnel-shift
   // reads (+4), rounded to 16 bytes for the TMA box
   const int stride = ((2 * radius + 1 + 15 + 4 + 15) / 16) * 16;
-  GatherTables t{nullptr, nullptr, radius, stride};
+  GatherTables t{nullptr, nullptr, radius, stride, {}};
+  for (int a = 0; a < O && a < 8; ++a) t.hbbox[a] = bbox[a];
   if ((size_t)radius * stride + radius > 32767) return t;   // offsets must fit int16
   std::vector<short> soff(off.size());
   for (size_t i = 0; i < off.size(); ++i) soff[i] = (short)(off[i].y * stride + off[i].x);
@@ -114,6 +116,7 @@ struct DescConst {
   int mode;
   int R, stride, rows;   // staging radius, staged row bytes, staged rows (2R+1)
   int tma;               // stage the neighbourhood with one TMA box load
+  int4 bbox[8];          // per-angle rotated-patch bounding boxes (dx_min, dx_max, dy_min, dy_max)
 };
 
 // six 5-bit counters (<= 31 samples) -> 10-bit fields: values 1,3,5 into e, 2,4,6 into o
@@ -122,14 +125,22 @@ R2_DEV void widen(uint32_t acc, uint32_t& e, uint32_t& o) {
   o += ((acc >> 5) & 31u) | ((acc >> 15) & 31u) << 10 | ((acc >> 25) & 31u) << 20;
 }
 
-// reduce the 4 threads of a cell and write its O counts
-R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int O) {
+// reduce the 4 threads of a cell, write its O counts and add their squares
+// to the descriptor's squared norm (recode only permutes bins)
+R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int O, int* sq) {
   e += __shfl_xor_sync(0xffffffffu, e, 1);
   o += __shfl_xor_sync(0xffffffffu, o, 1);
   e += __shfl_xor_sync(0xffffffffu, e, 2);
   o += __shfl_xor_sync(0xffffffffu, o, 2);
-  if (writer)
-    for (int v = 0; v < O; ++v) out[v] = (((v & 1) ? o : e) >> (10 * (v >> 1))) & 1023u;
+  if (writer) {
+    int q = 0;
+    for (int v = 0; v < O; ++v) {
+      const unsigned n = (((v & 1) ? o : e) >> (10 * (v >> 1))) & 1023u;
+      out[v] = n;
+      q += (int)(n * n);
+    }
+    atomicAdd(sq, q);
+  }
 }
 
 // 1 << s for a staged shift byte; PTX shl clamps shifts >= 32 to a zero
@@ -143,7 +154,7 @@ R2_DEV uint32_t one_hot(uint32_t s) {
 
 // axis-aligned patch: thread = (cell, quarter); 4 columns x CS rows per thread
 template <int CS>
-R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsigned* cnt) {
+R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsigned* cnt, int* sq) {
   const int tpc = CS / 4;                       // threads per cell
   const int t = threadIdx.x;
   const bool on = t < c.cells * tpc;
@@ -163,12 +174,13 @@ R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsign
       if (r % 7 == 6 || r == CS - 1) { widen(acc, e, o); acc = 0; }   // 4 samples/row: <= 28 per field
     }
   }
-  reduce_cell(e, o, on && sub == 0, cnt + cell * c.O, c.O);
+  reduce_cell(e, o, on && sub == 0, cnt + cell * c.O, c.O, sq);
 }
 
 // rotated patch of angle table t: sample (i, j) at ctr + t[i*P + j]
 template <int CS>
-R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const short* __restrict__ t, unsigned* cnt) {
+R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const short* __restrict__ t, unsigned* cnt,
+                          int* sq) {
   const int tpc = CS / 4;
   const int tid = threadIdx.x;
   const bool on = tid < c.cells * tpc;
@@ -186,15 +198,13 @@ R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const short* _
       if (r % 7 == 6 || r == CS - 1) { widen(acc, e, o); acc = 0; }
     }
   }
-  reduce_cell(e, o, on && sub == 0, cnt + cell * c.O, c.O);
+  reduce_cell(e, o, on && sub == 0, cnt + cell * c.O, c.O, sq);
 }
 
 // write one descriptor row: output bin (cell, w-1) holds the count of the
 // input value v with recode(v) = w, i.e. v = (w - 1 + pivot - 1) mod O + 1
 // (ref: mim.py:117-136)
-R2_DEV void emit_row(const DescribeArgs& a, const DescConst& c, const unsigned* cnt, int pivot, __half* row,
-                     int* s_sq) {
-  int sq = 0;
+R2_DEV void emit_row(const DescribeArgs& a, const DescConst& c, const unsigned* cnt, int pivot, __half* row) {
   for (int i = threadIdx.x; i < a.stride; i += kT) {
     unsigned v = 0;
     if (i < c.dim) {
@@ -202,11 +212,7 @@ R2_DEV void emit_row(const DescribeArgs& a, const DescConst& c, const unsigned* 
       v = cnt[cell * c.O + (w + pivot - 1) % c.O];
     }
     row[i] = __uint2half_rn(v);
-    sq += (int)(v * v);
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(s_sq, sq);
 }
 
 template <int CS>
@@ -218,8 +224,10 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   // staged bytes (c.rows x c.stride, 128-byte aligned for the TMA box), then cnt
   uint32_t* s_dyn = s_raw + ((128u - (smem_u32(s_raw) & 127u)) & 127u) / 4;
   uint8_t* sreg = reinterpret_cast<uint8_t*>(s_dyn);
-  unsigned* cnt = s_dyn + (c.rows * c.stride) / 4;   // [cells * O]
-  __shared__ int s_pick[16], s_np, s_sq;
+  // count buffers: axis patch, first and second rotated pick, [cells * O] each
+  unsigned* cnt = s_dyn + (c.rows * c.stride) / 4;
+  unsigned* cnt_rot[2] = {cnt + c.cells * c.O, cnt + 2 * c.cells * c.O};
+  __shared__ int s_pick[16], s_np, s_sq[3];
   const int b = blockIdx.y, k = blockIdx.x;
   const size_t slot0 = ((size_t)b * a.kp_stride + k) * c.per;
   int* meta = slot_meta + slot0 * 3;              // (valid, variant, sqnorm) per slot
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
       mbar_expect_tx(&s_bar, (uint32_t)(c.rows * c.stride));
       tma_load_2d(sw, &tmap, ax0, b * c.H + y - c.R, &s_bar);
     }
-    for (int i = threadIdx.x; i < c.cells * c.O; i += kT) cnt[i] = 0;
+    if (threadIdx.x == 0) { s_sq[0] = 0; s_sq[1] = 0; s_sq[2] = 0; }
     __syncthreads();
     mbar_wait(&s_bar, 0);
     uint4* q4 = reinterpret_cast<uint4*>(sw);
@@ -293,13 +301,12 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
       sw[r * wpr + wq] = v;
     }
   }
-  if (!c.tma)
-    for (int i = threadIdx.x; i < c.cells * c.O; i += kT) cnt[i] = 0;
+  if (!c.tma && threadIdx.x == 0) { s_sq[0] = 0; s_sq[1] = 0; s_sq[2] = 0; }
   __syncthreads();
   const int bx = x - ax0;                         // keypoint column within a staged row
   const uint8_t* ctr = sreg + c.R * c.stride + bx;   // keypoint pixel
   // ---- axis-aligned patch
-  count_axis<CS>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt);
+  count_axis<CS>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt, &s_sq[0]);
   __syncthreads();
   // ---- dominant index / runner-up (ref: mim.py:69-91)
   if (threadIdx.x < 32) {
@@ -336,7 +343,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
         for (int q = 0; q < cand; ++q) {
           const int dom = picks[q];
           if (c.rotate && dom != 1) {
-            const int4 bb = tab.bbox[dom - 1];
+            const int4 bb = c.bbox[dom - 1];
             if (x + bb.x < 0 || x + bb.y >= c.W || y + bb.z < 0 || y + bb.w >= c.H) { ++skip; continue; }
           }
           s_pick[np++] = dom;
@@ -348,27 +355,30 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   }
   __syncthreads();
   const int np = s_np;
-  // axis-patch descriptors first (they reuse `cnt`), rotated ones after
+  // one phase: axis-patch rows are emitted from `cnt` while the rotated picks
+  // (at most two) are counted into their own buffers; then one barrier
+  const bool rot_mode = c.mode == 2 && c.rotate;
+  int nrot = 0;
   for (int q = 0; q < np; ++q) {
     const int dom = s_pick[q];
-    if (c.mode == 2 && c.rotate && dom != 1) continue;
-    if (threadIdx.x == 0) s_sq = 0;
-    __syncthreads();
-    emit_row(a, c, cnt, c.mode == 0 ? 1 : dom, slot_rows + (slot0 + q) * a.stride, &s_sq);
-    __syncthreads();
-    if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = c.mode == 0 ? 1 : dom; meta[3 * q + 2] = s_sq; }
+    if (rot_mode && dom != 1) {
+      count_rotated<CS>(c, ctr, tab.soff + (size_t)(dom - 1) * c.P * c.P, cnt_rot[nrot], &s_sq[1 + nrot]);
+      ++nrot;
+    } else {
+      const int var = c.mode == 0 ? 1 : dom;
+      emit_row(a, c, cnt, var, slot_rows + (slot0 + q) * a.stride);
+      if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = var; meta[3 * q + 2] = s_sq[0]; }
+    }
   }
-  if (c.mode == 2 && c.rotate) {
+  if (nrot > 0) {
+    __syncthreads();
+    int r = 0;
     for (int q = 0; q < np; ++q) {
       const int dom = s_pick[q];
-      if (dom == 1) continue;
-      __syncthreads();
-      count_rotated<CS>(c, ctr, tab.soff + (size_t)(dom - 1) * c.P * c.P, cnt);
-      if (threadIdx.x == 0) s_sq = 0;
-      __syncthreads();
-      emit_row(a, c, cnt, dom, slot_rows + (slot0 + q) * a.stride, &s_sq);
-      __syncthreads();
-      if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq; }
+      if (!(rot_mode && dom != 1)) continue;
+      emit_row(a, c, cnt_rot[r], dom, slot_rows + (slot0 + q) * a.stride);
+      if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[1 + r]; }
+      ++r;
     }
   }
   for (int q = np + threadIdx.x; q < c.per; q += kT) meta[3 * q] = 0;
@@ -481,6 +491,7 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
   GatherTables tab = gather_tables(a.patch, a.O);
   if (!tab.soff) return 2;
   c.R = tab.radius;
+  for (int q = 0; q < 8; ++q) c.bbox[q] = tab.hbbox[q];
   c.stride = tab.stride;
   c.rows = 2 * c.R + 1;
   char* w = static_cast<char*>(ws);
@@ -493,7 +504,7 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
     cudaMemsetAsync(a.skipped, 0, sizeof(int32_t) * a.B, st);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
   }
-  const size_t smem = (size_t)c.rows * c.stride + (size_t)c.cells * c.O * sizeof(uint32_t) + 128;
+  const size_t smem = (size_t)c.rows * c.stride + 3 * (size_t)c.cells * c.O * sizeof(uint32_t) + 128;
   if (smem > 200 * 1024) return 2;
   dim3 grid(a.kp_stride, a.B);
   CUtensorMap tmap{};
