@@ -5,6 +5,12 @@ size (images interleaved [ref0, tgt0, ref1, tgt1, ...]) and runs the four
 stages back to back on the current stream with no host synchronisation.
 The two stage groups (filter bank; detect + describe + match) are captured
 into CUDA graphs after a warm-up, so a step is two graph launches.
+
+Throughput mode (`capture_pipelined` / `pipelined_step` /
+`run_from_host_pipelined`): the filter bank of batch i runs on one stream
+while detect / describe / match of batch i-1 runs on another, on
+double-buffered field maps -- each step still completes one batch, one step
+later, with results identical to `step()`.
 """
 
 from __future__ import annotations
@@ -57,102 +63,53 @@ class BatchPipeline:
         self._copy_stream = None
 
     # ---- stages (eager) --------------------------------------------------
-    # The batch is processed as (up to) two halves of pairs with their own
-    # workspaces.  In the captured step the second half's filter bank runs
-    # while the first half's detect / describe / match (whose per-image
-    # kernels leave most SMs idle) runs on a second stream.
-    def _halves(self):
-        if self.P < 2:
-            return [(0, self.P)]
-        h = self.P // 2
-        return [(0, h), (h, self.P)]
+    def run_fields(self, images=None, f=None, ws: str = "b_"):
+        engine.fields(self.images if images is None else images, self.bank, out=self.f if f is None else f,
+                      ws_key=ws + "fields")
 
-    def run_fields_half(self, i: int, images=None):
-        p0, p1 = self._halves()[i]
-        img = self.images if images is None else images
-        f = {k: v[2 * p0:2 * p1] for k, v in self.f.items()}
-        engine.fields(img[2 * p0:2 * p1], self.bank, out=f, ws_key=f"b_fields{i}")
-
-    def run_features_half(self, i: int):
-        p0, p1 = self._halves()[i]
+    def run_features(self, f=None, ws: str = "b_"):
+        f = self.f if f is None else f
         c = self.cfg
-        sl = slice(2 * p0, 2 * p1)
-        k = {n: v[sl] for n, v in self.k.items()}
-        d = {n: v[sl] for n, v in self.d.items()}
-        m = {n: v[p0:p1] for n, v in self.m.items()}
-        n = p1 - p0
-        engine.detect(self.f["mmin"][sl], self.f["mmax"][sl], c.fast_threshold, self.K, c.patch_size // 2,
-                      ws_key=f"b_detect{i}", out=k)
-        engine.describe(self.f["mim"][sl], k["x"], k["y"], k["count"], c.n_orient, c.patch_size,
-                        c.grid, c.dominant_ratio, c.rotate_patch, "rift2", capacity=2 * self.K,
-                        ws_key=f"b_describe{i}", out=d)
-        engine.match(d, self.dim, self.rb[:n], self.tb[:n], self.K, ws_key=f"b_match{i}", out=m)
-
-    def run_fields(self, images=None):
-        for i in range(len(self._halves())):
-            self.run_fields_half(i, images)
-
-    def run_features(self):
-        for i in range(len(self._halves())):
-            self.run_features_half(i)
+        engine.detect(f["mmin"], f["mmax"], c.fast_threshold, self.K, c.patch_size // 2, ws_key=ws + "detect",
+                      out=self.k)
+        engine.describe(f["mim"], self.k["x"], self.k["y"], self.k["count"], c.n_orient, c.patch_size, c.grid,
+                        c.dominant_ratio, c.rotate_patch, "rift2", capacity=2 * self.K, ws_key=ws + "describe",
+                        out=self.d)
+        engine.match(self.d, self.dim, self.rb, self.tb, self.K, ws_key=ws + "match", out=self.m)
 
     def run(self):
         self.run_fields()
         self.run_features()
 
-    def _run_overlapped(self, images, side: torch.cuda.Stream):
-        """Enqueue one step: F0, then F1 on this stream while D0 runs on `side`, then D1."""
-        main = torch.cuda.current_stream()
-        nh = len(self._halves())
-        self.run_fields_half(0, images)
-        if nh == 1:
-            self.run_features_half(0)
-            return
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            self.run_features_half(0)
-        self.run_fields_half(1, images)
-        self.run_features_half(1)
-        main.wait_stream(side)
-
-    @property
-    def KERNELS_PER_STEP(self):
-        # our kernels per step: per half, fields 7 + detect 5 + describe 3 + match 4
-        return 19 * len(self._halves())
+    # our kernels per step: fields 7 + detect 5 + describe 3 + match 4
+    KERNELS_PER_STEP = 19
 
     # ---- graphs ------------------------------------------------------------
     def capture(self):
-        """Warm up (allocates workspaces and cached tables), then capture.
-
-        Graphs: the overlapped whole step on each of two image buffers (a
-        host upload can fill one while the other is being read), plus the
-        filter bank alone (both halves, one stream) and the feature stages
-        alone, used by bench.py to time the filter bank by itself."""
+        """Warm up (allocates workspaces and cached tables), then capture the
+        filter bank on each of two image buffers (a host upload can fill one
+        while the other is read) and the detect + describe + match group."""
         self.run()
         torch.cuda.synchronize()
         if self._alt is None:
             self._alt = torch.zeros_like(self.images)
         s = torch.cuda.Stream()
-        side = self._side = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        g_a, g_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        g_f, g_d = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        g_a, g_b, g_d = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             with torch.cuda.graph(g_a, stream=s):
-                self._run_overlapped(self.images, side)
-            with torch.cuda.graph(g_b, stream=s):
-                self._run_overlapped(self._alt, side)
-            with torch.cuda.graph(g_f, stream=s):
                 self.run_fields()
+            with torch.cuda.graph(g_b, stream=s):
+                self.run_fields(images=self._alt)
             with torch.cuda.graph(g_d, stream=s):
                 self.run_features()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        self.graphs = {"step": (g_a, g_b), "fields": g_f, "features": g_d}
+        self.graphs = {"fields": (g_a, g_b), "features": g_d}
         return self
 
-    def replay_fields(self):
-        self.graphs["fields"].replay()
+    def replay_fields(self, buf: int = 0):
+        self.graphs["fields"][buf].replay()
 
     def replay_features(self):
         self.graphs["features"].replay()
@@ -161,7 +118,8 @@ class BatchPipeline:
         if self.graphs is None:
             self.run()
         else:
-            self.graphs["step"][0].replay()
+            self.replay_fields()
+            self.replay_features()
 
     def run_from_host(self, host_images, steps: int, host_out: dict | None = None):
         """End-to-end steps from host memory: step i uploads host_images[i %
@@ -177,7 +135,6 @@ class BatchPipeline:
         cs = torch.cuda.current_stream()
         xs = self._copy_stream = self._copy_stream or torch.cuda.Stream()
         bufs = (self.images, self._alt)
-        step_graph = self.graphs["step"]
         ready = [torch.cuda.Event(), torch.cuda.Event()]
         done = [torch.cuda.Event(), torch.cuda.Event()]
         xs.wait_stream(cs)
@@ -193,9 +150,84 @@ class BatchPipeline:
                     bufs[1 - b].copy_(host_images[(i + 1) % len(host_images)], non_blocking=True)
                     ready[1 - b].record(xs)
             cs.wait_event(ready[b])
-            step_graph[b].replay()
+            self.replay_fields(b)
             done[b].record(cs)
+            self.replay_features()
             if host_out is not None:
+                for k, t in host_out.items():
+                    t.copy_(self.m[k], non_blocking=True)
+        cs.wait_stream(xs)
+
+    # ---- cross-step pipeline --------------------------------------------------
+    # Step i runs the filter bank of batch i (stream 1) concurrently with
+    # detect / describe / match of batch i-1 (stream 2), on double-buffered
+    # field maps; every pair still goes through the whole path, one step
+    # later.  After pipelined_step(p) the match arrays hold the batch whose
+    # filter bank ran in the previous pipelined step.
+    def capture_pipelined(self):
+        if self.graphs is None:
+            self.capture()
+        if getattr(self, "_f2", None) is None:
+            self._f2 = {k: torch.empty_like(v) for k, v in self.f.items()}
+        fbuf = (self.f, self._f2)
+        imgs = (self.images, self._alt)
+        for p in (0, 1):                                   # warm-up: allocate workspaces
+            self.run_fields(imgs[p], fbuf[p], "p_")
+            self.run_features(fbuf[1 - p], "p_")
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        side = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        graphs = []
+        with torch.cuda.stream(s):
+            for p in (0, 1):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    side.wait_stream(s)
+                    with torch.cuda.stream(side):
+                        self.run_features(fbuf[1 - p], "p_")
+                    self.run_fields(imgs[p], fbuf[p], "p_")
+                    s.wait_stream(side)
+                graphs.append(g)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graphs["pipe"] = tuple(graphs)
+        return self
+
+    def pipelined_step(self, parity: int):
+        self.graphs["pipe"][parity & 1].replay()
+
+    def run_from_host_pipelined(self, host_images, steps: int, host_out: dict | None = None):
+        """As run_from_host, pipelined: step i uploads batch i+1 on the copy
+        stream, runs the filter bank of batch i next to the features of batch
+        i-1, and copies batch i-1's match arrays back.  A priming step (the
+        filter bank of batch 0) precedes the loop; the caller times `steps`
+        steps, each of which completes one batch.  Enqueues only."""
+        if "pipe" not in (self.graphs or {}):
+            self.capture_pipelined()
+        if not isinstance(host_images, (list, tuple)):
+            host_images = [host_images]
+        cs = torch.cuda.current_stream()
+        xs = self._copy_stream = self._copy_stream or torch.cuda.Stream()
+        bufs = (self.images, self._alt)
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        done = [torch.cuda.Event(), torch.cuda.Event()]
+        xs.wait_stream(cs)
+        with torch.cuda.stream(xs):
+            bufs[0].copy_(host_images[0], non_blocking=True)
+            ready[0].record(xs)
+        for i in range(steps + 1):
+            b = i % 2
+            if i + 1 <= steps:
+                with torch.cuda.stream(xs):
+                    if i >= 1:
+                        xs.wait_event(done[1 - b])
+                    bufs[1 - b].copy_(host_images[(i + 1) % len(host_images)], non_blocking=True)
+                    ready[1 - b].record(xs)
+            cs.wait_event(ready[b])
+            self.pipelined_step(b)
+            done[b].record(cs)
+            if i >= 1 and host_out is not None:            # batch i-1 is complete
                 for k, t in host_out.items():
                     t.copy_(self.m[k], non_blocking=True)
         cs.wait_stream(xs)

@@ -146,3 +146,29 @@ def test_batch_pipeline_equals_api(r2):
         api = r2.match_pair(imgs[2 * p].astype(np.float64), imgs[2 * p + 1].astype(np.float64), cfg)
         got = set(zip(res[p][0].tolist(), res[p][1].tolist()))
         assert got == {(a, b) for a, b, _ in api.matches.pairs}
+
+
+def test_pipelined_step_equals_step(r2):
+    """Throughput mode: filter bank of batch i next to the features of batch
+    i-1 on two streams; each batch's matches equal the plain step's."""
+    from paper_2303_00319_b200 import synth
+    cfg = r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=800)
+    imgs_a, _ = synth.make_batch(2, 256, seed0=10)
+    imgs_b, _ = synth.make_batch(2, 256, seed0=20)
+    pipe = r2.BatchPipeline(2, 256, 256, cfg)
+    want = []
+    for imgs in (imgs_a, imgs_b):
+        pipe.load(imgs)
+        pipe.step()
+        torch.cuda.synchronize()
+        want.append({k: v.clone() for k, v in pipe.m.items()})
+    pipe.capture_pipelined()
+    pipe.images.copy_(torch.from_numpy(imgs_a))
+    pipe._alt.copy_(torch.from_numpy(imgs_b))
+    pipe.pipelined_step(0)          # filter bank of A
+    pipe.pipelined_step(1)          # filter bank of B, features of A
+    torch.cuda.synchronize()
+    assert all(torch.equal(want[0][k], pipe.m[k]) for k in want[0])
+    pipe.pipelined_step(0)          # features of B (filter bank of A again)
+    torch.cuda.synchronize()
+    assert all(torch.equal(want[1][k], pipe.m[k]) for k in want[1])
