@@ -30,8 +30,8 @@ constexpr int kIn = kTile + 2 * kHalo;    // 40
 constexpr int kSc = kTile + 2;            // 34
 constexpr int kMaxNbr = 32;
 
-__constant__ int c_ring_dx[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
-__constant__ int c_ring_dy[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+// Bresenham circle of radius 3 (ref: detector.py:21-26, _CIRCLE) is spelled
+// out at compile time in fast_score, so the ring loads use immediate offsets
 
 R2_DEV unsigned long long ord_key(double v) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(v);
@@ -117,12 +117,47 @@ R2_DEV double div_span(double x, double lo, double span, double y) {
   return fma(r, y, q);
 }
 
+// FAST score of the pixel at staged position (cy, cx) (ref: detector.py:50-84
+// through the monotone normalisation, see the file header)
+template <class T>
+R2_DEV double fast_score(const T (*sv)[kIn + 1], int cy, int cx, double lo, double span, double rspan) {
+  constexpr int dx[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
+  constexpr int dy[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+  T v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = sv[cy + dy[k]][cx + dx[k]];
+  T A, B;
+  arc_extrema(v, A, B);
+  const T c = sv[cy][cx];
+  // ref: max(max(na - nc, nc - nb), 0) with n = (v - lo) / span; a side
+  // whose raw extreme does not beat the centre contributes <= 0: skipped
+  double s = 0.0;
+  if (A > c || B < c) {
+    const double nc = div_span((double)c, lo, span, rspan);
+    if (A > c) s = fmax(s, div_span((double)A, lo, span, rspan) - nc);
+    if (B < c) s = fmax(s, nc - div_span((double)B, lo, span, rspan));
+  }
+  return s;
+}
+
+// score of score-tile position (sy, sx) = image pixel (y, x): -inf outside the
+// image (never wins the NMS), 0 in the 3-pixel frame (ref: detector.py:63-76)
+template <class T>
+R2_DEV double tile_score(const T (*sv)[kIn + 1], int sy, int sx, int y, int x, int H, int W, bool inner, double lo,
+                         double span, double rspan) {
+  if (!inner) {
+    if (y < 0 || y >= H || x < 0 || x >= W) return -DBL_MAX;
+    if (y < 3 || y >= H - 3 || x < 3 || x >= W - 3) return 0.0;
+  }
+  return fast_score(sv, sy + kHalo - 1, sx + kHalo - 1, lo, span, rspan);
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, const T* __restrict__ maxs, int H, int W,
                                                   const unsigned long long* __restrict__ mm, double thr,
                                                   int margin, int nm, K128* __restrict__ cand,
                                                   unsigned* __restrict__ cnt, size_t cap) {
-  __shared__ T sv[kIn][kIn + 1];
+  __shared__ __align__(16) T sv[kIn][kIn + 1];
   __shared__ double ss[kSc][kSc + 1];
   const int plane = blockIdx.z;
   const int kind = nm == 2 ? (plane & 1) : 0;
@@ -134,43 +169,43 @@ __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, co
   const double rspan = 1.0 / span;
   const int ty0 = blockIdx.y * kTile, tx0 = blockIdx.x * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < kIn; r += 8) {
-    const int yy = ty0 - kHalo + r;
-    const bool row_in = yy >= 0 && yy < H;
-    const T* prow = p + (size_t)(row_in ? yy : 0) * W;
-    for (int cx = lane; cx < kIn; cx += 32) {
-      const int xx = tx0 - kHalo + cx;
-      sv[r][cx] = (row_in && xx >= 0 && xx < W) ? prow[xx] : T(0);
+  // tile-uniform: the staged input lies inside the image / every scored
+  // pixel is at least 3 pixels from the border
+  const bool in_img = ty0 - kHalo >= 0 && ty0 + kTile + kHalo <= H && tx0 - kHalo >= 0 && tx0 + kTile + kHalo <= W;
+  const bool inner = ty0 - 1 >= 3 && ty0 + kTile + 1 <= H - 3 && tx0 - 1 >= 3 && tx0 + kTile + 1 <= W - 3;
+  if (sizeof(T) == 4 && in_img && (W & 3) == 0) {
+    // 40 x 40 floats as 10 float4 per row (the row start tx0 - 4 is 16-byte aligned)
+    for (int i = threadIdx.x; i < kIn * (kIn / 4); i += 256) {
+      const int r = i / (kIn / 4), q = i - r * (kIn / 4);
+      const float4 f = __ldg(reinterpret_cast<const float4*>(p + (size_t)(ty0 - kHalo + r) * W + tx0 - kHalo) + q);
+      T* d = &sv[r][4 * q];
+      d[0] = f.x; d[1] = f.y; d[2] = f.z; d[3] = f.w;
+    }
+  } else {
+    for (int r = warp; r < kIn; r += 8) {
+      const int yy = ty0 - kHalo + r;
+      const bool row_in = yy >= 0 && yy < H;
+      const T* prow = p + (size_t)(row_in ? yy : 0) * W;
+      for (int cx = lane; cx < kIn; cx += 32) {
+        const int xx = tx0 - kHalo + cx;
+        sv[r][cx] = (row_in && xx >= 0 && xx < W) ? prow[xx] : T(0);
+      }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kSc * kSc; i += blockDim.x) {
-    const int sy = i / kSc, sx = i - sy * kSc;
-    const int y = ty0 - 1 + sy, x = tx0 - 1 + sx;
-    double s;
-    if (y < 0 || y >= H || x < 0 || x >= W) {
-      s = -DBL_MAX;
-    } else if (y < 3 || y >= H - 3 || x < 3 || x >= W - 3) {
-      s = 0.0;
-    } else {
-      const int cy = sy + kHalo - 1, cx = sx + kHalo - 1;
-      T v[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = sv[cy + c_ring_dy[k]][cx + c_ring_dx[k]];
-      T A, B;
-      arc_extrema(v, A, B);
-      const T c = sv[cy][cx];
-      // ref: max(max(na - nc, nc - nb), 0) with n = (v - lo) / span; the
-      // normalisation is monotone, so a side whose raw extreme does not
-      // beat the centre contributes <= 0 and is skipped
-      s = 0.0;
-      if (A > c || B < c) {
-        const double nc = div_span((double)c, lo, span, rspan);
-        if (A > c) s = fmax(s, div_span((double)A, lo, span, rspan) - nc);
-        if (B < c) s = fmax(s, nc - div_span((double)B, lo, span, rspan));
-      }
-    }
-    ss[sy][sx] = s;
+  // interior 32 x 32 scores: warp = row group, lane = column
+#pragma unroll 1
+  for (int r = warp; r < kTile; r += 8)
+    ss[r + 1][lane + 1] = tile_score(sv, r + 1, lane + 1, ty0 + r, tx0 + lane, H, W, inner, lo, span, rspan);
+  // the one-pixel border ring of the score tile (132 positions)
+  if (threadIdx.x < 4 * kSc - 4) {
+    int sy, sx;
+    const int i = threadIdx.x;
+    if (i < kSc) { sy = 0; sx = i; }
+    else if (i < 2 * kSc) { sy = kSc - 1; sx = i - kSc; }
+    else if (i < 2 * kSc + kTile) { sy = 1 + i - 2 * kSc; sx = 0; }
+    else { sy = 1 + i - 2 * kSc - kTile; sx = kSc - 1; }
+    ss[sy][sx] = tile_score(sv, sy, sx, ty0 - 1 + sy, tx0 - 1 + sx, H, W, false, lo, span, rspan);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
