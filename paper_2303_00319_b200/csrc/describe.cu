@@ -215,6 +215,22 @@ R2_DEV void emit_row(const DescribeArgs& a, const DescConst& c, const unsigned* 
   }
 }
 
+// 90-degree pick: with cos/sin snapped to (0, 1) the rotated sample (i, j)
+// reads the axis-patch pixel (j, P-1-i) (ref: descriptor.py:46-82, P even), so
+// rotated cell (R, C) is axis cell (C, g-1-R): a permutation of the axis
+// counts, no gather
+R2_DEV void emit_row_rot90(const DescribeArgs& a, const DescConst& c, const unsigned* cnt, int pivot, __half* row) {
+  for (int i = threadIdx.x; i < a.stride; i += kT) {
+    unsigned v = 0;
+    if (i < c.dim) {
+      const int cell = i / c.O, w = i % c.O;
+      const int R = cell / c.g, C = cell % c.g;
+      v = cnt[(C * c.g + (c.g - 1 - R)) * c.O + (w + pivot - 1) % c.O];
+    }
+    row[i] = __uint2half_rn(v);
+  }
+}
+
 template <int CS>
 __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ mim, DescribeArgs a,
                                                   DescConst c, GatherTables tab, __half* __restrict__ slot_rows,
@@ -359,9 +375,13 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   // (at most two) are counted into their own buffers; then one barrier
   const bool rot_mode = c.mode == 2 && c.rotate;
   int nrot = 0;
+  const int dom90 = (c.O % 2 == 0 && c.P % 2 == 0) ? c.O / 2 + 1 : -1;
   for (int q = 0; q < np; ++q) {
     const int dom = s_pick[q];
-    if (rot_mode && dom != 1) {
+    if (rot_mode && dom == dom90) {
+      emit_row_rot90(a, c, cnt, dom, slot_rows + (slot0 + q) * a.stride);
+      if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[0]; }
+    } else if (rot_mode && dom != 1) {
       count_rotated<CS>(c, ctr, tab.soff + (size_t)(dom - 1) * c.P * c.P, cnt_rot[nrot], &s_sq[1 + nrot]);
       ++nrot;
     } else {
@@ -375,7 +395,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
     int r = 0;
     for (int q = 0; q < np; ++q) {
       const int dom = s_pick[q];
-      if (!(rot_mode && dom != 1)) continue;
+      if (!(rot_mode && dom != 1 && dom != dom90)) continue;
       emit_row(a, c, cnt_rot[r], dom, slot_rows + (slot0 + q) * a.stride);
       if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[1 + r]; }
       ++r;
