@@ -169,11 +169,12 @@ R2_DEV float transfer_s(float lnr, float th, float ll, float ang, float a2, floa
 // (ky < N/2 <=> m < 16), and the imaginary part takes a sign.  The spectrum
 // buffer holds the periodic copy S[N] = S[0], so the mirror index needs no wrap.
 template <int G, class Sync>
-R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float* Ln, const float* Th,
+R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* Geo,
                          float2* buf, float2* Qb, int xo, int t, bool mir, Sync& sync) {
   constexpr int N = 32 * G;
   constexpr int PS = G + G / 32;                          // padded stride of one m step
   const int W = c.W, F = c.S * c.O;
+  // pad32(N - t - G m) and pad32(t + G m) as base -/+ PS * m (t < G, G % 32 == 0)
   const float2* sp = Sc + (mir ? (N + N / 32) - t - ((t + 31) >> 5) : t + (t >> 5));
   const int sstep = mir ? -PS : PS;
   const float tsg = mir ? -1.f : 1.f;                     // theta_m = +-pi - theta
@@ -188,8 +189,9 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float* Ln
     for (int m = 0; m < 32; ++m) {
       const int ky = t + G * m;
       const float2 sv = sp[sstep * m];
-      const float th = fmaf(tsg, Th[ky], m < 16 ? tpi : -tpi);
-      const float gv = transfer_s(Ln[ky], th, ll, ang, a2, b2);
+      const float2 gq = Geo[ky];                         // (ln r, theta): one 8-byte load
+      const float th = fmaf(tsg, gq.y, m < 16 ? tpi : -tpi);
+      const float gv = transfer_s(gq.x, th, ll, ang, a2, b2);
       // conj(spectrum * G) for the inverse; the mirror reads S(-ky, kx) = conj S(ky, W - kx)
       v[m] = __fmul2_rn(sv, make_float2(gv, gv * ysg));
     }
@@ -222,9 +224,8 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     constexpr int NS = CG;           // spectrum columns held
     constexpr int PL = padded_len(N);
     float2* S = sm;                                              // [NS][PL]
-    float* glnr = reinterpret_cast<float*>(sm + NS * PL);        // [NS][N]
-    float* gth = glnr + NS * N;                                  // [NS][N]
-    float2* bufs = reinterpret_cast<float2*>(gth + NS * N);      // [NG][PL]
+    float2* geo = sm + NS * PL;                                  // [NS][N] (ln r, theta)
+    float2* bufs = geo + NS * N;                                 // [NG][PL]
     const int g = threadIdx.x / G, t = threadIdx.x % G;
     float2* buf = bufs + g * PL;
     const int kx0 = blockIdx.x * CG;
@@ -246,8 +247,7 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     for (int i = threadIdx.x; i < NS * N; i += ColsCfg<G>::T) {
       float lnr, L2, th;
       geometry(c, i % N, min(kx0 + i / N, Wh - 1), lnr, L2, th);
-      glnr[i] = lnr;
-      gth[i] = th;
+      geo[i] = make_float2(lnr, th);
       // the radius-only factor lowpass / (H*W) goes into the spectrum (the
       // mirror column has the same radius); 0 at DC
       const int cc = i / N, ky = i % N;
@@ -265,11 +265,10 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     if (!valid) return;              // whole group idles; no CTA barrier follows
     const int xo = mir ? W - kx : kx;
     const float2* Sc = S + cc * PL;
-    const float* Ln = glnr + cc * N;
-    const float* Th = gth + cc * N;
+    const float2* Geo = geo + cc * N;
     if constexpr (G >= 32) {
-      if constexpr (G <= 32) cols_filters<G>(c, Sc, Ln, Th, buf, Qb, xo, t, mir != 0, sw);
-      else cols_filters<G>(c, Sc, Ln, Th, buf, Qb, xo, t, mir != 0, sn);
+      if constexpr (G <= 32) cols_filters<G>(c, Sc, Geo, buf, Qb, xo, t, mir != 0, sw);
+      else cols_filters<G>(c, Sc, Geo, buf, Qb, xo, t, mir != 0, sn);
       return;
     } else {
     const float a2 = c.a2, b2 = c.b2;
@@ -279,7 +278,7 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const int ky = t + G * m;
-        float th = Th[ky];
+        float th = Geo[ky].y;
         float2 sv;
         if (mir) {
           sv = Sc[pad32((N - ky) & (N - 1))];       // S(-ky, kx) = conj S(ky, W - kx)
@@ -288,7 +287,7 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
           sv = Sc[pad32(ky)];
           sv.y = -sv.y;
         }
-        const float gv = transfer_s(Ln[ky], th, ll, ang, a2, b2);
+        const float gv = transfer_s(Geo[ky].x, th, ll, ang, a2, b2);
         v[m] = make_float2(sv.x * gv, sv.y * gv);   // conj(spectrum * G) for the inverse
       }
       fft_fast<G>(v, buf, c.tw_h, t, sw);
