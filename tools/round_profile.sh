@@ -13,6 +13,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --csv --log-file gpurun_out/bench_launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
     > gpurun_out/bench_ncu_$TAG.log 2>&1
 echo "launch list rc=$?"
-ncu --set full --import-source on --clock-control none -k regex:$TOP -s 40 -c 1 -o gpurun_out/full_$TAG \
+ncu --set full --import-source on --clock-control none -k regex:$TOP -s 2 -c 1 -o gpurun_out/full_$TAG \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/full_ncu_$TAG.log 2>&1
 echo "full capture rc=$?"
