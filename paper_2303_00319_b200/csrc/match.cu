@@ -36,27 +36,38 @@ namespace r2 {
 namespace {
 
 constexpr int BM = 128;            // target rows per CTA (UMMA M)
-constexpr int BN = 128;            // reference columns per tile (UMMA N)
+constexpr int BN = 256;            // reference columns per tile (UMMA N)
 constexpr int BK = 64;             // fp16 elements per 128-byte swizzle atom
 constexpr int KBOX = 4;            // K boxes of 64 -> 256 >= 224
 constexpr int A_BOX = BM * BK * 2;             // 16 KB per K box
-constexpr int B_BOX = BN * BK * 2;             // 16 KB per K box
+constexpr int B_BOX = BN * BK * 2;             // 32 KB per K box (one ring stage)
 constexpr int A_BYTES = KBOX * A_BOX;          // 64 KB, resident
-constexpr int B_BYTES = KBOX * B_BOX;          // 64 KB per stage
-constexpr int STAGES = 2;
-constexpr int NACC = 4;                        // TMEM accumulator buffers
-constexpr int TMEM_COLS = NACC * BN;
-constexpr int NEPI = BN / 32 * 4;             // epilogue warps: 4 lane quarters x BN/32 column blocks
+constexpr int NSTAGE = 4;                      // B ring: K boxes in flight
+constexpr int NACC = 2;                        // TMEM accumulator buffers
+constexpr int TMEM_COLS = NACC * BN;           // 512: all of TMEM
+constexpr int NEPI = 16;                       // epilogue warps: 4 lane quarters x 4 column groups
+constexpr int CPW = BN / 32 / (NEPI / 4);      // 32-column chunks per epilogue warp per tile
 constexpr int GEMM_THREADS = 64 + NEPI * 32;  // producer, MMA, epilogue warps
-constexpr int BAR_OFF = A_BYTES + STAGES * B_BYTES;
+constexpr int BAR_OFF = A_BYTES + NSTAGE * B_BOX;
 constexpr int SMEM_GEMM = BAR_OFF + 256 + NEPI * 64 * 4 + 4 * (NEPI / 4 - 1) * BM * 4 + 1024;
+static_assert(SMEM_GEMM <= 227 * 1024, "GEMM shared memory");
 
 #ifdef R2_GEMM_TRACE
-// development trace: clock64 stamps of the pipeline roles of CTA (0, 0)
+// development trace: clock64 stamps of the pipeline roles of CTA (0, 0), and
+// per CTA (SM id, globaltimer start / end, tiles)
 __device__ unsigned long long g_trace[8][512];
+__device__ unsigned long long g_cta[8192][4];
 #define R2_TR(ev, i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (i) < 512) g_trace[ev][i] = clock64(); } while (0)
+R2_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define R2_CTA(slot, val) do { const unsigned b_ = blockIdx.y * gridDim.x + blockIdx.x; \
+  if (threadIdx.x == 0 && b_ < 8192) g_cta[b_][slot] = (val); } while (0)
 #else
 #define R2_TR(ev, i) do {} while (0)
+#define R2_CTA(slot, val) do {} while (0)
 #endif
 
 struct Part {
@@ -81,7 +92,7 @@ R2_DEV uint64_t smem_desc(uint32_t addr) {
   return d;
 }
 
-// kind::f16 instruction descriptor: f16 x f16 -> f32, both K-major, M=128, N=128
+// kind::f16 instruction descriptor: f16 x f16 -> f32, both K-major, M=128, N=BN
 constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
 
@@ -170,9 +181,9 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
   uint8_t* sA = smem;
   uint8_t* sB = smem + A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
-  uint64_t* full = bars;                 // [STAGES]
-  uint64_t* empty = bars + STAGES;       // [STAGES]
-  uint64_t* a_full = bars + 2 * STAGES;
+  uint64_t* full = bars;                 // [NSTAGE]
+  uint64_t* empty = bars + NSTAGE;       // [NSTAGE]
+  uint64_t* a_full = bars + 2 * NSTAGE;
   uint64_t* t_full = a_full + 1;         // [NACC]
   uint64_t* t_empty = t_full + NACC;     // [NACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + NACC);
@@ -180,6 +191,15 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
   float* s_mrg_f = s_inv + NEPI * 64;                              // [2][NB-1][BM] best / D of blocks 1..
   int* s_mrg_i = reinterpret_cast<int*>(s_mrg_f + 2 * (NEPI / 4 - 1) * BM);   // [2][NB-1][BM] q / column
 
+#ifdef R2_GEMM_TRACE
+  {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    R2_CTA(0, smid);
+    R2_CTA(1, gtimer());
+    R2_CTA(3, 0ull);
+  }
+#endif
   const int pair = blockIdx.y;
   const int split = blockIdx.x % p.splits;
   const int mt = blockIdx.x / p.splits;
@@ -201,11 +221,12 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
     return;
   }
   const int ntiles = nt1 - nt0;
+  R2_CTA(3, (unsigned long long)ntiles);
   const int rowA = tb * p.cap + mt * BM;
   const int rowB0 = rb * p.cap;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NSTAGE; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(a_full, 1);
     for (int s = 0; s < NACC; ++s) { mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], NEPI); }
     mbar_fence_init();
@@ -228,14 +249,15 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
       mbar_expect_tx(a_full, A_BYTES);
       for (int kb = 0; kb < KBOX; ++kb) tma_load_2d(sA + kb * A_BOX, &tmapA, kb * BK, rowA, a_full);
       for (int i = 0; i < ntiles; ++i) {
-        const int s = i % STAGES;
-        R2_TR(0, i);
-        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-        R2_TR(1, i);
-        mbar_expect_tx(&full[s], B_BYTES);
         const int rowB = rowB0 + (nt0 + i) * BN;
-        for (int kb = 0; kb < KBOX; ++kb)
-          tma_load_2d(sB + s * B_BYTES + kb * B_BOX, &tmapB, kb * BK, rowB, &full[s]);
+        R2_TR(0, i);
+        for (int kb = 0; kb < KBOX; ++kb) {
+          const int u = i * KBOX + kb, s = u % NSTAGE;
+          mbar_wait(&empty[s], ((u / NSTAGE) & 1) ^ 1);
+          if (kb == 0) R2_TR(1, i);
+          mbar_expect_tx(&full[s], B_BOX);
+          tma_load_2d(sB + s * B_BOX, &tmapB, kb * BK, rowB, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -244,22 +266,25 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
       mbar_wait(a_full, 0);
       const uint32_t a_base = smem_u32(sA);
       for (int i = 0; i < ntiles; ++i) {
-        const int s = i % STAGES, acc = i % NACC;
+        const int acc = i % NACC;
         R2_TR(2, i);
-        mbar_wait(&full[s], (i / STAGES) & 1);
-        R2_TR(3, i);
         mbar_wait(&t_empty[acc], ((i / NACC) & 1) ^ 1);
         R2_TR(4, i);
-        tc_fence_after();
-        const uint32_t b_base = smem_u32(sB + s * B_BYTES);
         const uint32_t d = tmem + acc * BN;
+        // 14 K-steps of 16 over the 4 boxes (the last box holds K 192..223 + zero fill)
 #pragma unroll
-        for (int ks = 0; ks < 14; ++ks) {
-          const uint32_t ka = (ks >> 2) * A_BOX + (ks & 3) * 32;
-          const uint32_t kb = (ks >> 2) * B_BOX + (ks & 3) * 32;
-          mma_f16(d, smem_desc(a_base + ka), smem_desc(b_base + kb), ks > 0 ? 1u : 0u);
+        for (int kb = 0; kb < KBOX; ++kb) {
+          const int u = i * KBOX + kb, s = u % NSTAGE;
+          mbar_wait(&full[s], (u / NSTAGE) & 1);
+          if (kb == 0) R2_TR(3, i);
+          tc_fence_after();
+          const uint32_t b_base = smem_u32(sB + s * B_BOX);
+#pragma unroll
+          for (int kk = 0; kk < (kb == KBOX - 1 ? 2 : 4); ++kk)
+            mma_f16(d, smem_desc(a_base + kb * A_BOX + kk * 32), smem_desc(b_base + kk * 32),
+                    (kb | kk) ? 1u : 0u);
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
         mma_commit(&t_full[acc]);
         R2_TR(5, i);
       }
@@ -277,12 +302,13 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
     // the new chunk becomes R.  R is resolved once more after the last tile.
     // Record events are rare per row (~ln n) but frequent per warp, so (b)
     // is kept branch-light; exact work happens only for (c) and at the end.
-    constexpr int NB = NEPI / 4;                    // column blocks per tile (BN / 32)
+    constexpr int NB = NEPI / 4;                    // column groups (warps per lane quarter)
     const int e = warp - 2;
     const int q = warp & 3, h = e >> 2;
     const int row_loc = q * 32 + lane;
     const int row = mt * BM + row_loc;
-    float* inv_buf = s_inv + e * 64;                // two 32-float buffers (current / next tile)
+    const bool row_ok = row < n_t;
+    float* inv_buf = s_inv + e * 64;                // two 32-float buffers (current / next chunk)
     const int* sq = p.sqnorm + (size_t)rb * p.cap;
     float best = -1.f, bestD = 0.f;
     int bestq = 1, bestcol = -1;
@@ -291,37 +317,48 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
     int r_c0 = -1;
 #pragma unroll
     for (int j = 0; j < 32; ++j) rv[j] = 0.f;
+    // chunk j = CPW * tile + k covers columns tile * BN + (h + NB * k) * 32 .. + 31:
+    // increasing along j, so ties keep the first column
+    auto chunk_c0 = [&](int j) { return (nt0 + j / CPW) * BN + (h + NB * (j % CPW)) * 32; };
+    const int nch = ntiles * CPW;
     int q_nxt;
     {
-      const int c = nt0 * BN + h * 32 + lane;
-      q_nxt = c < n_r ? __ldg(&sq[c]) : 0;          // first tile's squared norms
+      const int c = chunk_c0(0) + lane;
+      q_nxt = c < n_r ? __ldg(&sq[c]) : 0;          // first chunk's squared norms
     }
-    // iteration i == ntiles is virtual: it only resolves the pending chunk
+    // iteration j == nch is virtual: it only resolves the pending chunk
     // (one call site for the exact path keeps the code and register use small)
-    for (int i = 0;; ++i) {
-      const bool last = i == ntiles;
+    for (int j = 0;; ++j) {
+      const bool last = j == nch;
+      const int i = j / CPW, k = j % CPW;
       const int acc = i % NACC;
-      const int c0 = (nt0 + i) * BN + h * 32;
+      const int c0 = chunk_c0(j);
       float v[32];
-      bool rec = false, near = last;
+      // rows past the target count (the last M-tile's padding) never take the
+      // exact path: their zero / stale rows would tie on every chunk
+      bool rec = false, near = last && row_ok;
       float cm = 0.f;
       if (!last) {
-        float* ic = inv_buf + (i & 1) * 32;
+        float* ic = inv_buf + (j & 1) * 32;
         ic[lane] = inv_norm(q_nxt);
         {
-          const int c = c0 + BN + lane;
-          q_nxt = (i + 1 < ntiles && c < n_r) ? __ldg(&sq[c]) : 0;   // next tile, in flight
+          const int c = chunk_c0(j + 1) + lane;
+          q_nxt = (j + 1 < nch && c < n_r) ? __ldg(&sq[c]) : 0;   // next chunk, in flight
         }
         __syncwarp();
-        if (e == 0 && lane == 0) R2_TR(6, i);
-        mbar_wait(&t_full[acc], (i / NACC) & 1);
-        if (e == 0 && lane == 0) R2_TR(7, i);
-        tc_fence_after();
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + h * 32, v);
-        // the chunk is in registers: hand the accumulator back to the MMA warp now
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&t_empty[acc]);
+        if (k == 0) {
+          if (e == 0 && lane == 0) R2_TR(6, i);
+          mbar_wait(&t_full[acc], (i / NACC) & 1);
+          if (e == 0 && lane == 0) R2_TR(7, i);
+          tc_fence_after();
+        }
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + (h + NB * k) * 32, v);
+        if (k == CPW - 1) {
+          // the tile's chunks are in registers: hand the accumulator back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&t_empty[acc]);
+        }
         if (c0 < n_r) {                               // warp-uniform
           // screening maximum; invalid tail columns carry inv = 0 (score 0)
           const float4* iv = reinterpret_cast<const float4*>(ic);
@@ -334,8 +371,8 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
             cm = fmaxf(fmaxf(cm, b.x), b.y);
           }
           const float T = fmaxf(r_cm, best);
-          rec = cm > T * (1.f + 1e-5f);               // for T < 0 (nothing yet) always true
-          near = !rec && cm >= T * (1.f - 1e-5f);
+          rec = row_ok && cm > T * (1.f + 1e-5f);     // for T < 0 (nothing yet) always true
+          near = row_ok && !rec && cm >= T * (1.f - 1e-5f);
         }
       }
       if (__any_sync(0xffffffffu, rec || near)) {
@@ -345,10 +382,11 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
         if (rec) { best = -1.f; bestD = 0.f; bestq = 1; bestcol = -1; }
         const bool take = rec || near;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) rv[j] = take ? v[j] : rv[j];
+        for (int jj = 0; jj < 32; ++jj) rv[jj] = take ? v[jj] : rv[jj];
         r_cm = take ? cm : r_cm;
         r_c0 = take ? c0 : r_c0;
       }
+      if (last) break;                                // also for warps of padding rows only
     }
     // merge the NB column blocks of each row (exact; ties -> smaller column = smaller kp id)
     if (h > 0) {
@@ -389,6 +427,9 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(TMEM_COLS));
   }
+#ifdef R2_GEMM_TRACE
+  R2_CTA(2, gtimer());
+#endif
 }
 
 // ------------------------------------------------------------ index / combine
@@ -801,5 +842,8 @@ int match_vectors_run(const double* R, const int* rkp, int nr, const double* T, 
 #ifdef R2_GEMM_TRACE
 extern "C" int rift2_debug_gemm_trace(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, r2::g_trace, sizeof(r2::g_trace)) == cudaSuccess ? 0 : 3;
+}
+extern "C" int rift2_debug_gemm_ctas(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, r2::g_cta, sizeof(r2::g_cta)) == cudaSuccess ? 0 : 3;
 }
 #endif
