@@ -127,3 +127,35 @@ def test_full_size_batch_invariance(eng):
     for k in ("ref", "tgt", "dist"):
         assert np.array_equal(m[k][0][:n0], m[k][1][:n1]), k
     assert np.all(np.diff(m["dist"][0][:n0]) >= 0)
+
+
+def test_fields_4096_vs_oracle(eng):
+    """configs[3] size (4096^2, blob sigma x4): the G = 128 FFT path against the
+    oracle on the full image."""
+    from paper_2303_00319_b200 import synth
+    a, _, _ = synth.make_pair(4096, seed=1, looks=None)
+    bank = O.Bank(scale_mult=1.6, sigma_on_f=0.75)
+    out = _fields_gpu(eng, a[None], bank, extras=False)
+    ref = O.fields(a, bank, workers=16)
+    assert max_norm_err(out["mmax"][0], ref["moment_max"]) <= 1e-4
+    assert max_norm_err(out["mmin"][0], ref["moment_min"]) <= 1e-4
+    assert np.mean(out["mim"][0] == ref["mim"]) >= 0.999
+
+
+def test_c4_pair_runs_and_matches(eng):
+    """configs[3] end to end on one GPU: 4096^2 pair, up to 20,000 keypoints;
+    the recovered matches agree with the generator's similarity transform.
+    (Without the 4-look speckle: with it the matches are wrong on the CPU
+    path too -- SURVEY D5 -- and this test is about the large-size path.)"""
+    import paper_2303_00319_b200 as r2
+    from paper_2303_00319_b200 import synth
+    a, b, truth = synth.make_pair(4096, seed=2, looks=None)
+    cfg = r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=20000)
+    res = r2.match_pair(a, b, cfg)
+    assert len(res.ref.keypoints) > 5000
+    rx = np.array([[k.x, k.y] for k in res.ref.keypoints])
+    tx = np.array([[k.x, k.y] for k in res.tgt.keypoints])
+    r = np.array([p[0] for p in res.matches.pairs])
+    t = np.array([p[1] for p in res.matches.pairs])
+    resid = np.linalg.norm(truth.apply(rx[r]) - tx[t], axis=1)
+    assert (resid < 3).sum() >= 1000
