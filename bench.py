@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pairs", type=int, default=16, help="pairs per GPU per step")
     ap.add_argument("--size", type=int, default=1024)
+    ap.add_argument("--max-kp", type=int, default=5000, help="max keypoints per image (configs[3]: 20000)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -49,7 +50,7 @@ def workload(args, n):
     return {"workload": f"{args.pairs} independent {args.size}x{args.size} pairs per GPU per step "
                         f"(BASELINE generator: blobs+band-limited noise, rotation+translation, inversion/gamma, "
                         f"4-look speckle; seeds rank*{args.pairs}+0..{args.pairs - 1}); 4x6 log-Gabor "
-                        f"scale_mult 1.6 sigma_on_f 0.75, <=5000 FAST keypoints, RIFT2 216-D, NN matching",
+                        f"scale_mult 1.6 sigma_on_f 0.75, <={args.max_kp} FAST keypoints, RIFT2 216-D, NN matching",
             "pairs_per_gpu": args.pairs, "size": args.size, "global_pairs_per_step": args.pairs * n,
             "parallelism": f"dp{n} (pairs sharded, no collective)",
             "l2": "inputs + inter-pass planes (192 MB/image) far exceed the 126 MB L2"}
@@ -290,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2303_00319_b200 import BatchPipeline, RiftConfig, synth
 
     torch.cuda.set_device(local_rank)
-    cfg = RiftConfig(**BASE_PARAMS)
+    cfg = RiftConfig(max_keypoints=args.max_kp, **BASE_PARAMS)
     imgs, _ = synth.make_batch(args.pairs, args.size, seed0=rank_seed0(rank, args.pairs))
     pipe = BatchPipeline(args.pairs, args.size, args.size, cfg)
     pipe.load(imgs)
