@@ -564,6 +564,52 @@ R2_DEV float rcp_approx(float x) {
   return y;
 }
 
+// Phase congruency of two pixels at once in the fp32x2 lanes (SC scales,
+// ref: loggabor.py:193-251): the FP work of the pixel phase in packed
+// instructions; square roots, reciprocals and exp stay per lane (MUFU).  The
+// weight and 1 / (sum of amplitudes) share one reciprocal:
+// pc = en / ((1 + exp(g (cut - spread))) (sa + eps)).
+template <int SC>
+R2_DEV void pc_pair(const float2* __restrict__ b0, const float2* __restrict__ b1, int PL, float T, float inv_sm1,
+                    float gain, float cut, float2& sa, float2& pc) {
+  float2 X[SC], Y[SC];
+#pragma unroll
+  for (int s = 0; s < SC; ++s) {
+    const float2 z0 = b0[s * PL], z1 = b1[s * PL];
+    X[s] = make_float2(z0.x, z1.x);
+    Y[s] = make_float2(z0.y, z1.y);
+  }
+  float2 se = make_float2(0.f, 0.f), so = se;
+  sa = se;
+  float mx0 = 0.f, mx1 = 0.f;
+#pragma unroll
+  for (int s = 0; s < SC; ++s) {
+    const float2 q = __ffma2_rn(X[s], X[s], __fmul2_rn(Y[s], Y[s]));
+    const float2 a = make_float2(sqrt_approx(q.x), sqrt_approx(q.y));
+    se = __fadd2_rn(se, X[s]);
+    so = __fadd2_rn(so, Y[s]);
+    sa = __fadd2_rn(sa, a);
+    mx0 = fmaxf(mx0, a.x);
+    mx1 = fmaxf(mx1, a.y);
+  }
+  const float2 q = __ffma2_rn(se, se, __fmul2_rn(so, so));
+  const float2 ixe = make_float2(rcp_approx(sqrt_approx(q.x) + 1e-4f), rcp_approx(sqrt_approx(q.y) + 1e-4f));
+  const float2 me = __fmul2_rn(se, ixe), mo = __fmul2_rn(so, ixe);
+  const float2 nme = make_float2(-me.x, -me.y);
+  float2 en = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int s = 0; s < SC; ++s) {
+    const float2 t1 = __ffma2_rn(X[s], me, __fmul2_rn(Y[s], mo));
+    const float2 t2 = __ffma2_rn(X[s], mo, __fmul2_rn(Y[s], nme));
+    en = __fadd2_rn(en, make_float2(t1.x - fabsf(t2.x), t1.y - fabsf(t2.y)));
+  }
+  en = make_float2(fmaxf(en.x - T, 0.f), fmaxf(en.y - T, 0.f));
+  const float sp0 = fmaf(sa.x, rcp_approx(mx0 + 1e-4f), -1.f) * inv_sm1;
+  const float sp1 = fmaf(sa.y, rcp_approx(mx1 + 1e-4f), -1.f) * inv_sm1;
+  const float e0 = __expf(gain * (cut - sp0)), e1 = __expf(gain * (cut - sp1));
+  pc = make_float2(en.x * rcp_approx((1.f + e0) * (sa.x + 1e-4f)), en.y * rcp_approx((1.f + e1) * (sa.y + 1e-4f)));
+}
+
 // One CTA per row pair (y0, y0+1).  Stage = `ops` orientations of `rr` rows;
 // its buffers (row, orientation, scale) are filled by FFT jobs (scales >= 1)
 // and plain loads of the K3a responses (scale 0), then the per-pixel phase
@@ -653,6 +699,37 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
       for (int oo = 0; oo < no; ++oo) {
         const int o = o0 + oo;
         const float T = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
+        if constexpr (SC > 0 && PIX % 2 == 0) {
+          // pixel pairs (i, i + 1) in the fp32x2 lanes when both are live
+          // (warp-uniform: npix is a multiple of kThreads for these sizes)
+          if (npix == PIX * kThreads && y0 + rbase + rr <= H) {
+#pragma unroll
+            for (int i = 0; i < PIX; i += 2) {
+              const int p0 = threadIdx.x + kThreads * i, p1 = p0 + kThreads;
+              const int r0 = p0 / W, x0 = p0 % W, r1 = p1 / W, x1 = p1 % W;
+              const float2* b0 = sm + ((r0 * ops + oo) * S) * PL + pad32(x0);
+              const float2* b1 = sm + ((r1 * ops + oo) * S) * PL + pad32(x1);
+              float2 sa2, pc2;
+              pc_pair<SC>(b0, b1, PL, T, inv_sm1, gain, cut, sa2, pc2);
+              const float2 pcc = __fmul2_rn(pc2, make_float2(ca, ca)), pcs = __fmul2_rn(pc2, make_float2(sa_o, sa_o));
+              acc_a[i] = fmaf(pcc.x, pcc.x, acc_a[i]);
+              acc_a[i + 1] = fmaf(pcc.y, pcc.y, acc_a[i + 1]);
+              acc_b[i] = fmaf(pcc.x, pcs.x, acc_b[i]);
+              acc_b[i + 1] = fmaf(pcc.y, pcs.y, acc_b[i + 1]);
+              acc_c[i] = fmaf(pcs.x, pcs.x, acc_c[i]);
+              acc_c[i + 1] = fmaf(pcs.y, pcs.y, acc_c[i + 1]);
+              if (sa2.x > best[i]) { best[i] = sa2.x; bidx[i] = o + 1; }
+              if (sa2.y > best[i + 1]) { best[i + 1] = sa2.y; bidx[i + 1] = o + 1; }
+              if (out.a_o || out.pc) {
+                const size_t q0 = (((size_t)b * O + o) * H + y0 + rbase + r0) * W + x0;
+                const size_t q1 = (((size_t)b * O + o) * H + y0 + rbase + r1) * W + x1;
+                if (out.a_o) { out.a_o[q0] = sa2.x; out.a_o[q1] = sa2.y; }
+                if (out.pc) { out.pc[q0] = pc2.x; out.pc[q1] = pc2.y; }
+              }
+            }
+            continue;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < PIX; ++i) {
           const int p = threadIdx.x + kThreads * i;
