@@ -596,12 +596,12 @@ R2_DEV void pc_pair(const float2* __restrict__ b0, const float2* __restrict__ b1
   const float2 ixe = make_float2(rcp_approx(sqrt_approx(q.x) + 1e-4f), rcp_approx(sqrt_approx(q.y) + 1e-4f));
   const float2 me = __fmul2_rn(se, ixe), mo = __fmul2_rn(so, ixe);
   const float2 nme = make_float2(-me.x, -me.y);
-  float2 en = make_float2(0.f, 0.f);
+  // sum_s z_s . m = |S|^2 / (|S| + eps) = q * ixe: only the cross terms are per scale
+  float2 en = __fmul2_rn(q, ixe);
 #pragma unroll
   for (int s = 0; s < SC; ++s) {
-    const float2 t1 = __ffma2_rn(X[s], me, __fmul2_rn(Y[s], mo));
     const float2 t2 = __ffma2_rn(X[s], mo, __fmul2_rn(Y[s], nme));
-    en = __fadd2_rn(en, make_float2(t1.x - fabsf(t2.x), t1.y - fabsf(t2.y)));
+    en = make_float2(en.x - fabsf(t2.x), en.y - fabsf(t2.y));
   }
   en = make_float2(fmaxf(en.x - T, 0.f), fmaxf(en.y - T, 0.f));
   const float sp0 = fmaf(sa.x, rcp_approx(mx0 + 1e-4f), -1.f) * inv_sm1;
@@ -748,12 +748,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
               se += z[s].x; so += z[s].y; sa += a; mx = fmaxf(mx, a);
             }
           }
-          const float ixe = rcp_approx(sqrt_approx(fmaf(se, se, so * so)) + 1e-4f);
+          const float qe = fmaf(se, se, so * so);
+          const float ixe = rcp_approx(sqrt_approx(qe) + 1e-4f);
           const float me = se * ixe, mo = so * ixe;
-          float en = 0.f;
+          // sum_s z_s . m = |S|^2 / (|S| + eps): only the cross terms are per scale
+          float en = qe * ixe;
 #pragma unroll
           for (int s = 0; s < SMAX; ++s)
-            if (SC > 0 || s < S) en += fmaf(z[s].x, me, z[s].y * mo) - fabsf(fmaf(z[s].x, mo, -z[s].y * me));
+            if (SC > 0 || s < S) en -= fabsf(fmaf(z[s].x, mo, -z[s].y * me));
           en = fmaxf(en - T, 0.f);
           const float spread = fmaf(sa, rcp_approx(mx + 1e-4f), -1.f) * inv_sm1;
           const float wgt = rcp_approx(1.f + __expf(gain * (cut - spread)));
