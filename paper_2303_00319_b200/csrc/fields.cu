@@ -458,11 +458,13 @@ __global__ void __launch_bounds__(1024) k_med_bins(const unsigned* __restrict__ 
 }
 
 // gather the float bits of every value falling into one of the two bins;
-// hits are staged per CTA and appended with one global atomic per CTA pass
+// hits are appended warp-aggregated into a per-CTA shared buffer and flushed
+// with one global atomic per CTA pass (16 values per thread per pass)
+constexpr int kCollectVec = 4;                  // float4 loads per thread per pass
 __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ amp0, const MedInfo* __restrict__ info,
                                                      unsigned* __restrict__ cand, unsigned* __restrict__ cnt,
                                                      unsigned n) {
-  __shared__ unsigned s_buf[4 * 256];
+  __shared__ unsigned s_buf[kCollectVec * 4 * 256];
   __shared__ unsigned s_n, s_base;
   const int plane = blockIdx.y;
   const unsigned b0 = info[plane].bin[0], b1 = info[plane].bin[1];
@@ -470,23 +472,55 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
   const float4* A = reinterpret_cast<const float4*>(Ap);
   unsigned* out = cand + (size_t)plane * n;
   const unsigned n4 = (n + 3) / 4;
-  for (unsigned base = blockIdx.x * blockDim.x; base < n4; base += gridDim.x * blockDim.x) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned per_pass = kCollectVec * blockDim.x;
+  for (unsigned base = blockIdx.x * per_pass; base < n4; base += gridDim.x * per_pass) {
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
-    const unsigned i = base + threadIdx.x;
-    float4 q = make_float4(-1.f, -1.f, -1.f, -1.f);
-    if (4 * i + 3 < n) q = A[i];
-    else if (i < n4) {
-      q.x = Ap[4 * i];
-      if (4 * i + 1 < n) q.y = Ap[4 * i + 1];
-      if (4 * i + 2 < n) q.z = Ap[4 * i + 2];
-    }
-    const float vals[4] = {q.x, q.y, q.z, q.w};
+    float4 qv[kCollectVec];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const unsigned bits = __float_as_uint(vals[e]);
-      const bool hit = vals[e] >= 0.f && ((bits >> 19) == b0 || (bits >> 19) == b1);
-      if (hit) s_buf[atomicAdd(&s_n, 1u)] = bits;
+    for (int k = 0; k < kCollectVec; ++k) {
+      const unsigned i = base + k * blockDim.x + threadIdx.x;
+      qv[k] = make_float4(-1.f, -1.f, -1.f, -1.f);
+      if (4 * i + 3 < n) qv[k] = __ldg(&A[i]);
+      else if (i < n4) {
+        qv[k].x = Ap[4 * i];
+        if (4 * i + 1 < n) qv[k].y = Ap[4 * i + 1];
+        if (4 * i + 2 < n) qv[k].z = Ap[4 * i + 2];
+      }
+    }
+    // per-thread hit mask over its 16 values, one warp prefix sum, one
+    // shared atomic per warp, then each thread writes its own hits
+    unsigned mask = 0;
+#pragma unroll
+    for (int k = 0; k < kCollectVec; ++k) {
+      const float vals[4] = {qv[k].x, qv[k].y, qv[k].z, qv[k].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const unsigned hb = __float_as_uint(vals[e]) >> 19;
+        mask |= (vals[e] >= 0.f && (hb == b0 || hb == b1)) ? (1u << (4 * k + e)) : 0u;
+      }
+    }
+    const unsigned cntt = __popc(mask);
+    unsigned incl = cntt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= (unsigned)d) incl += t;
+    }
+    const unsigned wtot = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned wbase = 0;
+    if (lane == 31 && wtot) wbase = atomicAdd(&s_n, wtot);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    unsigned pos = wbase + incl - cntt;
+    if (mask) {                                     // static indices: qv stays in registers
+#pragma unroll
+      for (int k = 0; k < kCollectVec; ++k) {
+        const float vals[4] = {qv[k].x, qv[k].y, qv[k].z, qv[k].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if ((mask >> (4 * k + e)) & 1u) s_buf[pos++] = __float_as_uint(vals[e]);
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0 && s_n) s_base = atomicAdd(&cnt[plane], s_n);
