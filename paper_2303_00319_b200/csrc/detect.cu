@@ -60,10 +60,28 @@ __global__ void __launch_bounds__(256) k_minmax(const T* __restrict__ mins, cons
   const int plane = blockIdx.y;
   const T* p = plane_ptr(mins, maxs, plane, nm, n);
   unsigned long long lo = ~0ull, hi = 0ull;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const unsigned long long k = ord_key((double)p[i]);
-    lo = k < lo ? k : lo;
-    hi = k > hi ? k : hi;
+  if constexpr (sizeof(T) == 4) {
+    // float maps: float4 loads and float min / max; only the warp results
+    // become ordered double keys (the conversion is exact and monotone)
+    float flo = FLT_MAX, fhi = -FLT_MAX;
+    const size_t n4 = ((size_t)reinterpret_cast<uintptr_t>(p) & 15) == 0 ? n / 4 : 0;
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+      const float4 v = __ldg(&p4[i]);
+      flo = fminf(flo, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+      fhi = fmaxf(fhi, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    }
+    for (size_t i = 4 * n4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+      flo = fminf(flo, p[i]);
+      fhi = fmaxf(fhi, p[i]);
+    }
+    if (flo <= fhi) { lo = ord_key((double)flo); hi = ord_key((double)fhi); }
+  } else {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+      const unsigned long long k = ord_key((double)p[i]);
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
+    }
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
@@ -510,7 +528,7 @@ int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, siz
   k_init<<<(planes + 255) / 256, 256, 0, st>>>(mm, cnt, planes);
   const size_t n = (size_t)a.H * a.W;
   {
-    dim3 grid((unsigned)min((size_t)32, (n + 255) / 256), planes);
+    dim3 grid((unsigned)min((size_t)64, (n + 1023) / 1024), planes);
     k_minmax<T><<<grid, 256, 0, st>>>(mins, maxs, nm, n, mm);
   }
   {
