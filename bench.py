@@ -254,6 +254,16 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def tensor_peak():
+    """Dense fp16/bf16 tensor peak (the matching GEMM runs kind::f16)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+    except (OSError, KeyError, ValueError):
+        return 2250.0, "nominal dense bf16 (fallback)"
+
+
 def rank_seed0(rank, pairs):
     """First generator seed of this rank's pairs: ranks own disjoint, contiguous
     seed ranges (configs[2]: the 128-pair batch split over the GPUs)."""
@@ -331,6 +341,18 @@ def run_ours(args, rank, world, local_rank):
         ev[i][1].record()
     torch.cuda.synchronize()
     fields_ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    # matching: the match stage (tensor-core GEMM + exact combine + sort) on
+    # this step's descriptor arrays, K launches timed with CUDA events
+    from paper_2303_00319_b200 import engine
+    em = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for i in range(K):
+        em[i][0].record()
+        engine.match(pipe.d, pipe.dim, pipe.rb, pipe.tb, pipe.K, ws_key="bench_match")
+        em[i][1].record()
+    torch.cuda.synchronize()
+    match_ms = sum(a.elapsed_time(b) for a, b in em) / K
+    dcnt = pipe.d["count"].cpu().numpy().astype(np.int64)
+    match_flops = float(sum(2 * dcnt[2 * q] * dcnt[2 * q + 1] * pipe.dim for q in range(args.pairs)))
 
     # e2e: public API with host buffers -- every step uploads its images from
     # pinned host memory (copy stream, double-buffered against the previous
@@ -360,6 +382,7 @@ def run_ours(args, rank, world, local_rank):
     value = pairs / (total_ms / 1e3)
     e2e = args.pairs * world * KE / (e2e_ms / 1e3)
     peak, peak_src = peaks()
+    tpk, tpk_src = tensor_peak()
     bytes_launch = BYTES_PER_PX * args.size * args.size * 2 * args.pairs
     achieved = bytes_launch / (fields_ms / 1e3) / 1e9
     tr, tr_src = traffic()
@@ -377,6 +400,10 @@ def run_ours(args, rank, world, local_rank):
                          "traffic": tr, "traffic_source": tr_src, "bytes_per_launch": bytes_launch, "launch_ms": fields_ms,
                          "share_of_step": fields_ms / (total_ms / K), "peak_source": peak_src,
                          "note": "filter bank timed alone; in the pipelined step it overlaps the previous batch's features"},
+            "roofline_match": {"bound": "tensor", "kernel": "match stage (k_match_gemm tcgen05 f16 + combine + sort)",
+                               "achieved": match_flops / (match_ms / 1e3) / 1e12, "peak": tpk, "unit": "TFLOP/s",
+                               "frac": match_flops / (match_ms / 1e3) / 1e12 / tpk,
+                               "flops_per_launch": match_flops, "launch_ms": match_ms, "peak_source": tpk_src},
             "clocks": clocks,
             "matches_per_pair": float(np.mean(counts))}
     if world == 1 and not args.no_cpu_baseline:
