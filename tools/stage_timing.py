@@ -13,8 +13,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-from oracle.rift2_oracle import Bank  # noqa: E402  (parameter holder only)
-from paper_2303_00319_b200 import engine, synth  # noqa: E402
+from paper_2303_00319_b200 import RiftConfig, engine, synth  # noqa: E402
 
 
 def main():
@@ -29,7 +28,7 @@ def main():
     imgs = np.concatenate([imgs] * reps)[: 2 * args.pairs]
     print(f"generated in {time.time() - t0:.1f}s", flush=True)
     x = torch.as_tensor(imgs).cuda()
-    bank = Bank(scale_mult=1.6, sigma_on_f=0.75)
+    bank = RiftConfig(scale_mult=1.6, sigma_on_f=0.75).bank_params()
     B = x.shape[0]
     rb = torch.arange(0, B, 2, dtype=torch.int32, device="cuda")
     tb = rb + 1
