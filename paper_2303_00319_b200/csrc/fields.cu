@@ -972,7 +972,7 @@ static cudaError_t launch_pc_s(const float2* Q, const float2* R0, const float* t
 template <int G>
 static cudaError_t launch_pc(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
                              const FieldsConst& c, cudaStream_t st) {
-  if (c.S == 4 && G >= 8 && G <= 64) return launch_pc_s<G, 4>(Q, R0, thr, out, c, st);
+  if (c.S == 4 && G >= 8 && G <= 128) return launch_pc_s<G, 4>(Q, R0, thr, out, c, st);
   return launch_pc_s<G, 0>(Q, R0, thr, out, c, st);
 }
 
