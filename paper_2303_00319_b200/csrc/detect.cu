@@ -12,8 +12,8 @@
 // float64 operations per pixel touch the normalised values.
 //
 // Kernels: k_init -> k_minmax -> k_fast_nms (score + 3x3 NMS + margin +
-// candidate keys) -> k_select_sort (radix-select the max_points smallest
-// (-score, y, x, kind) keys, sort) -> k_merge_suppress (2-px greedy merge of
+// candidate keys) -> k_sel_* (multi-CTA top max_points of the (-score, y, x,
+// kind) keys: histogram, threshold bin, gather, rank) -> k_merge_suppress (2-px greedy merge of
 // corners and edges as a parallel priority MIS, cap).
 #include <cfloat>
 
@@ -251,100 +251,119 @@ __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, co
   }
 }
 
-R2_DEV bool top_bits_le(const K128& k, const K128& pref, int bits) {
-  // compare the top `bits` bits of k and pref as unsigned 128-bit numbers
-  K128 a = k, b = pref;
-  if (bits < 64) {
-    const unsigned long long m = bits == 0 ? 0ull : (~0ull << (64 - bits));
-    a.hi &= m; b.hi &= m; a.lo = 0; b.lo = 0;
-  } else {
-    const int lb = bits - 64;
-    const unsigned long long m = lb == 0 ? 0ull : (~0ull << (64 - lb));
-    a.lo &= m; b.lo &= m;
-  }
-  return !k_less(b, a);
+// ---- multi-CTA top-K selection -------------------------------------------
+// Keys are (-score, y, x, kind) with the score's float64 bits in `hi`, so a
+// monotone log-scale bin of the score orders them coarsely.  A histogram of
+// all candidates finds the bin holding the K-th key (the threshold bin);
+// keys of that bin and above are scattered into per-bin buckets at offsets
+// from a scan of the histogram (higher bins first), and each key's final
+// position is its bucket offset plus its rank among the keys of its own
+// bucket.  Keys are unique (pixel + kind), so positions are a permutation
+// and the first K equal the full sort's first K.
+constexpr int kSelBins = 4096;
+constexpr int kSelCtas = 32;                    // CTAs per plane in the streaming passes
+
+R2_DEV int sel_bin(const K128& k) {
+  // score bits (sign 0): exponent + 7 mantissa bits; scores > threshold >= 2^-20
+  const unsigned long long b = ~k.hi;
+  const long long v = (long long)(b >> 45) - (long long)((1003ull << 7));
+  return v < 0 ? 0 : (v >= kSelBins ? kSelBins - 1 : (int)v);
 }
 
-R2_DEV unsigned digit_of(const K128& k, int d) {   // d = 0..15, MSB first
-  return d < 8 ? (unsigned)(k.hi >> (56 - 8 * d)) & 255u : (unsigned)(k.lo >> (56 - 8 * (d - 8))) & 255u;
-}
-
-// Select the K smallest keys of each plane and sort them.
-__global__ void __launch_bounds__(1024) k_select_sort(const K128* __restrict__ cand, const unsigned* __restrict__ cnt,
-                                                      size_t cap, int K, K128* __restrict__ sorted,
-                                                      K128* __restrict__ tmp, unsigned* __restrict__ nsel) {
-  extern __shared__ K128 s_keys[];
-  __shared__ unsigned h[256];
-  __shared__ unsigned s_need, s_bin, s_done, s_out;
-  const int plane = blockIdx.x;
-  const K128* c = cand + (size_t)plane * cap;
+__global__ void __launch_bounds__(256) k_sel_hist(const K128* __restrict__ cand, const unsigned* __restrict__ cnt,
+                                                  size_t cap, unsigned* __restrict__ ghist) {
+  __shared__ unsigned h[kSelBins];
+  const int plane = blockIdx.y;
   const int n = (int)min((size_t)cnt[plane], cap);
-  K128* out = sorted + (size_t)plane * K;
-  K128* scratch = tmp + (size_t)plane * K;
-  int m = n;
-  if (n > K) {
-    K128 pref{0ull, 0ull};
-    int bits = 0;
-    if (threadIdx.x == 0) { s_need = K; s_done = 0; }
+  for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const K128* c = cand + (size_t)plane * cap;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&h[sel_bin(c[i])], 1u);
+  __syncthreads();
+  unsigned* g = ghist + (size_t)plane * kSelBins;
+  for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
+    if (h[i]) atomicAdd(&g[i], h[i]);
+}
+
+// per plane: threshold bin b* (the bin holding the K-th largest score; 0 when
+// there are at most K candidates), bucket offsets of the bins >= b* (keys in
+// higher bins first) and the kept-set size
+__global__ void __launch_bounds__(1024) k_sel_thresh(const unsigned* __restrict__ cnt, size_t cap, int K,
+                                                     const unsigned* __restrict__ ghist, int* __restrict__ bstar,
+                                                     unsigned* __restrict__ bbase, unsigned* __restrict__ setn) {
+  __shared__ unsigned part[1024];
+  __shared__ int s_b;
+  const int plane = blockIdx.x;
+  const int n = (int)min((size_t)cnt[plane], cap);
+  const unsigned* g = ghist + (size_t)plane * kSelBins;
+  unsigned* bb = bbase + (size_t)plane * kSelBins;
+  constexpr int per = kSelBins / 1024;          // bins per thread, thread 0 = highest bins
+  const int b0 = kSelBins - per * (threadIdx.x + 1);
+  unsigned s = 0;
+  for (int i = 0; i < per; ++i) s += g[b0 + i];
+  part[threadIdx.x] = s;
+  if (threadIdx.x == 0) s_b = 0;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {    // inclusive scan from the top bins down
+    const unsigned add = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
     __syncthreads();
-    for (int d = 0; d < 16; ++d) {
-      for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const K128 k = c[i];
-        bool match;
-        if (bits == 0) match = true;
-        else {
-          K128 a = k;
-          if (bits <= 64) {
-            const unsigned long long msk = ~0ull << (64 - bits);
-            match = (a.hi & msk) == (pref.hi & msk);
-          } else {
-            const unsigned long long msk = ~0ull << (128 - bits);
-            match = a.hi == pref.hi && (a.lo & msk) == (pref.lo & msk);
-          }
-        }
-        if (match) atomicAdd(&h[digit_of(k, d)], 1u);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned cum = 0, need = s_need;
-        for (int b = 0; b < 256; ++b) {
-          if (cum + h[b] >= need) {
-            s_bin = b;
-            s_need = need - cum;
-            s_done = (h[b] == need - cum) ? 1u : 0u;
-            break;
-          }
-          cum += h[b];
-        }
-      }
-      __syncthreads();
-      const unsigned long long bv = s_bin;
-      if (d < 8) pref.hi |= bv << (56 - 8 * d);
-      else pref.lo |= bv << (56 - 8 * (d - 8));
-      bits += 8;
-      const bool done = s_done;
-      __syncthreads();
-      if (done) break;
-    }
-    if (threadIdx.x == 0) s_out = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const K128 k = c[i];
-      if (top_bits_le(k, pref, bits)) {
-        const unsigned slot = atomicAdd(&s_out, 1u);
-        if (slot < (unsigned)K) out[slot] = k;
-      }
-    }
-    __syncthreads();
-    m = min((int)s_out, K);
-  } else {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = c[i];
+    part[threadIdx.x] += add;
     __syncthreads();
   }
-  sort_keys_block(out, scratch, m, s_keys);
-  if (threadIdx.x == 0) nsel[plane] = m;
+  const unsigned above = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+  unsigned run = above;
+  for (int i = per - 1; i >= 0; --i) {          // highest bin of this thread first
+    bb[b0 + i] = run;
+    const unsigned nxt = run + g[b0 + i];
+    if (n > K && run < (unsigned)K && nxt >= (unsigned)K) s_b = b0 + i;
+    run = nxt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int bs = s_b;
+    bstar[plane] = bs;
+    setn[plane] = n <= K ? (unsigned)n : bb[bs] + g[bs];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sel_scatter(const K128* __restrict__ cand, const unsigned* __restrict__ cnt,
+                                                     size_t cap, const int* __restrict__ bstar,
+                                                     const unsigned* __restrict__ bbase, unsigned* __restrict__ bfill,
+                                                     K128* __restrict__ set) {
+  const int plane = blockIdx.y;
+  const int n = (int)min((size_t)cnt[plane], cap);
+  const int bs = bstar[plane];
+  const K128* c = cand + (size_t)plane * cap;
+  const unsigned* bb = bbase + (size_t)plane * kSelBins;
+  unsigned* bf = bfill + (size_t)plane * kSelBins;
+  K128* o = set + (size_t)plane * cap;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const K128 k = c[i];
+    const int bin = sel_bin(k);
+    if (bin >= bs) o[bb[bin] + atomicAdd(&bf[bin], 1u)] = k;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sel_rank(const K128* __restrict__ set, const unsigned* __restrict__ setn,
+                                                  const unsigned* __restrict__ bbase,
+                                                  const unsigned* __restrict__ ghist, size_t cap, int K,
+                                                  K128* __restrict__ sorted, unsigned* __restrict__ nsel) {
+  const int plane = blockIdx.y;
+  const int n = (int)min((size_t)setn[plane], cap);
+  const K128* s = set + (size_t)plane * cap;
+  const unsigned* bb = bbase + (size_t)plane * kSelBins;
+  const unsigned* g = ghist + (size_t)plane * kSelBins;
+  if (blockIdx.x == 0 && threadIdx.x == 0) nsel[plane] = (unsigned)min(n, K);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const K128 mine = s[i];
+    const int bin = sel_bin(mine);
+    const unsigned lo = bb[bin], hi = lo + g[bin];
+    if (lo >= (unsigned)K) continue;               // the whole bucket lies past K
+    unsigned pos = lo;
+    for (unsigned j = lo; j < hi; ++j) pos += k_less(s[j], mine) ? 1u : 0u;
+    if (pos < (unsigned)K) sorted[(size_t)plane * K + pos] = mine;
+  }
 }
 
 R2_DEV void write_kp(const K128& k, int idx, const DetectArgs& a, int b) {
@@ -475,7 +494,8 @@ __global__ void __launch_bounds__(1024) k_merge_suppress(const K128* __restrict_
 struct DetectPlan {
   int P, K, tsz;
   size_t cap;
-  size_t off_mm, off_cnt, off_nsel, off_cand, off_sorted, off_tmp, off_merged, off_hk, off_hv, off_nbr, total;
+  size_t off_mm, off_cnt, off_nsel, off_cand, off_sorted, off_tmp, off_merged, off_hk, off_hv, off_nbr;
+  size_t off_ghist, off_bstar, off_setcnt, off_set, off_bbase, off_bfill, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -500,6 +520,12 @@ DetectPlan plan_detect(int B, int H, int W, int K) {
   p.off_hk = take((size_t)B * p.tsz * sizeof(int));
   p.off_hv = take((size_t)B * p.tsz * sizeof(int));
   p.off_nbr = take((size_t)B * 2 * p.K * kMaxNbr * sizeof(int));
+  p.off_ghist = take((size_t)p.P * kSelBins * sizeof(unsigned));
+  p.off_bstar = take((size_t)p.P * sizeof(int));
+  p.off_setcnt = take((size_t)p.P * sizeof(unsigned));
+  p.off_set = take((size_t)p.P * p.cap * sizeof(K128));
+  p.off_bbase = take((size_t)p.P * kSelBins * sizeof(unsigned));
+  p.off_bfill = take((size_t)p.P * kSelBins * sizeof(unsigned));
   p.total = off;
   return p;
 }
@@ -535,9 +561,22 @@ int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, siz
     dim3 grid((a.W + kTile - 1) / kTile, (a.H + kTile - 1) / kTile, planes);
     k_fast_nms<T><<<grid, 256, 0, st>>>(mins, maxs, a.H, a.W, mm, a.threshold, a.margin, nm, cand, cnt, p.cap);
   }
-  const size_t sort_smem = kSortChunk * sizeof(K128);
-  cudaFuncSetAttribute(k_select_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
-  k_select_sort<<<planes, 1024, sort_smem, st>>>(cand, cnt, p.cap, a.max_points, sorted, tmp, nsel);
+  {
+    auto* ghist = reinterpret_cast<unsigned*>(w + p.off_ghist);
+    auto* bstar = reinterpret_cast<int*>(w + p.off_bstar);
+    auto* setn = reinterpret_cast<unsigned*>(w + p.off_setcnt);
+    auto* set = reinterpret_cast<K128*>(w + p.off_set);
+    auto* bbase = reinterpret_cast<unsigned*>(w + p.off_bbase);
+    auto* bfill = reinterpret_cast<unsigned*>(w + p.off_bfill);
+    (void)tmp;
+    cudaMemsetAsync(ghist, 0, (size_t)planes * kSelBins * sizeof(unsigned), st);
+    cudaMemsetAsync(bfill, 0, (size_t)planes * kSelBins * sizeof(unsigned), st);
+    k_sel_hist<<<dim3(kSelCtas, planes), 256, 0, st>>>(cand, cnt, p.cap, ghist);
+    k_sel_thresh<<<planes, 1024, 0, st>>>(cnt, p.cap, a.max_points, ghist, bstar, bbase, setn);
+    k_sel_scatter<<<dim3(kSelCtas, planes), 256, 0, st>>>(cand, cnt, p.cap, bstar, bbase, bfill, set);
+    const int rank_ctas = (int)min((size_t)64, ((size_t)2 * a.max_points + 255) / 256);
+    k_sel_rank<<<dim3(rank_ctas, planes), 256, 0, st>>>(set, setn, bbase, ghist, p.cap, a.max_points, sorted, nsel);
+  }
   if (a.single_map) {
     k_emit_single<<<a.B, 1024, 0, st>>>(sorted, nsel, a);
   } else {
