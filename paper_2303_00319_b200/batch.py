@@ -81,8 +81,8 @@ class BatchPipeline:
         self.run_fields()
         self.run_features()
 
-    # our kernels per step: fields 7 + detect 5 + describe 3 + match 4
-    KERNELS_PER_STEP = 19
+    # our kernels per step: fields 7 + detect 8 + describe 3 + match 7
+    KERNELS_PER_STEP = 25
 
     # ---- graphs ------------------------------------------------------------
     def capture(self):

@@ -21,7 +21,8 @@
 //   k_match_combine per target keypoint: best over its variants and over the
 //                 column splits (exact 128-bit comparison), then the exact
 //                 float64 distance of the winner (ref: matcher.py:137-141)
-//   k_match_sort  per pair: order by (dist, ref, tgt) (ref: matcher.py:143-146)
+//   k_msort_*     per pair: order by (dist, ref, tgt) (ref: matcher.py:143-146),
+//                 bucket sort on the distance bits, multi-CTA
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -551,21 +552,95 @@ __global__ void __launch_bounds__(256) k_match_combine(MatchArgs a, IdxWs w, con
   }
 }
 
-__global__ void __launch_bounds__(1024) k_match_sort(MatchArgs a, IdxWs w, K128* __restrict__ keys,
-                                                     K128* __restrict__ tmp) {
-  extern __shared__ K128 s_keys[];
-  const int pair = blockIdx.x;
+// (dist, ref, tgt) order by bucket sort: a monotone linear bin of the
+// float64 distance (in [0, 2]), a histogram, the
+// bucket offsets, a scatter, and each key's rank among its own bucket's keys
+// (keys are unique: tgt ids are).  All passes are multi-CTA per pair.
+constexpr int kMsBins = 4096;
+constexpr int kMsCtas = 16;
+
+R2_DEV int ms_bin(const K128& k) {
+  // distances of unit vectors lie in [0, 2]: linear bins, monotone in the key
+  const double d = __longlong_as_double((long long)k.hi);
+  const int v = (int)(d * (kMsBins / 2));
+  return v < 0 ? 0 : (v >= kMsBins ? kMsBins - 1 : v);
+}
+
+__global__ void __launch_bounds__(256) k_msort_hist(IdxWs w, const K128* __restrict__ keys, int cap,
+                                                    unsigned* __restrict__ hist) {
+  __shared__ unsigned h[kMsBins];
+  const int pair = blockIdx.y;
   const int ng = w.ng[pair];
-  K128* k = keys + (size_t)pair * a.cap;
-  sort_keys_block(k, tmp + (size_t)pair * a.cap, ng, s_keys);
-  const int n = min(ng, a.tgt_kp_cap);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const size_t o = (size_t)pair * a.tgt_kp_cap + i;
-    a.out_dist[o] = __longlong_as_double((long long)k[i].hi);
-    a.out_ref[o] = (int32_t)(k[i].lo >> 32);
-    a.out_tgt[o] = (int32_t)(k[i].lo & 0xffffffffull);
+  for (int i = threadIdx.x; i < kMsBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const K128* k = keys + (size_t)pair * cap;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) atomicAdd(&h[ms_bin(k[i])], 1u);
+  __syncthreads();
+  unsigned* g = hist + (size_t)pair * kMsBins;
+  for (int i = threadIdx.x; i < kMsBins; i += blockDim.x)
+    if (h[i]) atomicAdd(&g[i], h[i]);
+}
+
+__global__ void __launch_bounds__(1024) k_msort_scan(const unsigned* __restrict__ hist, unsigned* __restrict__ base) {
+  __shared__ unsigned part[1024];
+  const int pair = blockIdx.x;
+  const unsigned* g = hist + (size_t)pair * kMsBins;
+  unsigned* bb = base + (size_t)pair * kMsBins;
+  constexpr int per = kMsBins / 1024;
+  const int b0 = per * threadIdx.x;
+  unsigned s = 0;
+  for (int i = 0; i < per; ++i) s += g[b0 + i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const unsigned add = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += add;
+    __syncthreads();
   }
-  if (threadIdx.x == 0) a.out_count[pair] = n;
+  unsigned run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+  for (int i = 0; i < per; ++i) { bb[b0 + i] = run; run += g[b0 + i]; }
+}
+
+__global__ void __launch_bounds__(256) k_msort_scatter(IdxWs w, const K128* __restrict__ keys, int cap,
+                                                       const unsigned* __restrict__ base, unsigned* __restrict__ fill,
+                                                       K128* __restrict__ out) {
+  const int pair = blockIdx.y;
+  const int ng = w.ng[pair];
+  const K128* k = keys + (size_t)pair * cap;
+  const unsigned* bb = base + (size_t)pair * kMsBins;
+  unsigned* f = fill + (size_t)pair * kMsBins;
+  K128* o = out + (size_t)pair * cap;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
+    const K128 key = k[i];
+    const int bin = ms_bin(key);
+    o[bb[bin] + atomicAdd(&f[bin], 1u)] = key;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_msort_rank(MatchArgs a, IdxWs w, const K128* __restrict__ bucketed,
+                                                    const unsigned* __restrict__ hist,
+                                                    const unsigned* __restrict__ base) {
+  const int pair = blockIdx.y;
+  const int ng = w.ng[pair];
+  const K128* s = bucketed + (size_t)pair * a.cap;
+  const unsigned* g = hist + (size_t)pair * kMsBins;
+  const unsigned* bb = base + (size_t)pair * kMsBins;
+  const int n = min(ng, a.tgt_kp_cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.out_count[pair] = n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
+    const K128 mine = s[i];
+    const int bin = ms_bin(mine);
+    const unsigned lo = bb[bin], hi = lo + g[bin];
+    unsigned pos = lo;
+    for (unsigned j = lo; j < hi; ++j) pos += k_less(s[j], mine) ? 1u : 0u;
+    if (pos < (unsigned)n) {
+      const size_t o = (size_t)pair * a.tgt_kp_cap + pos;
+      a.out_dist[o] = __longlong_as_double((long long)mine.hi);
+      a.out_ref[o] = (int32_t)(mine.lo >> 32);
+      a.out_tgt[o] = (int32_t)(mine.lo & 0xffffffffull);
+    }
+  }
 }
 
 // ------------------------------------------------ generic float64 vectors
@@ -678,7 +753,7 @@ __global__ void __launch_bounds__(1024) k_vec_sort(K128* __restrict__ keys, K128
 constexpr int kMaxSplits = 8;
 
 struct MatchWs {
-  size_t off_part, off_gstart, off_ng, off_rstart, off_rend, off_keys, off_tmp, total;
+  size_t off_part, off_gstart, off_ng, off_rstart, off_rend, off_keys, off_tmp, off_mhist, off_mbase, off_mfill, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -694,6 +769,9 @@ MatchWs plan_match(int n_pairs, int cap) {
   p.off_rend = take((size_t)n_pairs * cap * sizeof(int));
   p.off_keys = take((size_t)n_pairs * cap * sizeof(K128));
   p.off_tmp = take((size_t)n_pairs * cap * sizeof(K128));
+  p.off_mhist = take((size_t)n_pairs * kMsBins * sizeof(unsigned));
+  p.off_mbase = take((size_t)n_pairs * kMsBins * sizeof(unsigned));
+  p.off_mfill = take((size_t)n_pairs * kMsBins * sizeof(unsigned));
   p.total = off;
   return p;
 }
@@ -763,9 +841,15 @@ void finish_launch(const MatchArgs& a, const Part* part, int n_parts, PartLayout
     dim3 g2((a.cap + 7) / 8, a.n_pairs);
     k_match_combine<<<g2, 256, 0, st>>>(a, iw, part, n_parts, lay, keys);
   }
-  const size_t sort_smem = kSortChunk * sizeof(K128);
-  cudaFuncSetAttribute(k_match_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
-  k_match_sort<<<a.n_pairs, 1024, sort_smem, st>>>(a, iw, keys, tmp);
+  auto* mh = reinterpret_cast<unsigned*>(w + p.off_mhist);
+  auto* mb = reinterpret_cast<unsigned*>(w + p.off_mbase);
+  auto* mf = reinterpret_cast<unsigned*>(w + p.off_mfill);
+  cudaMemsetAsync(mh, 0, (size_t)a.n_pairs * kMsBins * sizeof(unsigned), st);
+  cudaMemsetAsync(mf, 0, (size_t)a.n_pairs * kMsBins * sizeof(unsigned), st);
+  k_msort_hist<<<dim3(kMsCtas, a.n_pairs), 256, 0, st>>>(iw, keys, a.cap, mh);
+  k_msort_scan<<<a.n_pairs, 1024, 0, st>>>(mh, mb);
+  k_msort_scatter<<<dim3(kMsCtas, a.n_pairs), 256, 0, st>>>(iw, keys, a.cap, mb, mf, tmp);
+  k_msort_rank<<<dim3(kMsCtas, a.n_pairs), 256, 0, st>>>(a, iw, tmp, mh, mb);
 }
 
 }  // namespace

@@ -13,7 +13,8 @@ for (i, k), v in sorted(agg.items()):
     tot += t
     if t > minus * 1e3:
         inst = v.get("sm__inst_executed.sum", 0)
-        print(f"{k[:30]:30s} {t / 1e3:9.1f} us  inst {inst / 1e6:8.1f} M  warps {v.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):5.1f}%"
+        name = k.split("(")[0].split("::")[-1] if "::" in k else k
+        print(f"{name[:30]:30s} {t / 1e3:9.1f} us  inst {inst / 1e6:8.1f} M  warps {v.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):5.1f}%"
               f"  IPC/SM {inst / (t * 1.965) / 148:5.2f}  rd {v.get('dram__bytes_read.sum', 0) / 1e9:6.2f} GB"
               f"  wr {v.get('dram__bytes_write.sum', 0) / 1e9:6.2f} GB")
 print(f"total {tot / 1e6:.3f} ms")
