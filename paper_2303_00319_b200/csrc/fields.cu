@@ -35,6 +35,7 @@ constexpr int kThreads = 256;
 template <int G>
 struct ColsCfg { static constexpr int T = G == 0 ? 256 : (G >= 64 ? 2 * G : 128); };
 constexpr int kHistBins = 4096;   // float bits >> 19 of a non-negative float
+constexpr int kAmpRows = 4;       // row groups per k_rows_amp0 CTA
 constexpr int kMaxS = 8;
 constexpr int kMaxO = 16;
 constexpr float kPi = 3.14159265358979f;
@@ -351,6 +352,11 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
 // Scale-0 responses of orientation blockIdx.y for a block of rows: written
 // out (for K3b) with |response| and a 4096-bin histogram of its float bits
 // (radix-select level 1 of the median).
+R2_DEV float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 template <int G>
 __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict__ Q, float2* __restrict__ R0,
                                                         float* __restrict__ amp0, unsigned* __restrict__ hist,
@@ -369,8 +375,8 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
     __syncthreads();
     const int g = threadIdx.x / G, t = threadIdx.x % G;
     float2* buf = sm + g * PL;
-    const int y = blockIdx.x * NG + g;
-    if (y < H) {
+    // kAmpRows row groups per CTA amortise the histogram zero / flush
+    for (int y = blockIdx.x * NG * kAmpRows + g; y < min(H, (blockIdx.x + 1) * NG * kAmpRows); y += NG) {
       float2 v[32];
 #pragma unroll
       for (int m = 0; m < 32; ++m) v[m] = cconj(Qp[tq(y, t + G * m, W)]);
@@ -380,11 +386,13 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const float2 z = cconj(v[m]);
-        const float a = sqrtf(z.x * z.x + z.y * z.y);
+        // MUFU sqrt: the median only needs amplitudes consistent with themselves
+        const float a = sqrt_approx(fmaf(z.x, z.x, z.y * z.y));
         Rp[(size_t)y * W + t + G * m] = z;
         A[(size_t)y * W + t + G * m] = a;
         atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
       }
+      if constexpr (G <= 32) sw(); else sn();   // buf is rewritten by the next row
     }
   } else {
     const int PL = padded_len(W);
@@ -398,7 +406,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
     fft_generic(buf, scr, W, c.plan_w, c.tw_w, threadIdx.x, blockDim.x);
     for (int x = threadIdx.x; x < W; x += blockDim.x) {
       const float2 z = cconj(buf[pad32(x)]);
-      const float a = sqrtf(z.x * z.x + z.y * z.y);
+      const float a = sqrt_approx(fmaf(z.x, z.x, z.y * z.y));
       Rp[(size_t)y * W + x] = z;
       A[(size_t)y * W + x] = a;
       atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
@@ -587,11 +595,6 @@ struct PcShape {
   static constexpr int PIX = G == 0 ? 16 : (G == 128 ? 16 : (G >= 4 ? G / 4 : 1));
 };
 
-R2_DEV float sqrt_approx(float x) {
-  float y;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 R2_DEV float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -931,7 +934,7 @@ static cudaError_t launch_amp0(const float2* Q, float2* R0, float* amp0, unsigne
   if constexpr (G > 0) {
     const int NG = kThreads / G;
     smem = (size_t)NG * padded_len(32 * G) * sizeof(float2) + kHistBins * sizeof(unsigned);
-    grid = dim3((c.H + NG - 1) / NG, c.O, c.B);
+    grid = dim3((c.H + NG * kAmpRows - 1) / (NG * kAmpRows), c.O, c.B);
   } else {
     smem = (size_t)2 * padded_len(c.W) * sizeof(float2) + kHistBins * sizeof(unsigned);
     grid = dim3(c.H, c.O, c.B);

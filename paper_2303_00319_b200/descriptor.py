@@ -15,9 +15,21 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import ParameterError
+from .errors import FormatError, ParameterError
 
 MODE_CODES = {"plain": 0, "ring": 1, "rift2": 2}
+_MODE_NAMES = {v: k for k, v in MODE_CODES.items()}
+
+# "RIF2" container (ref: descriptor.py:26-32, 255-294): an 11-byte header
+# (magic, version u8, n_orient u8, grid u8, count u32 LE) and fixed-size
+# records (keypoint id u32, variant u8, mode code u8, float32 LE vector),
+# read and written here as one packed numpy record array
+_MAGIC, _VERSION = b"RIF2", 1
+_HEAD = np.dtype([("magic", "S4"), ("version", "u1"), ("n_orient", "u1"), ("grid", "u1"), ("count", "<u4")])
+
+
+def _record_dtype(dim: int) -> np.dtype:
+    return np.dtype([("kp", "<u4"), ("variant", "u1"), ("mode", "u1"), ("vec", "<f4", (dim,))])
 
 
 @dataclass(frozen=True)
@@ -104,3 +116,66 @@ def describe_ring(mim, keypoints, patch_size: int = 96, grid: int = 6, weighted:
 def describe_plain(mim, keypoints, patch_size: int = 96, grid: int = 6, weighted: bool = False) -> DescriptorSet:
     """ref: descriptor.py:239-254."""
     return _run(mim, keypoints, patch_size, grid, 0.8, False, weighted, "plain")
+
+
+def _write_records(path, n_orient: int, grid: int, kp, variant, mode_code, vec32) -> None:
+    dim = grid * grid * n_orient
+    rec = np.empty(len(kp), dtype=_record_dtype(dim))
+    rec["kp"], rec["variant"], rec["mode"], rec["vec"] = kp, variant, mode_code, vec32
+    head = np.array([(_MAGIC, _VERSION, n_orient, grid, len(kp))], dtype=_HEAD)
+    with open(path, "wb") as fh:
+        fh.write(head.tobytes())
+        fh.write(rec.tobytes())
+
+
+def write_descriptors(path, descriptors, n_orient: int = 6, grid: int = 6) -> None:
+    """ref: descriptor.py:255-268 (same bytes)."""
+    dim = grid * grid * n_orient
+    descriptors = list(descriptors)
+    for d in descriptors:
+        if np.shape(d.vector) != (dim,):
+            raise ParameterError(f"descriptor length {np.shape(d.vector)} does not match {dim}")
+    vec = np.array([d.vector for d in descriptors], dtype=np.float64).reshape(len(descriptors), dim)
+    _write_records(path, n_orient, grid, [d.keypoint_id for d in descriptors], [d.variant for d in descriptors],
+                   [MODE_CODES[d.mode] for d in descriptors], vec.astype("<f4"))
+
+
+def write_descriptor_counts(path, counts, kp, variant, mode: str = "rift2", n_orient: int = 6,
+                            grid: int = 6) -> None:
+    """The same container straight from the batched tensors of one image
+    (`BatchPipeline.d` / `engine.describe` rows, counts (n, >= dim)): the
+    float64 unit vector counts / ||counts|| is formed on the device, rounded
+    to float32 as write_descriptors does, and written without building
+    Descriptor objects."""
+    import torch
+    dim = grid * grid * n_orient
+    c = counts[:, :dim].to(torch.float64)
+    vec = (c / torch.sqrt((c * c).sum(dim=1, keepdim=True))).to(torch.float32).cpu().numpy()
+    as_np = (lambda t: t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t))
+    _write_records(path, n_orient, grid, as_np(kp), as_np(variant), MODE_CODES[mode], vec)
+
+
+def read_descriptors(path) -> list:
+    """ref: descriptor.py:271-294 (FormatError on a short header, bad magic,
+    unknown version or mode code, and truncated records)."""
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    if len(raw) < _HEAD.itemsize:
+        raise FormatError("descriptor file too short for header")
+    head = np.frombuffer(raw, dtype=_HEAD, count=1)[0]
+    if head["magic"] != _MAGIC:
+        raise FormatError(f"bad magic {bytes(head['magic'])!r}")
+    if head["version"] != _VERSION:
+        raise FormatError(f"unsupported version {int(head['version'])}")
+    dim = int(head["grid"]) * int(head["grid"]) * int(head["n_orient"])
+    rdt = _record_dtype(dim)
+    count = int(head["count"])
+    if len(raw) - _HEAD.itemsize < count * rdt.itemsize:
+        raise FormatError("descriptor file truncated")
+    rec = np.frombuffer(raw, dtype=rdt, count=count, offset=_HEAD.itemsize)
+    bad = ~np.isin(rec["mode"], list(_MODE_NAMES))
+    if bad.any():
+        raise FormatError(f"unknown mode code {int(rec['mode'][bad][0])}")
+    vec = rec["vec"].astype(np.float64)
+    return [Descriptor(vec[i], int(rec["kp"][i]), int(rec["variant"][i]), _MODE_NAMES[int(rec["mode"][i])])
+            for i in range(count)]

@@ -165,8 +165,28 @@ def case_matcher():
     save("matcher.npz", **out)
 
 
+def case_container():
+    """The RIF2 descriptor container bytes written by the reference
+    (ref: descriptor.py:255-268): seeded unit vectors over all three modes,
+    plus an empty file."""
+    from rift2.descriptor import write_descriptors
+    rng = np.random.default_rng(21)
+    descs = []
+    for i in range(9):
+        v = rng.random(216)
+        descs.append(rift2.Descriptor(v / np.linalg.norm(v), int(rng.integers(0, 2**32 - 1)), (i % 6) + 1,
+                                      ("plain", "ring", "rift2")[i % 3]))
+    write_descriptors(os.path.join(HERE, "container.rif2"), descs)
+    write_descriptors(os.path.join(HERE, "container_empty.rif2"), [])
+    save("container.npz", vec=np.array([d.vector for d in descs]),
+         kp=np.array([d.keypoint_id for d in descs], np.uint32),
+         variant=np.array([d.variant for d in descs], np.int8),
+         mode=np.array([("plain", "ring", "rift2").index(d.mode) for d in descs], np.int8))
+
+
+CASES = dict(fields_small=case_fields_small, detector=case_detector, matcher=case_matcher, pair=case_pair,
+             container=case_container)
+
 if __name__ == "__main__":
-    case_fields_small()
-    case_detector()
-    case_matcher()
-    case_pair()
+    for name in (sys.argv[1:] or CASES):
+        CASES[name]()

@@ -172,3 +172,25 @@ def test_pipelined_step_equals_step(r2):
     pipe.pipelined_step(0)          # features of B (filter bank of A again)
     torch.cuda.synchronize()
     assert all(torch.equal(want[1][k], pipe.m[k]) for k in want[1])
+
+
+def test_container_from_device_counts(r2, pair512, tmp_path):
+    """write_descriptor_counts on the engine's device rows writes the same
+    bytes as write_descriptors on the dataclass descriptors (ref:
+    descriptor.py:255-268), and read_descriptors returns them."""
+    from paper_2303_00319_b200 import engine
+    cfg = r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=600)
+    pc, mim = r2.compute_fields(pair512[0], cfg)
+    kps = r2.detect_keypoints(pc, cfg.fast_threshold, cfg.max_keypoints, cfg.patch_size)
+    ds = r2.describe_rift2(mim, kps)
+    a, b = tmp_path / "a.rif2", tmp_path / "b.rif2"
+    r2.write_descriptors(a, ds.descriptors)
+    m = torch.from_numpy(mim.indices.astype(np.uint8)).cuda()[None]
+    x = torch.tensor([[k.x for k in kps]], dtype=torch.int32).cuda()
+    y = torch.tensor([[k.y for k in kps]], dtype=torch.int32).cuda()
+    out = engine.describe(m, x, y, torch.tensor([len(kps)], dtype=torch.int32).cuda(), 6)
+    n = int(out["count"][0])
+    r2.write_descriptor_counts(b, out["counts"][0, :n], out["kp"][0, :n], out["variant"][0, :n], "rift2")
+    assert a.read_bytes() == b.read_bytes()
+    back = r2.read_descriptors(b)
+    assert [(d.keypoint_id, d.variant) for d in back] == [(d.keypoint_id, d.variant) for d in ds]

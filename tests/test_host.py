@@ -113,3 +113,59 @@ def test_product_package_never_imports_oracle():
     for fn in os.listdir(pkg):
         if fn.endswith(".py"):
             assert "oracle" not in open(os.path.join(pkg, fn)).read().replace("oracle/", ""), fn
+
+
+# ---- RIF2 descriptor container (ref: descriptor.py:26-32, 255-294) ----------
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def _golden_descs():
+    from paper_2303_00319_b200 import Descriptor
+    g = np.load(os.path.join(GOLDEN, "container.npz"))
+    modes = ("plain", "ring", "rift2")
+    return [Descriptor(v, int(k), int(var), modes[m]) for v, k, var, m in zip(g["vec"], g["kp"], g["variant"], g["mode"])]
+
+
+def test_container_bytes_equal_reference(tmp_path):
+    from paper_2303_00319_b200 import write_descriptors
+    p = tmp_path / "d.rif2"
+    write_descriptors(p, _golden_descs())
+    assert p.read_bytes() == open(os.path.join(GOLDEN, "container.rif2"), "rb").read()
+    write_descriptors(p, [])
+    assert p.read_bytes() == open(os.path.join(GOLDEN, "container_empty.rif2"), "rb").read()
+
+
+def test_container_read_reference_file():
+    from paper_2303_00319_b200 import read_descriptors
+    want = _golden_descs()
+    got = read_descriptors(os.path.join(GOLDEN, "container.rif2"))
+    assert len(got) == len(want)
+    for a, b in zip(want, got):
+        assert (a.keypoint_id, a.variant, a.mode) == (b.keypoint_id, b.variant, b.mode)
+        assert np.array_equal(a.vector.astype(np.float32).astype(np.float64), b.vector)
+    assert read_descriptors(os.path.join(GOLDEN, "container_empty.rif2")) == []
+
+
+def test_container_errors(tmp_path):
+    from paper_2303_00319_b200 import Descriptor, FormatError, ParameterError, read_descriptors, write_descriptors
+    p = tmp_path / "d.rif2"
+    p.write_bytes(b"RIF2\x01")
+    with pytest.raises(FormatError):
+        read_descriptors(p)                                  # short header
+    p.write_bytes(b"NOPE" + bytes(7))
+    with pytest.raises(FormatError):
+        read_descriptors(p)                                  # bad magic
+    p.write_bytes(b"RIF2\x02\x06\x06" + bytes(4))
+    with pytest.raises(FormatError):
+        read_descriptors(p)                                  # version
+    v = np.full(216, 1 / np.sqrt(216))
+    write_descriptors(p, [Descriptor(v, 0, 1, "plain")])
+    raw = p.read_bytes()
+    p.write_bytes(raw[:-8])
+    with pytest.raises(FormatError):
+        read_descriptors(p)                                  # truncated record
+    p.write_bytes(raw[:16] + b"\x07" + raw[17:])
+    with pytest.raises(FormatError):
+        read_descriptors(p)                                  # unknown mode code
+    with pytest.raises(ParameterError):
+        write_descriptors(p, [Descriptor(v[:100], 0, 1, "plain")])
