@@ -194,6 +194,24 @@ int32_t rift2_match_vectors(const double* ref_vec, const int32_t* ref_kp, int32_
                             double* out_dist, int32_t* out_count, void* workspace, size_t workspace_bytes,
                             void* stream);
 
+/* ---- ground-truth evaluation of match sets ----------
+ * Replaces ref: pkg/src/rift2/evalbench.py:63-96 (evaluate) for a batch of
+ * pairs laid out like rift2_detect / rift2_match outputs: keypoints
+ * [images][kp_stride] with kp_count[images]; pair p compares image
+ * ref_img[p] against tgt_img[p] with match rows match_ref / match_tgt
+ * [n_pairs][match_stride] (match_count[p] live rows) and the 2x3 transform
+ * gt[p] = (R00, R01, R10, R11, t0, t1) mapping reference to target points.
+ * Per pair: number of matches with residual < residual_threshold, RMSE over
+ * them (clamped to rmse_cap, +inf with none), success = n_correct >=
+ * success_min_matches, and out_bad = 1 if a match index does not resolve
+ * (the reference raises IntegrityError there). */
+int32_t rift2_evaluate(const int32_t* kp_x, const int32_t* kp_y, const int32_t* kp_count, int32_t kp_stride,
+                       const int32_t* ref_img, const int32_t* tgt_img, const int32_t* match_ref,
+                       const int32_t* match_tgt, const int32_t* match_count, int32_t match_stride, int32_t n_pairs,
+                       const double* gt, double residual_threshold, double rmse_cap, int32_t success_min_matches,
+                       int32_t* out_n_correct, double* out_rmse, uint8_t* out_success, int32_t* out_bad,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

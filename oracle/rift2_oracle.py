@@ -445,3 +445,24 @@ def match_nn(ref_vec, ref_kp, tgt_vec, tgt_kp, block: int = 1024):
                       float(np.sqrt((d * d).sum(-1).min()))))
     pairs.sort(key=lambda p: (p[2], p[0], p[1]))
     return pairs, len(R) * len(T)
+
+
+# ---------------------------------------------------------------- evaluation
+def evaluate(ref_xy, tgt_xy, pairs, gt_row, thr: float = 3.0, min_matches: int = 10, cap: float = 20.0):
+    """ref: evalbench.py:63-96 -- (n_correct, rmse, success).  gt_row =
+    (R00, R01, R10, R11, t0, t1); p' = p @ R^T + t (ref: imaging.py:71-74).
+    Raises IndexError where the reference raises IntegrityError."""
+    ref_xy = np.asarray(ref_xy, np.float64).reshape(-1, 2)
+    tgt_xy = np.asarray(tgt_xy, np.float64).reshape(-1, 2)
+    pairs = np.asarray(pairs, np.int64).reshape(-1, 2)
+    if len(pairs) and (pairs.min() < 0 or pairs[:, 0].max() >= len(ref_xy) or pairs[:, 1].max() >= len(tgt_xy)):
+        raise IndexError("match does not resolve to keypoints")
+    if not len(pairs):
+        return 0, math.inf, 0 >= min_matches
+    rot = np.array(gt_row[:4], np.float64).reshape(2, 2)
+    res = np.linalg.norm(ref_xy[pairs[:, 0]] @ rot.T + np.array(gt_row[4:], np.float64) - tgt_xy[pairs[:, 1]],
+                         axis=1)
+    ok = res < thr
+    n = int(ok.sum())
+    rmse = min(float(np.sqrt(np.mean(res[ok] ** 2))), cap) if n else math.inf
+    return n, rmse, n >= min_matches

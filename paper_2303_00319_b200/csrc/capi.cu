@@ -16,6 +16,7 @@
 #include "../../include/rift2_b200.h"
 #include "detect.h"
 #include "describe.h"
+#include "evaluate.h"
 #include "fields.h"
 #include "match.h"
 
@@ -321,6 +322,24 @@ int32_t rift2_match_vectors(const double* ref_vec, const int32_t* ref_kp, int32_
                                      out_dist, out_count, workspace, workspace_bytes,
                                      static_cast<cudaStream_t>(stream));
   return map_internal(rc, "rift2_match_vectors");
+}
+
+int32_t rift2_evaluate(const int32_t* kp_x, const int32_t* kp_y, const int32_t* kp_count, int32_t kp_stride,
+                       const int32_t* ref_img, const int32_t* tgt_img, const int32_t* match_ref,
+                       const int32_t* match_tgt, const int32_t* match_count, int32_t match_stride, int32_t n_pairs,
+                       const double* gt, double residual_threshold, double rmse_cap, int32_t success_min_matches,
+                       int32_t* out_n_correct, double* out_rmse, uint8_t* out_success, int32_t* out_bad,
+                       void* stream) {
+  if (n_pairs < 0 || kp_stride < 0 || match_stride < 0) return fail(RIFT2_BAD_ARGUMENT, "negative size");
+  if (n_pairs > 0 && (!kp_x || !kp_y || !kp_count || !ref_img || !tgt_img || !match_ref || !match_tgt ||
+                      !match_count || !gt || !out_n_correct || !out_rmse || !out_success || !out_bad))
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  if (!(residual_threshold > 0.0) || !(rmse_cap > 0.0))
+    return fail(RIFT2_BAD_ARGUMENT, "residual_threshold and rmse_cap must be > 0");
+  r2::EvalArgs a{kp_x, kp_y, kp_count, kp_stride, ref_img, tgt_img, match_ref, match_tgt, match_count,
+                 match_stride, n_pairs, gt, residual_threshold, rmse_cap, success_min_matches,
+                 out_n_correct, out_rmse, out_success, out_bad};
+  return map_internal(r2::evaluate_run(a, static_cast<cudaStream_t>(stream)), "rift2_evaluate");
 }
 
 }  // extern "C"

@@ -238,3 +238,28 @@ def match_finish(parts: torch.Tensor, desc: dict, dim: int, ref_block: torch.Ten
                                 _ptr(out["count"]), _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "rift2_match_finish")
     return out
+
+
+def evaluate(kp: dict, ref_img: torch.Tensor, tgt_img: torch.Tensor, m: dict, gt: torch.Tensor,
+             residual_threshold: float = 3.0, rmse_cap: float = 20.0, success_min_matches: int = 10, out=None):
+    """Ground-truth scoring of match sets (rift2_evaluate).  kp: detect()
+    dict (x, y, count; (images, K)); m: match() dict (ref, tgt, count);
+    ref_img / tgt_img int32 (P,); gt (P, 6) float64 CUDA = R00 R01 R10 R11 t0
+    t1.  -> dict(n_correct int32, rmse float64, success uint8, bad int32)."""
+    lib = _lib.load(require_gpu=True)
+    P = ref_img.numel()
+    dev = gt.device
+    if gt.dtype != torch.float64 or tuple(gt.shape) != (P, 6):
+        raise ParameterError("gt must be a (n_pairs, 6) float64 tensor")
+    if out is None:
+        out = dict(n_correct=torch.empty(P, dtype=torch.int32, device=dev),
+                   rmse=torch.empty(P, dtype=torch.float64, device=dev),
+                   success=torch.empty(P, dtype=torch.uint8, device=dev),
+                   bad=torch.empty(P, dtype=torch.int32, device=dev))
+    rc = lib.rift2_evaluate(_ptr(kp["x"]), _ptr(kp["y"]), _ptr(kp["count"]), kp["x"].shape[1], _ptr(ref_img),
+                            _ptr(tgt_img), _ptr(m["ref"]), _ptr(m["tgt"]), _ptr(m["count"]), m["ref"].shape[1], P,
+                            _ptr(gt.contiguous()), float(residual_threshold), float(rmse_cap),
+                            int(success_min_matches), _ptr(out["n_correct"]), _ptr(out["rmse"]),
+                            _ptr(out["success"]), _ptr(out["bad"]), _stream())
+    _lib.check(rc, "rift2_evaluate")
+    return out

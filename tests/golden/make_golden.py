@@ -184,8 +184,42 @@ def case_container():
          mode=np.array([("plain", "ring", "rift2").index(d.mode) for d in descs], np.int8))
 
 
+def case_evaluate():
+    """evalbench.evaluate (ref: evalbench.py:63-96) on seeded keypoints and
+    match sets under rigid transforms: matches built to land within, near
+    and beyond the residual threshold, several thresholds, empty sets."""
+    from rift2.detector import Keypoint
+    from rift2.evalbench import evaluate
+    from rift2.imaging import RigidTransform
+    rng = np.random.default_rng(31)
+    out = {}
+    for trial in range(6):
+        nr, nt = int(rng.integers(50, 400)), int(rng.integers(50, 400))
+        rxy = rng.integers(0, 1024, (nr, 2)).astype(np.float64)
+        gt = RigidTransform.rotation_about(float(rng.uniform(0, 2 * np.pi)), (512.0, 512.0))
+        gt = RigidTransform(gt.rotation, gt.translation + rng.uniform(-20, 20, 2))
+        txy = rng.integers(0, 1024, (nt, 2)).astype(np.float64)
+        n = 0 if trial == 5 else int(rng.integers(10, min(nr, nt)))
+        tsel = rng.permutation(nt)[:n]
+        rsel = rng.integers(0, nr, n)
+        # a third of the targets placed at the transformed reference point plus a jitter of 0-5 px
+        k = n // 3
+        jit = rng.uniform(0, 5, k)[:, None] * np.stack([np.cos(a := rng.uniform(0, 6.3, k)), np.sin(a)], 1)
+        txy[tsel[:k]] = np.rint(gt.apply(rxy[rsel[:k]]) + jit)
+        kr = [Keypoint(float(x), float(y), 1.0, "corner") for x, y in rxy]
+        kt = [Keypoint(float(x), float(y), 1.0, "corner") for x, y in txy]
+        ms = rift2.MatchSet(pairs=[(int(r), int(t), 0.0) for r, t in zip(rsel, tsel)])
+        row = np.array([*gt.rotation.ravel(), *gt.translation], np.float64)
+        out[f"t{trial}_ref_xy"], out[f"t{trial}_tgt_xy"], out[f"t{trial}_gt"] = rxy, txy, row
+        out[f"t{trial}_pairs"] = np.stack([rsel, tsel], 1).astype(np.int32).reshape(n, 2)
+        for j, thr in enumerate((3.0, 1.5, 0.5)):
+            rep = evaluate(ms, kr, kt, gt, residual_threshold=thr, success_min_matches=10, rmse_cap=2.0 if j == 2 else 20.0)
+            out[f"t{trial}_thr{j}"] = np.array([thr, rep.n_correct, rep.rmse, float(rep.success)], np.float64)
+    save("evaluate.npz", **out)
+
+
 CASES = dict(fields_small=case_fields_small, detector=case_detector, matcher=case_matcher, pair=case_pair,
-             container=case_container)
+             container=case_container, evaluate=case_evaluate)
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or CASES):

@@ -194,3 +194,45 @@ def test_container_from_device_counts(r2, pair512, tmp_path):
     assert a.read_bytes() == b.read_bytes()
     back = r2.read_descriptors(b)
     assert [(d.keypoint_id, d.variant) for d in back] == [(d.keypoint_id, d.variant) for d in ds]
+
+
+_G_EVAL = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "evaluate.npz"))
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_evaluate_vs_reference_golden(r2, trial):
+    """evaluate() (rift2_evaluate kernel) against the reference's
+    evalbench.evaluate outputs: n_correct and success exact, RMSE to 1e-12."""
+    g = _G_EVAL
+    kr = [r2.Keypoint(float(x), float(y), 1.0, "corner") for x, y in g[f"t{trial}_ref_xy"]]
+    kt = [r2.Keypoint(float(x), float(y), 1.0, "corner") for x, y in g[f"t{trial}_tgt_xy"]]
+    ms = r2.MatchSet(pairs=[(int(a), int(b), 0.0) for a, b in g[f"t{trial}_pairs"]])
+    row = g[f"t{trial}_gt"]
+    for j in range(3):
+        thr, n, rmse, succ = g[f"t{trial}_thr{j}"]
+        gt = np.array([[row[0], row[1], row[4]], [row[2], row[3], row[5]]])
+        rep = r2.evaluate(ms, kr, kt, gt, residual_threshold=thr, rmse_cap=2.0 if j == 2 else 20.0)
+        assert rep.n_correct == n and rep.success == bool(succ) and rep.n_matches_total == len(ms.pairs)
+        assert (np.isinf(rep.rmse) and np.isinf(rmse)) or abs(rep.rmse - rmse) <= 1e-12 * rmse
+    bad = r2.MatchSet(pairs=[(0, 0, 0.0), (len(kr), 0, 0.0)])
+    with pytest.raises(r2.IntegrityError):
+        r2.evaluate(bad, kr, kt, np.eye(2, 3))
+
+
+def test_evaluate_batch_vs_oracle(r2):
+    """evaluate_batch on a BatchPipeline step (1024^2 pairs from the BASELINE
+    generator) against the oracle's evaluate on the same keypoints/matches."""
+    from paper_2303_00319_b200 import synth
+    imgs, truths = synth.make_batch(2, 1024, seed0=40, looks=None)
+    pipe = r2.BatchPipeline(2, 1024, 1024, r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75))
+    pipe.load(imgs)
+    pipe.step()
+    ev = r2.evaluate_batch(pipe, truths)
+    torch.cuda.synchronize()
+    for p, (ri, ti, _) in enumerate(pipe.matches_host()):
+        kr, kt = pipe.keypoints_host(2 * p), pipe.keypoints_host(2 * p + 1)
+        n, rmse, succ = O.evaluate(np.stack([kr["x"], kr["y"]], 1), np.stack([kt["x"], kt["y"]], 1),
+                                   np.stack([ri, ti], 1), truths[p].matrix[:, :2].ravel().tolist()
+                                   + truths[p].matrix[:, 2].tolist())
+        assert int(ev["n_correct"][p]) == n > 100 and bool(ev["success"][p]) == succ
+        assert abs(float(ev["rmse"][p]) - rmse) <= 1e-12 * rmse

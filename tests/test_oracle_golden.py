@@ -126,3 +126,18 @@ def test_rotated_offsets_half_turn():
     base_dx, base_dy = O.rotated_offsets(96, 0.0)
     # ref tests/test_descriptor.py:27-31: the half turn samples the crop in reverse
     assert np.array_equal(dx, base_dx[::-1, ::-1]) and np.array_equal(dy, base_dy[::-1, ::-1])
+
+
+_G_EVAL = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "evaluate.npz"))
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_evaluate_golden(trial):
+    # ref: evalbench.py:63-96, golden from the reference's evaluate()
+    g = _G_EVAL
+    for j in range(3):
+        thr, n, rmse, succ = g[f"t{trial}_thr{j}"]
+        got = O.evaluate(g[f"t{trial}_ref_xy"], g[f"t{trial}_tgt_xy"], g[f"t{trial}_pairs"], g[f"t{trial}_gt"], thr,
+                         10, 2.0 if j == 2 else 20.0)
+        assert got[0] == n and got[2] == bool(succ)
+        assert (math.isinf(got[1]) and math.isinf(rmse)) or abs(got[1] - rmse) <= 1e-12 * rmse
