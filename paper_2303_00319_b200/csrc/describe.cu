@@ -41,7 +41,7 @@ namespace {
 constexpr int kT = 160;   // 5 warps: 144 counting threads for the 6x6 grid of 16-px cells
 
 struct GatherTables {
-  const short* soff;     // [O][P*P] dy*stride + dx into the staged region; angle 0 unused
+  const int* soff;       // [O][P*P] dy*stride + dx into the staged region; angle 0 unused
   const int4* bbox;      // [O] (dx_min, dx_max, dy_min, dy_max)
   int radius;            // max |offset| over all angles (and the axis crop)
   int stride;            // staged row length in bytes (multiple of 16)
@@ -94,14 +94,14 @@ GatherTables gather_tables(int P, int O) {
   const int stride = ((2 * radius + 1 + 15 + 4 + 15) / 16) * 16;
   GatherTables t{nullptr, nullptr, radius, stride, {}};
   for (int a = 0; a < O && a < 8; ++a) t.hbbox[a] = bbox[a];
-  if ((size_t)radius * stride + radius > 32767) return t;   // offsets must fit int16
-  std::vector<short> soff(off.size());
-  for (size_t i = 0; i < off.size(); ++i) soff[i] = (short)(off[i].y * stride + off[i].x);
-  short* d_off = nullptr;
+  // int32 offsets: a thread's four samples of a row are one 16-byte load
+  std::vector<int> soff(off.size());
+  for (size_t i = 0; i < off.size(); ++i) soff[i] = off[i].y * stride + off[i].x;
+  int* d_off = nullptr;
   int4* d_bb = nullptr;
-  if (cudaMalloc(&d_off, soff.size() * sizeof(short)) != cudaSuccess) return t;
+  if (cudaMalloc(&d_off, soff.size() * sizeof(int)) != cudaSuccess) return t;
   if (cudaMalloc(&d_bb, bbox.size() * sizeof(int4)) != cudaSuccess) return t;
-  cudaMemcpy(d_off, soff.data(), soff.size() * sizeof(short), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_off, soff.data(), soff.size() * sizeof(int), cudaMemcpyHostToDevice);
   cudaMemcpy(d_bb, bbox.data(), bbox.size() * sizeof(int4), cudaMemcpyHostToDevice);
   t.soff = d_off;
   t.bbox = d_bb;
@@ -127,14 +127,18 @@ R2_DEV void widen(uint32_t acc, uint32_t& e, uint32_t& o) {
 
 // reduce the 4 threads of a cell, write its O counts and add their squares
 // to the descriptor's squared norm (recode only permutes bins)
-R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int O, int* sq) {
+template <int OT>
+R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int O_rt, int* sq) {
+  const int O = OT ? OT : O_rt;
   e += __shfl_xor_sync(0xffffffffu, e, 1);
   o += __shfl_xor_sync(0xffffffffu, o, 1);
   e += __shfl_xor_sync(0xffffffffu, e, 2);
   o += __shfl_xor_sync(0xffffffffu, o, 2);
   if (writer) {
     int q = 0;
-    for (int v = 0; v < O; ++v) {
+#pragma unroll
+    for (int v = 0; v < (OT ? OT : 8); ++v) {
+      if (!OT && v >= O) break;
       const unsigned n = (((v & 1) ? o : e) >> (10 * (v >> 1))) & 1023u;
       out[v] = n;
       q += (int)(n * n);
@@ -152,14 +156,16 @@ R2_DEV uint32_t one_hot(uint32_t s) {
   return r;
 }
 
-// axis-aligned patch: thread = (cell, quarter); 4 columns x CS rows per thread
-template <int CS>
+// axis-aligned patch: thread = (cell, quarter); 4 columns x CS rows per thread.
+// OT / GT: orientation count and grid fixed at compile time (0 = runtime)
+template <int CS, int OT, int GT>
 R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsigned* cnt, int* sq) {
   const int tpc = CS / 4;                       // threads per cell
+  const int g = GT ? GT : c.g, O = OT ? OT : c.O;
   const int t = threadIdx.x;
-  const bool on = t < c.cells * tpc;
+  const bool on = t < g * g * tpc;
   const int cell = on ? t / tpc : 0, sub = t % tpc;
-  const int cr = cell / c.g, cc = cell % c.g;
+  const int cr = cell / g, cc = cell % g;
   uint32_t e = 0, o = 0;
   if (on) {
     const int col = off0 + cc * CS + 4 * sub;   // byte offset of this thread's 4 columns within a row
@@ -174,42 +180,45 @@ R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsign
       if (r % 7 == 6 || r == CS - 1) { widen(acc, e, o); acc = 0; }   // 4 samples/row: <= 28 per field
     }
   }
-  reduce_cell(e, o, on && sub == 0, cnt + cell * c.O, c.O, sq);
+  reduce_cell<OT>(e, o, on && sub == 0, cnt + cell * O, O, sq);
 }
 
 // rotated patch of angle table t: sample (i, j) at ctr + t[i*P + j]
-template <int CS>
-R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const short* __restrict__ t, unsigned* cnt,
+template <int CS, int OT, int GT>
+R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const int* __restrict__ t, unsigned* cnt,
                           int* sq) {
   const int tpc = CS / 4;
+  const int g = GT ? GT : c.g, O = OT ? OT : c.O, P = GT ? GT * CS : c.P;
   const int tid = threadIdx.x;
-  const bool on = tid < c.cells * tpc;
+  const bool on = tid < g * g * tpc;
   const int cell = on ? tid / tpc : 0, sub = tid % tpc;
-  const int cr = cell / c.g, cc = cell % c.g;
+  const int cr = cell / g, cc = cell % g;
   uint32_t e = 0, o = 0;
   if (on) {
-    const short* tr = t + (cr * CS) * c.P + cc * CS + 4 * sub;
+    const int4* tr = reinterpret_cast<const int4*>(t + (cr * CS) * P + cc * CS + 4 * sub);
     uint32_t acc = 0;
 #pragma unroll
     for (int r = 0; r < CS; ++r) {
-      const short2 a = __ldg(reinterpret_cast<const short2*>(tr + r * c.P));
-      const short2 b = __ldg(reinterpret_cast<const short2*>(tr + r * c.P + 2));
-      acc += one_hot(ctr[a.x]) + one_hot(ctr[a.y]) + one_hot(ctr[b.x]) + one_hot(ctr[b.y]);
+      const int4 a = __ldg(tr + r * (P / 4));
+      acc += one_hot(ctr[a.x]) + one_hot(ctr[a.y]) + one_hot(ctr[a.z]) + one_hot(ctr[a.w]);
       if (r % 7 == 6 || r == CS - 1) { widen(acc, e, o); acc = 0; }
     }
   }
-  reduce_cell(e, o, on && sub == 0, cnt + cell * c.O, c.O, sq);
+  reduce_cell<OT>(e, o, on && sub == 0, cnt + cell * O, O, sq);
 }
 
 // write one descriptor row: output bin (cell, w-1) holds the count of the
 // input value v with recode(v) = w, i.e. v = (w - 1 + pivot - 1) mod O + 1
 // (ref: mim.py:117-136)
+template <int OT, int GT>
 R2_DEV void emit_row(const DescribeArgs& a, const DescConst& c, const unsigned* cnt, int pivot, __half* row) {
+  const int O = OT ? OT : c.O, dim = GT ? GT * GT * O : c.dim;
   for (int i = threadIdx.x; i < a.stride; i += kT) {
     unsigned v = 0;
-    if (i < c.dim) {
-      const int cell = i / c.O, w = i % c.O;
-      v = cnt[cell * c.O + (w + pivot - 1) % c.O];
+    if (i < dim) {
+      const int cell = i / O, w = i % O;
+      const int u = w + pivot - 1;
+      v = cnt[cell * O + (u >= O ? u - O : u)];
     }
     row[i] = __uint2half_rn(v);
   }
@@ -219,19 +228,22 @@ R2_DEV void emit_row(const DescribeArgs& a, const DescConst& c, const unsigned* 
 // reads the axis-patch pixel (j, P-1-i) (ref: descriptor.py:46-82, P even), so
 // rotated cell (R, C) is axis cell (C, g-1-R): a permutation of the axis
 // counts, no gather
+template <int OT, int GT>
 R2_DEV void emit_row_rot90(const DescribeArgs& a, const DescConst& c, const unsigned* cnt, int pivot, __half* row) {
+  const int O = OT ? OT : c.O, g = GT ? GT : c.g, dim = g * g * O;
   for (int i = threadIdx.x; i < a.stride; i += kT) {
     unsigned v = 0;
-    if (i < c.dim) {
-      const int cell = i / c.O, w = i % c.O;
-      const int R = cell / c.g, C = cell % c.g;
-      v = cnt[(C * c.g + (c.g - 1 - R)) * c.O + (w + pivot - 1) % c.O];
+    if (i < dim) {
+      const int cell = i / O, w = i % O;
+      const int R = cell / g, C = cell % g;
+      const int u = w + pivot - 1;
+      v = cnt[(C * g + (g - 1 - R)) * O + (u >= O ? u - O : u)];
     }
     row[i] = __uint2half_rn(v);
   }
 }
 
-template <int CS>
+template <int CS, int OT, int GT>
 __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ mim, DescribeArgs a,
                                                   DescConst c, GatherTables tab, __half* __restrict__ slot_rows,
                                                   int* __restrict__ slot_meta, int* __restrict__ kp_skip) {
@@ -241,8 +253,9 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   uint32_t* s_dyn = s_raw + ((128u - (smem_u32(s_raw) & 127u)) & 127u) / 4;
   uint8_t* sreg = reinterpret_cast<uint8_t*>(s_dyn);
   // count buffers: axis patch, first and second rotated pick, [cells * O] each
+  const int O = OT ? OT : c.O, cells = GT ? GT * GT : c.cells;
   unsigned* cnt = s_dyn + (c.rows * c.stride) / 4;
-  unsigned* cnt_rot[2] = {cnt + c.cells * c.O, cnt + 2 * c.cells * c.O};
+  unsigned* cnt_rot[2] = {cnt + cells * O, cnt + 2 * cells * O};
   __shared__ int s_pick[16], s_np, s_sq[3];
   const int b = blockIdx.y, k = blockIdx.x;
   const size_t slot0 = ((size_t)b * a.kp_stride + k) * c.per;
@@ -322,14 +335,14 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   const int bx = x - ax0;                         // keypoint column within a staged row
   const uint8_t* ctr = sreg + c.R * c.stride + bx;   // keypoint pixel
   // ---- axis-aligned patch
-  count_axis<CS>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt, &s_sq[0]);
+  count_axis<CS, OT, GT>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt, &s_sq[0]);
   __syncthreads();
   // ---- dominant index / runner-up (ref: mim.py:69-91)
   if (threadIdx.x < 32) {
     unsigned hs[16];
-    for (int v = 0; v < c.O; ++v) {
+    for (int v = 0; v < O; ++v) {
       unsigned s = 0;
-      for (int q = threadIdx.x; q < c.cells; q += 32) s += cnt[q * c.O + v];
+      for (int q = threadIdx.x; q < cells; q += 32) s += cnt[q * O + v];
 #pragma unroll
       for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       hs[v] = s;
@@ -337,20 +350,20 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
     if (threadIdx.x == 0) {
       int np = 0, skip = 0;
       if (c.mode == 0) { s_pick[np++] = 1; }
-      else if (c.mode == 1) { for (int v = 1; v <= c.O; ++v) s_pick[np++] = v; }
+      else if (c.mode == 1) { for (int v = 1; v <= O; ++v) s_pick[np++] = v; }
       else {
         // first argmax; runner-up if >= ratio * peak (float64, inclusive);
         // runner-up ties go to the bin cyclically closest after the peak
         int pk = 0;
-        for (int v = 1; v < c.O; ++v) if (hs[v] > hs[pk]) pk = v;
+        for (int v = 1; v < O; ++v) if (hs[v] > hs[pk]) pk = v;
         double rv = -1.0;
-        for (int v = 0; v < c.O; ++v) if (v != pk && (double)hs[v] > rv) rv = (double)hs[v];
+        for (int v = 0; v < O; ++v) if (v != pk && (double)hs[v] > rv) rv = (double)hs[v];
         int picks[2] = {pk + 1, 0}, cand = 1;
         if (rv >= c.ratio * (double)hs[pk]) {
           int best = -1, bestd = 1 << 30;
-          for (int v = 0; v < c.O; ++v) {
+          for (int v = 0; v < O; ++v) {
             if (v == pk || (double)hs[v] != rv) continue;
-            const int d = ((v - pk) % c.O + c.O) % c.O;
+            const int d = ((v - pk) % O + O) % O;
             if (d < bestd) { bestd = d; best = v; }
           }
           picks[1] = best + 1;
@@ -375,18 +388,18 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   // (at most two) are counted into their own buffers; then one barrier
   const bool rot_mode = c.mode == 2 && c.rotate;
   int nrot = 0;
-  const int dom90 = (c.O % 2 == 0 && c.P % 2 == 0) ? c.O / 2 + 1 : -1;
+  const int dom90 = (O % 2 == 0 && c.P % 2 == 0) ? O / 2 + 1 : -1;
   for (int q = 0; q < np; ++q) {
     const int dom = s_pick[q];
     if (rot_mode && dom == dom90) {
-      emit_row_rot90(a, c, cnt, dom, slot_rows + (slot0 + q) * a.stride);
+      emit_row_rot90<OT, GT>(a, c, cnt, dom, slot_rows + (slot0 + q) * a.stride);
       if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[0]; }
     } else if (rot_mode && dom != 1) {
-      count_rotated<CS>(c, ctr, tab.soff + (size_t)(dom - 1) * c.P * c.P, cnt_rot[nrot], &s_sq[1 + nrot]);
+      count_rotated<CS, OT, GT>(c, ctr, tab.soff + (size_t)(dom - 1) * c.P * c.P, cnt_rot[nrot], &s_sq[1 + nrot]);
       ++nrot;
     } else {
       const int var = c.mode == 0 ? 1 : dom;
-      emit_row(a, c, cnt, var, slot_rows + (slot0 + q) * a.stride);
+      emit_row<OT, GT>(a, c, cnt, var, slot_rows + (slot0 + q) * a.stride);
       if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = var; meta[3 * q + 2] = s_sq[0]; }
     }
   }
@@ -396,7 +409,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
     for (int q = 0; q < np; ++q) {
       const int dom = s_pick[q];
       if (!(rot_mode && dom != 1 && dom != dom90)) continue;
-      emit_row(a, c, cnt_rot[r], dom, slot_rows + (slot0 + q) * a.stride);
+      emit_row<OT, GT>(a, c, cnt_rot[r], dom, slot_rows + (slot0 + q) * a.stride);
       if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[1 + r]; }
       ++r;
     }
@@ -542,8 +555,10 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
       c.tma = 1;
   }
-  cudaFuncSetAttribute(k_desc_main<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_desc_main<16><<<grid, kT, smem, st>>>(tmap, mim, a, c, tab, rows, meta, skip);
+  // the BASELINE grid (6 orientations, 6 x 6 cells) with constant indexing
+  auto kern = (c.O == 6 && c.g == 6) ? k_desc_main<16, 6, 6> : k_desc_main<16, 0, 0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, kT, smem, st>>>(tmap, mim, a, c, tab, rows, meta, skip);
   k_desc_scan<<<a.B, 1024, 0, st>>>(meta, skip, a, c.per, offs);
   dim3 g2((a.kp_stride * c.per + 7) / 8, a.B);
   k_desc_copy<<<g2, 256, 0, st>>>(rows, meta, offs, a, c.per);

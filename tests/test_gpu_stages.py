@@ -240,3 +240,32 @@ def test_match_large_vs_oracle(eng):
     got = dict(zip(t.tolist(), r.tolist()))
     agree = np.mean([got[int(b)] == int(a) for a, b, _ in want])
     assert agree == 1.0
+
+
+@pytest.mark.parametrize("n_orient,grid", [(4, 4), (6, 5), (5, 6)])
+def test_describe_non_default_grid_vs_oracle(eng, n_orient, grid):
+    """The runtime-indexed descriptor kernel (any n_orient <= 6, 16-px cells)
+    against the oracle; the BASELINE 6 x 6 x 6 grid runs the compile-time
+    specialised kernel, covered by test_describe_golden."""
+    rng = np.random.default_rng(n_orient * 10 + grid)
+    # blocky random MIM: dominant indices and runner-ups vary between keypoints
+    small = rng.integers(1, n_orient + 1, (30, 30))
+    mim = np.kron(small, np.ones((8, 8), np.int64))[:230, :230]
+    noise = rng.random(mim.shape) < 0.3
+    mim[noise] = rng.integers(1, n_orient + 1, int(noise.sum()))
+    size = 16 * grid
+    kps = np.zeros(60, dtype=O.KP_DTYPE)
+    kps["x"] = rng.integers(0, 230, 60)
+    kps["y"] = rng.integers(0, 230, 60)
+    want_c, want_k, want_v, want_skip = O.describe_rift2(mim, kps, size=size, grid=grid, n_orient=n_orient)
+    m = torch.as_tensor(mim.astype(np.uint8)).cuda()[None]
+    x = torch.as_tensor(kps["x"].astype(np.int32)).cuda()[None]
+    y = torch.as_tensor(kps["y"].astype(np.int32)).cuda()[None]
+    out = eng.describe(m, x, y, torch.tensor([60], dtype=torch.int32).cuda(), n_orient, size, grid)
+    torch.cuda.synchronize()
+    n = int(out["count"][0])
+    dim = grid * grid * n_orient
+    assert n == len(want_k) > 0 and int(out["skipped"][0]) == want_skip
+    assert np.array_equal(out["kp"][0][:n].cpu().numpy(), want_k)
+    assert np.array_equal(out["variant"][0][:n].cpu().numpy(), want_v)
+    assert np.array_equal(out["counts"][0][:n, :dim].cpu().numpy().astype(np.int64), want_c)
