@@ -212,6 +212,16 @@ int32_t rift2_evaluate(const int32_t* kp_x, const int32_t* kp_y, const int32_t* 
                        int32_t* out_n_correct, double* out_rmse, uint8_t* out_success, int32_t* out_bad,
                        void* stream);
 
+/* ---- diagnostics ----------------------------------------------------------
+ * The filter bank's exact-median stage (the Rayleigh noise estimate, ref:
+ * loggabor.py:222, np.median) on caller-given complex64 planes
+ * [planes][n]: amplitudes[i] = |z_i| as the bank computes it, medians[p] =
+ * the exact median of plane p's amplitudes (mean of the two middle order
+ * statistics for even n).  For tests; not on the pipeline path. */
+int32_t rift2_debug_median_workspace_size(int32_t planes, int32_t n, size_t* bytes);
+int32_t rift2_debug_median(const void* planes_c64, int32_t planes, int32_t n, float* amplitudes, float* medians,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,6 +58,8 @@ _SIGNATURES = {
                                      _c_p, _c_sz, _c_p]),
     "rift2_evaluate": (_c_int, [_c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_int, _c_int, _c_p, _c_d,
                                 _c_d, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "rift2_debug_median_workspace_size": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_sz)]),
+    "rift2_debug_median": (_c_int, [_c_p, _c_int, _c_int, _c_p, _c_p, _c_p, _c_sz, _c_p]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

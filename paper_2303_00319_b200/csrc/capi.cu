@@ -342,4 +342,19 @@ int32_t rift2_evaluate(const int32_t* kp_x, const int32_t* kp_y, const int32_t* 
   return map_internal(r2::evaluate_run(a, static_cast<cudaStream_t>(stream)), "rift2_evaluate");
 }
 
+int32_t rift2_debug_median_workspace_size(int32_t planes, int32_t n, size_t* bytes) {
+  if (planes < 1 || n < 1 || n >= (1 << 28) || !bytes) return fail(RIFT2_BAD_ARGUMENT, "bad median plane sizes");
+  *bytes = r2::debug_median_workspace_bytes(planes, n);
+  return RIFT2_OK;
+}
+
+int32_t rift2_debug_median(const void* planes_c64, int32_t planes, int32_t n, float* amplitudes, float* medians,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (planes < 1 || n < 1 || n >= (1 << 28)) return fail(RIFT2_BAD_ARGUMENT, "bad median plane sizes");
+  if (!planes_c64 || !amplitudes || !medians || !workspace) return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  return map_internal(r2::debug_median_run(static_cast<const float2*>(planes_c64), planes, n, amplitudes, medians,
+                                           workspace, workspace_bytes, static_cast<cudaStream_t>(stream)),
+                      "rift2_debug_median");
+}
+
 }  // extern "C"

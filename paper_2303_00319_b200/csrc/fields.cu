@@ -480,6 +480,7 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
   const float4* A = reinterpret_cast<const float4*>(Ap);
   unsigned* out = cand + (size_t)plane * n;
   const unsigned n4 = (n + 3) / 4;
+  const bool vec = (n & 3) == 0;                  // plane starts 16-byte aligned
   const unsigned lane = threadIdx.x & 31;
   const unsigned per_pass = kCollectVec * blockDim.x;
   for (unsigned base = blockIdx.x * per_pass; base < n4; base += gridDim.x * per_pass) {
@@ -490,11 +491,12 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
     for (int k = 0; k < kCollectVec; ++k) {
       const unsigned i = base + k * blockDim.x + threadIdx.x;
       qv[k] = make_float4(-1.f, -1.f, -1.f, -1.f);
-      if (4 * i + 3 < n) qv[k] = __ldg(&A[i]);
+      if (vec && 4 * i + 3 < n) qv[k] = __ldg(&A[i]);
       else if (i < n4) {
         qv[k].x = Ap[4 * i];
         if (4 * i + 1 < n) qv[k].y = Ap[4 * i + 1];
         if (4 * i + 2 < n) qv[k].z = Ap[4 * i + 2];
+        if (4 * i + 3 < n) qv[k].w = Ap[4 * i + 3];
       }
     }
     // per-thread hit mask over its 16 values, one warp prefix sum, one
@@ -1051,6 +1053,52 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   R2_DISPATCH_G(p.gw, launch_pc, Q, R0, thr, po, c, st);
   if (e != cudaSuccess) return 3;
   return 0;
+}
+
+
+// ---------------------------------------------------------- diagnostics ---
+// The exact-median stage on arbitrary complex planes: |z| of each element
+// (as k_rows_amp0 computes it) and its radix histogram, then the same
+// k_med_bins / k_med_collect / k_med_final kernels the filter bank runs.
+__global__ void __launch_bounds__(256) k_debug_amp(const float2* __restrict__ z, float* __restrict__ amps,
+                                                   unsigned* __restrict__ hist, unsigned n) {
+  __shared__ unsigned sh[kHistBins];
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const size_t off = (size_t)blockIdx.y * n;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float2 v = z[off + i];
+    const float a = sqrt_approx(fmaf(v.x, v.x, v.y * v.y));
+    amps[off + i] = a;
+    atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[(size_t)blockIdx.y * kHistBins + i], sh[i]);
+}
+
+size_t debug_median_workspace_bytes(int planes, int n) {
+  return align_up((size_t)planes * kHistBins * sizeof(unsigned)) + align_up((size_t)planes * sizeof(MedInfo)) +
+         align_up((size_t)planes * n * sizeof(unsigned)) + align_up((size_t)planes * sizeof(unsigned));
+}
+
+int debug_median_run(const float2* z, int planes, int n, float* amps, float* med, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  if (ws_bytes < debug_median_workspace_bytes(planes, n)) return 1;
+  char* w = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) { char* p = w; w += align_up(bytes); return p; };
+  auto* hist = reinterpret_cast<unsigned*>(take((size_t)planes * kHistBins * sizeof(unsigned)));
+  auto* info = reinterpret_cast<MedInfo*>(take((size_t)planes * sizeof(MedInfo)));
+  auto* cand = reinterpret_cast<unsigned*>(take((size_t)planes * n * sizeof(unsigned)));
+  auto* cnt = reinterpret_cast<unsigned*>(take((size_t)planes * sizeof(unsigned)));
+  cudaMemsetAsync(hist, 0, (size_t)planes * kHistBins * sizeof(unsigned), st);
+  cudaMemsetAsync(cnt, 0, (size_t)planes * sizeof(unsigned), st);
+  k_debug_amp<<<dim3(32, planes), 256, 0, st>>>(z, amps, hist, (unsigned)n);
+  k_med_bins<<<planes, 1024, 0, st>>>(hist, info, (unsigned)n);
+  dim3 grid((unsigned)min((size_t)64, ((size_t)n / 4 + 255) / 256 + 1), planes);
+  k_med_collect<<<grid, 256, 0, st>>>(amps, info, cand, cnt, (unsigned)n);
+  k_med_final<<<planes, 1024, 0, st>>>(cand, cnt, info, med, (unsigned)n, 1.0);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace r2

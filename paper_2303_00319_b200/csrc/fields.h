@@ -33,4 +33,9 @@ size_t fields_workspace_bytes(int B, int H, int W, int S, int O);
 int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, const FieldsOutputs& out,
                void* ws, size_t ws_bytes, cudaStream_t st);
 
+// diagnostics: exact median of |z| per plane through the filter bank's median kernels
+size_t debug_median_workspace_bytes(int planes, int n);
+int debug_median_run(const float2* z, int planes, int n, float* amps, float* med, void* ws, size_t ws_bytes,
+                     cudaStream_t st);
+
 }  // namespace r2

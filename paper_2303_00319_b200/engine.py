@@ -263,3 +263,22 @@ def evaluate(kp: dict, ref_img: torch.Tensor, tgt_img: torch.Tensor, m: dict, gt
                             _ptr(out["success"]), _ptr(out["bad"]), _stream())
     _lib.check(rc, "rift2_evaluate")
     return out
+
+
+def debug_median(z: torch.Tensor):
+    """Diagnostics (rift2_debug_median): z (planes, n) complex64 CUDA ->
+    (amplitudes (planes, n) float32, exact medians (planes,) float32) through
+    the filter bank's median kernels."""
+    lib = _lib.load(require_gpu=True)
+    if z.dim() != 2 or z.dtype != torch.complex64 or not z.is_cuda:
+        raise ParameterError("z must be a (planes, n) complex64 CUDA tensor")
+    z = z.contiguous()
+    planes, n = z.shape
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_debug_median_workspace_size(planes, n, ctypes.byref(nbytes)), "debug_median")
+    ws = torch.empty(nbytes.value, dtype=torch.uint8, device=z.device)
+    amps = torch.empty((planes, n), dtype=torch.float32, device=z.device)
+    med = torch.empty(planes, dtype=torch.float32, device=z.device)
+    _lib.check(lib.rift2_debug_median(_ptr(z), planes, n, _ptr(amps), _ptr(med), _ptr(ws), ws.numel(), _stream()),
+               "rift2_debug_median")
+    return amps, med

@@ -269,3 +269,25 @@ def test_describe_non_default_grid_vs_oracle(eng, n_orient, grid):
     assert np.array_equal(out["kp"][0][:n].cpu().numpy(), want_k)
     assert np.array_equal(out["variant"][0][:n].cpu().numpy(), want_v)
     assert np.array_equal(out["counts"][0][:n, :dim].cpu().numpy().astype(np.int64), want_c)
+
+
+@pytest.mark.parametrize("n,planes,kind", [(1024 * 1024, 3, "gauss"), (30000, 4, "ties"), (3375, 2, "gauss"),
+                                           (1, 1, "gauss"), (2, 1, "gauss"), (4097, 2, "const")])
+def test_exact_median_kernels(eng, n, planes, kind):
+    """The filter bank's Rayleigh-noise median (ref: loggabor.py:222,
+    np.median) is exact: through the same kernels, on planes whose
+    amplitudes the kernel also returns, the result equals np.median of those
+    amplitudes bit for bit -- odd / even / unaligned sizes, heavy ties, a
+    constant plane."""
+    g = torch.Generator(device="cuda").manual_seed(n + planes)
+    z = torch.randn((planes, n), dtype=torch.complex64, device="cuda", generator=g)
+    if kind == "ties":
+        z = torch.round(z.real * 4) / 4 + 0j
+        z = z.to(torch.complex64)
+    elif kind == "const":
+        z = torch.full((planes, n), 0.75 + 0.5j, dtype=torch.complex64, device="cuda")
+    amps, med = eng.debug_median(z)
+    torch.cuda.synchronize()
+    a = amps.cpu().numpy().astype(np.float64)
+    want = np.median(a, axis=1).astype(np.float32)
+    assert np.array_equal(med.cpu().numpy(), want)
