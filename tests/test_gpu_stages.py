@@ -291,3 +291,21 @@ def test_exact_median_kernels(eng, n, planes, kind):
     a = amps.cpu().numpy().astype(np.float64)
     want = np.median(a, axis=1).astype(np.float32)
     assert np.array_equal(med.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("shape", [(45, 75), (101, 83), (64, 130)])
+def test_detect_float_maps_unaligned_widths(eng, shape):
+    """float32 maps (the pipeline's dtype: vectorised staging when W % 4 == 0,
+    scalar otherwise) at widths that are not multiples of 4, against the
+    oracle's detect_keypoints on the same values."""
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1])
+    from scipy.ndimage import gaussian_filter
+    mm = [gaussian_filter(rng.random(shape), 1.5).astype(np.float32) for _ in range(2)]
+    t = torch.as_tensor(np.stack(mm)[None]).cuda()
+    out = eng.detect(t[:, 0], t[:, 1], 0.001, 80, 5)
+    torch.cuda.synchronize()
+    want = O.detect_keypoints(mm[0].astype(np.float64), mm[1].astype(np.float64), 0.001, 80, 10)
+    n = int(out["count"][0])
+    assert n == len(want) > 0
+    for f in ("x", "y", "response", "kind"):
+        assert np.array_equal(out[f][0][:n].cpu().numpy(), want[f]), f
