@@ -242,20 +242,21 @@ def test_match_large_vs_oracle(eng):
     assert agree == 1.0
 
 
-@pytest.mark.parametrize("n_orient,grid", [(4, 4), (6, 5), (5, 6)])
-def test_describe_non_default_grid_vs_oracle(eng, n_orient, grid):
+@pytest.mark.parametrize("n_orient,grid,width", [(4, 4, 230), (6, 5, 230), (5, 6, 230), (6, 6, 236), (6, 6, 229)])
+def test_describe_non_default_grid_vs_oracle(eng, n_orient, grid, width):
     """The runtime-indexed descriptor kernel (any n_orient <= 6, 16-px cells)
-    against the oracle; the BASELINE 6 x 6 x 6 grid runs the compile-time
-    specialised kernel, covered by test_describe_golden."""
-    rng = np.random.default_rng(n_orient * 10 + grid)
+    against the oracle, and the 6 x 6 x 6 kernel on widths that take the
+    word-staged (W % 4 == 0, no TMA) and byte-staged neighbourhood paths;
+    the TMA path is covered by test_describe_golden."""
+    rng = np.random.default_rng(n_orient * 10 + grid + width)
     # blocky random MIM: dominant indices and runner-ups vary between keypoints
     small = rng.integers(1, n_orient + 1, (30, 30))
-    mim = np.kron(small, np.ones((8, 8), np.int64))[:230, :230]
+    mim = np.kron(small, np.ones((8, 8), np.int64))[:230, :width]
     noise = rng.random(mim.shape) < 0.3
     mim[noise] = rng.integers(1, n_orient + 1, int(noise.sum()))
     size = 16 * grid
     kps = np.zeros(60, dtype=O.KP_DTYPE)
-    kps["x"] = rng.integers(0, 230, 60)
+    kps["x"] = rng.integers(0, width, 60)
     kps["y"] = rng.integers(0, 230, 60)
     want_c, want_k, want_v, want_skip = O.describe_rift2(mim, kps, size=size, grid=grid, n_orient=n_orient)
     m = torch.as_tensor(mim.astype(np.uint8)).cuda()[None]
