@@ -593,8 +593,12 @@ struct PcOut {
 
 template <int G>
 struct PcShape {
-  // pixels per thread: a CTA holds (up to) two rows
-  static constexpr int PIX = G == 0 ? 16 : (G == 128 ? 16 : (G >= 4 ? G / 4 : 1));
+  // CTA size: 2048- and 4096-point rows use 512 threads (four / eight FFT
+  // groups), so a thread carries 8 pixels' accumulators next to its FFT
+  // slice without spilling and the stage's transforms are balanced
+  static constexpr int T = (G == 64 || G == 128) ? 512 : kThreads;
+  // pixels per thread: a CTA holds (up to) two rows (one at 4096 points)
+  static constexpr int PIX = G == 0 ? 16 : (G >= 64 ? 8 : (G >= 4 ? G / 4 : 1));
 };
 
 R2_DEV float rcp_approx(float x) {
@@ -657,7 +661,7 @@ R2_DEV void pc_pair(const float2* __restrict__ b0, const float2* __restrict__ b1
 // Approximate sqrt / rcp / exp (relative error ~1e-7) stay far inside the
 // 1e-4 map tolerance.
 template <int G, int SC>
-__global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restrict__ Q, const float2* __restrict__ R0,
+__global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k_rows_pc(const float2* __restrict__ Q, const float2* __restrict__ R0,
                                                          const float* __restrict__ thr, PcOut out,
                                                          const __grid_constant__ FieldsConst c, int rr, int ops) {
   extern __shared__ float2 sm[];
@@ -669,6 +673,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
   const int b = blockIdx.y;
   const int y0 = 2 * blockIdx.x;
   constexpr int PIX = PcShape<G>::PIX;
+  constexpr int TPC = PcShape<G>::T;
   const int PL = padded_len(W);
   const int nb = rr * ops * S;
   const float* thr_b = thr + (size_t)b * O;
@@ -685,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
     for (int o0 = 0; o0 < O; o0 += ops) {
       const int no = min(ops, O - o0);
       if constexpr (G > 0) {
-        constexpr int NG = kThreads / G;
+        constexpr int NG = TPC / G;
         const int g = threadIdx.x / G, t = threadIdx.x % G;
         SyncWarp sw{group_mask(G)};
         SyncNamed sn{1 + g, G};
@@ -740,11 +745,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
         const float T = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
         if constexpr (SC > 0 && PIX % 2 == 0) {
           // pixel pairs (i, i + 1) in the fp32x2 lanes when both are live
-          // (warp-uniform: npix is a multiple of kThreads for these sizes)
-          if (npix == PIX * kThreads && y0 + rbase + rr <= H) {
+          // (warp-uniform: npix is a multiple of TPC for these sizes)
+          if (npix == PIX * TPC && y0 + rbase + rr <= H) {
 #pragma unroll
             for (int i = 0; i < PIX; i += 2) {
-              const int p0 = threadIdx.x + kThreads * i, p1 = p0 + kThreads;
+              const int p0 = threadIdx.x + TPC * i, p1 = p0 + TPC;
               const int r0 = p0 / W, x0 = p0 % W, r1 = p1 / W, x1 = p1 % W;
               const float2* b0 = sm + ((r0 * ops + oo) * S) * PL + pad32(x0);
               const float2* b1 = sm + ((r1 * ops + oo) * S) * PL + pad32(x1);
@@ -771,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
         }
 #pragma unroll
         for (int i = 0; i < PIX; ++i) {
-          const int p = threadIdx.x + kThreads * i;
+          const int p = threadIdx.x + TPC * i;
           if (p >= npix) continue;
           const int r = p / W, x = p % W;
           const int y = y0 + rbase + r;
@@ -815,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc(const float2* __restric
     }
 #pragma unroll
     for (int i = 0; i < PIX; ++i) {
-      const int p = threadIdx.x + kThreads * i;
+      const int p = threadIdx.x + TPC * i;
       if (p >= npix) continue;
       const int r = p / W, x = p % W;
       const int y = y0 + rbase + r;
@@ -955,7 +960,7 @@ static cudaError_t launch_pc_s(const float2* Q, const float2* R0, const float* t
   int rr, ops;
   size_t nbuf;
   if constexpr (G > 0) {
-    const int NG = kThreads / G;
+    const int NG = PcShape<G>::T / G;
     rr = (2 * c.S * PLb <= budget) ? 2 : 1;
     ops = NG / (rr * c.S);
     if (ops < 1) ops = 1;
@@ -970,7 +975,7 @@ static cudaError_t launch_pc_s(const float2* Q, const float2* R0, const float* t
   cudaError_t e = set_smem(k_rows_pc<G, SC>, smem);
   if (e != cudaSuccess) return e;
   dim3 grid((c.H + 1) / 2, c.B);
-  k_rows_pc<G, SC><<<grid, kThreads, smem, st>>>(Q, R0, thr, out, c, rr, ops);
+  k_rows_pc<G, SC><<<grid, PcShape<G>::T, smem, st>>>(Q, R0, thr, out, c, rr, ops);
   return cudaPeekAtLastError();
 }
 

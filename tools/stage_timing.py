@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--pairs", type=int, default=16)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--max-kp", type=int, default=5000)
     args = ap.parse_args()
     t0 = time.time()
     imgs, _ = synth.make_batch(min(args.pairs, 4), args.size)
@@ -38,11 +39,11 @@ def main():
         ev[0].record()
         f = engine.fields(x, bank)
         ev[1].record()
-        k = engine.detect(f["mmin"], f["mmax"], 0.001, 5000, 48)
+        k = engine.detect(f["mmin"], f["mmax"], 0.001, args.max_kp, 48)
         ev[2].record()
-        d = engine.describe(f["mim"], k["x"], k["y"], k["count"], 6)
+        d = engine.describe(f["mim"], k["x"], k["y"], k["count"], 6, capacity=2 * args.max_kp)
         ev[3].record()
-        m = engine.match(d, 216, rb, tb, 5000)
+        m = engine.match(d, 216, rb, tb, args.max_kp)
         ev[4].record()
         torch.cuda.synchronize()
         return [ev[i].elapsed_time(ev[i + 1]) for i in range(4)], k, d, m
