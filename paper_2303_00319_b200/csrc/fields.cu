@@ -24,6 +24,8 @@
 //   R0    [B][O][H][W] c64            scale-0 responses, row-major
 //   amp0  [B][O][H*W] f32
 //   outputs M, m [B][H][W] f32, MIM [B][H][W] u8, optional a_o/pc [B][O][H][W], amax [B][H][W]
+#include <algorithm>
+
 #include "fft.cuh"
 #include "fields.h"
 
@@ -424,6 +426,8 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
 struct MedInfo {
   unsigned bin[2];     // level-1 bins of ranks (n-1)/2 and n/2
   unsigned rank[2];    // ranks inside those bins
+  unsigned pre[2];     // after level 2: float bits >> 9
+  unsigned rank2[2];   // ranks inside those level-2 bins
 };
 
 __device__ void block_exclusive_scan_1024(unsigned* data, int n, unsigned* tmp) {
@@ -540,45 +544,119 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
   }
 }
 
-// radix select the exact values among the candidates, then the noise threshold
-__global__ void __launch_bounds__(1024) k_med_final(const unsigned* __restrict__ cand, const unsigned* __restrict__ cnt,
-                                                    const MedInfo* __restrict__ info, float* __restrict__ thr,
-                                                    unsigned n, double thr_factor) {
-  __shared__ unsigned h[1024];
-  __shared__ unsigned tmp[1024];
-  __shared__ unsigned sel_prefix, sel_rank;
-  const int plane = blockIdx.x;
-  const unsigned* cd = cand + (size_t)plane * n;
+// Levels 2 (float bits 18..9) and 3 (bits 8..0) of the radix select over
+// the candidates, as histograms spread over kMedBlk CTAs per plane (the
+// candidate count is data dependent: ~3 % of a plane, 0.5 M at 4096^2) with
+// the bin picks in small per-plane steps.
+constexpr int kMedBlk = 16;                      // minimum CTAs per plane
+constexpr int kMedH = 2 * 1024;                  // global histogram words per plane (two ranks)
+
+// the bin holding `rank` in a 256-thread block scan of hist[0..nbins)
+__device__ void med_pick(const unsigned* __restrict__ hist, int nbins, unsigned rank, unsigned* s_out) {
+  __shared__ unsigned s_w[8];
+  const int t = threadIdx.x, per = nbins / 256;
+  unsigned loc[4], sum = 0;
+  for (int k = 0; k < per; ++k) { loc[k] = hist[t * per + k]; sum += loc[k]; }
+  unsigned incl = sum;
+  const unsigned lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= (unsigned)d) incl += v;
+  }
+  if (lane == 31) s_w[w] = incl;
+  __syncthreads();
+  unsigned run = incl - sum;
+  for (int k = 0; k < (int)w; ++k) run += s_w[k];
+  for (int k = 0; k < per; ++k) {
+    if (rank >= run && rank < run + loc[k]) { s_out[0] = t * per + k; s_out[1] = rank - run; }
+    run += loc[k];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_med_h2(const unsigned* __restrict__ cand, const unsigned* __restrict__ cnt,
+                                                const MedInfo* __restrict__ info, unsigned* __restrict__ gh,
+                                                unsigned n) {
+  __shared__ unsigned h[2][1024];
+  const int plane = blockIdx.y;
   const unsigned c = cnt[plane];
+  const unsigned b0 = info[plane].bin[0], b1 = info[plane].bin[1];
+  const unsigned* cd = cand + (size_t)plane * n;
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const unsigned bits = cd[i], hb = bits >> 19, lv = (bits >> 9) & 1023u;
+    if (hb == b0) atomicAdd(&h[0][lv], 1u);
+    if (b1 != b0 && hb == b1) atomicAdd(&h[1][lv], 1u);
+  }
+  __syncthreads();
+  unsigned* g = gh + (size_t)plane * kMedH;
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    if ((&h[0][0])[i]) atomicAdd(&g[i], (&h[0][0])[i]);
+}
+
+// every CTA picks the level-2 bins (same result), CTA 0 records them; then
+// the level-3 histograms of the candidates under those prefixes
+__global__ void __launch_bounds__(256) k_med_h3(const unsigned* __restrict__ cand, const unsigned* __restrict__ cnt,
+                                                MedInfo* __restrict__ info, const unsigned* __restrict__ gh2,
+                                                unsigned* __restrict__ gh3, unsigned n) {
+  __shared__ unsigned h[2][512];
+  __shared__ unsigned s_pick[2];
+  const int plane = blockIdx.y;
+  const unsigned c = cnt[plane];
+  const MedInfo inf = info[plane];
+  const unsigned* g2 = gh2 + (size_t)plane * kMedH;
+  unsigned pre[2], rk[2];
+  for (int q = 0; q < 2; ++q) {
+    med_pick(g2 + (inf.bin[1] != inf.bin[0] ? q * 1024 : 0), 1024, inf.rank[q], s_pick);
+    pre[q] = (inf.bin[q] << 10) | s_pick[0];
+    rk[q] = s_pick[1];
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    info[plane].pre[0] = pre[0]; info[plane].pre[1] = pre[1];
+    info[plane].rank2[0] = rk[0]; info[plane].rank2[1] = rk[1];
+  }
+  const unsigned* cd = cand + (size_t)plane * n;
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const unsigned bits = cd[i], p9 = bits >> 9;
+    if (p9 == pre[0]) atomicAdd(&h[0][bits & 511u], 1u);
+    if (pre[1] != pre[0] && p9 == pre[1]) atomicAdd(&h[1][bits & 511u], 1u);
+  }
+  __syncthreads();
+  unsigned* g = gh3 + (size_t)plane * kMedH;
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x)
+    if ((&h[0][0])[i]) atomicAdd(&g[i], (&h[0][0])[i]);
+}
+
+// level-3 picks -> the two middle order statistics -> the noise threshold
+__global__ void __launch_bounds__(256) k_med_final(const MedInfo* __restrict__ info, const unsigned* __restrict__ gh3,
+                                                   float* __restrict__ thr, double thr_factor) {
+  __shared__ unsigned s_pick[2];
+  const int plane = blockIdx.x;
+  const MedInfo inf = info[plane];
+  const unsigned* g3 = gh3 + (size_t)plane * kMedH;
   double val[2];
   for (int q = 0; q < 2; ++q) {
-    unsigned prefix = info[plane].bin[q];   // bits >> 19
-    unsigned rank = info[plane].rank[q];
-    const int shifts[2] = {9, 0};           // level 2: bits 18..9, level 3: bits 8..0
-    const int widths[2] = {10, 9};
-    for (int lv = 0; lv < 2; ++lv) {
-      const int sh = shifts[lv], nb = 1 << widths[lv];
-      for (int i = threadIdx.x; i < 1024; i += blockDim.x) h[i] = 0;
-      __syncthreads();
-      for (unsigned i = threadIdx.x; i < c; i += blockDim.x) {
-        const unsigned bits = cd[i];
-        if ((bits >> (sh + widths[lv])) == prefix) atomicAdd(&h[(bits >> sh) & (nb - 1)], 1u);
-      }
-      __syncthreads();
-      block_exclusive_scan_1024(h, nb, tmp);
-      for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-        const unsigned lo = h[i];
-        const unsigned hi = (i + 1 < nb) ? h[i + 1] : 0xffffffffu;
-        if (rank >= lo && rank < hi) { sel_prefix = (prefix << widths[lv]) | i; sel_rank = rank - lo; }
-      }
-      __syncthreads();
-      prefix = sel_prefix;
-      rank = sel_rank;
-      __syncthreads();
-    }
-    val[q] = (double)__uint_as_float(prefix);
+    med_pick(g3 + (inf.pre[1] != inf.pre[0] ? q * 512 : 0), 512, inf.rank2[q], s_pick);
+    val[q] = (double)__uint_as_float((inf.pre[q] << 9) | s_pick[0]);
+    __syncthreads();
   }
   if (threadIdx.x == 0) thr[plane] = (float)(0.5 * (val[0] + val[1]) * thr_factor);
+}
+
+static void launch_med_select(const unsigned* cand, const unsigned* cnt, MedInfo* info, unsigned* gh, float* thr,
+                              int planes, unsigned n, double factor, cudaStream_t st) {
+  unsigned* gh2 = gh;
+  unsigned* gh3 = gh + (size_t)planes * kMedH;
+  cudaMemsetAsync(gh, 0, (size_t)planes * 2 * kMedH * sizeof(unsigned), st);
+  const unsigned blk = std::min(256u, std::max((unsigned)kMedBlk, n >> 16));   // ~3 % of n are candidates
+  k_med_h2<<<dim3(blk, planes), 256, 0, st>>>(cand, cnt, info, gh2, n);
+  k_med_h3<<<dim3(blk, planes), 256, 0, st>>>(cand, cnt, info, gh2, gh3, n);
+  k_med_final<<<planes, 256, 0, st>>>(info, gh3, thr, factor);
 }
 
 // ----------------------------------------------------------------- K3b ---
@@ -859,7 +937,7 @@ static bool make_plan(int n, GenericPlan& p) {
 struct FieldsPlan {
   int B, H, W, Wh, Hp, S, O, F;
   int gw, gh;
-  size_t off_P, off_Q, off_R0, off_amp0, off_hist, off_info, off_cand, off_cnt, off_thr, total;
+  size_t off_P, off_Q, off_R0, off_amp0, off_hist, off_info, off_cand, off_cnt, off_mh, off_thr, total;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -879,6 +957,7 @@ static FieldsPlan plan_fields(int B, int H, int W, int S, int O) {
   p.off_info = take((size_t)B * O * sizeof(MedInfo));
   p.off_cand = take((size_t)B * O * n * sizeof(unsigned));
   p.off_cnt = take((size_t)B * O * sizeof(unsigned));
+  p.off_mh = take((size_t)B * O * 2 * kMedH * sizeof(unsigned));
   p.off_thr = take((size_t)B * O * sizeof(float));
   p.total = off;
   return p;
@@ -1052,7 +1131,7 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
     dim3 grid((unsigned)min((size_t)64, ((size_t)n / 4 + 255) / 256 + 1), B * c.O);
     k_med_collect<<<grid, 256, 0, st>>>(amp0, info, cand, cnt, n);
   }
-  k_med_final<<<B * c.O, 1024, 0, st>>>(cand, cnt, info, thr, n, c.thr_factor);
+  launch_med_select(cand, cnt, info, reinterpret_cast<unsigned*>(w + p.off_mh), thr, B * c.O, n, c.thr_factor, st);
   if (cudaPeekAtLastError() != cudaSuccess) return 3;
   PcOut po{o.mmax, o.mmin, o.mim, o.a_o, o.pc, o.amax};
   R2_DISPATCH_G(p.gw, launch_pc, Q, R0, thr, po, c, st);
@@ -1084,7 +1163,8 @@ __global__ void __launch_bounds__(256) k_debug_amp(const float2* __restrict__ z,
 
 size_t debug_median_workspace_bytes(int planes, int n) {
   return align_up((size_t)planes * kHistBins * sizeof(unsigned)) + align_up((size_t)planes * sizeof(MedInfo)) +
-         align_up((size_t)planes * n * sizeof(unsigned)) + align_up((size_t)planes * sizeof(unsigned));
+         align_up((size_t)planes * n * sizeof(unsigned)) + align_up((size_t)planes * sizeof(unsigned)) +
+         align_up((size_t)planes * 2 * kMedH * sizeof(unsigned));
 }
 
 int debug_median_run(const float2* z, int planes, int n, float* amps, float* med, void* ws, size_t ws_bytes,
@@ -1096,13 +1176,14 @@ int debug_median_run(const float2* z, int planes, int n, float* amps, float* med
   auto* info = reinterpret_cast<MedInfo*>(take((size_t)planes * sizeof(MedInfo)));
   auto* cand = reinterpret_cast<unsigned*>(take((size_t)planes * n * sizeof(unsigned)));
   auto* cnt = reinterpret_cast<unsigned*>(take((size_t)planes * sizeof(unsigned)));
+  auto* mh = reinterpret_cast<unsigned*>(take((size_t)planes * 2 * kMedH * sizeof(unsigned)));
   cudaMemsetAsync(hist, 0, (size_t)planes * kHistBins * sizeof(unsigned), st);
   cudaMemsetAsync(cnt, 0, (size_t)planes * sizeof(unsigned), st);
   k_debug_amp<<<dim3(32, planes), 256, 0, st>>>(z, amps, hist, (unsigned)n);
   k_med_bins<<<planes, 1024, 0, st>>>(hist, info, (unsigned)n);
   dim3 grid((unsigned)min((size_t)64, ((size_t)n / 4 + 255) / 256 + 1), planes);
   k_med_collect<<<grid, 256, 0, st>>>(amps, info, cand, cnt, (unsigned)n);
-  k_med_final<<<planes, 1024, 0, st>>>(cand, cnt, info, med, (unsigned)n, 1.0);
+  launch_med_select(cand, cnt, info, mh, med, planes, (unsigned)n, 1.0, st);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
 
