@@ -387,61 +387,88 @@ R2_DEV unsigned hash_pix(unsigned p, unsigned mask) { return (p * 2654435761u) &
 // Greedy 2-px suppression (ref: detector.py:116-137) as a priority MIS:
 // a point is accepted once every higher-priority neighbour is rejected and
 // rejected as soon as one of them is accepted; rounds repeat to a fixpoint,
-// which equals the sequential greedy walk.
-__global__ void __launch_bounds__(1024) k_merge_suppress(const K128* __restrict__ sorted, const unsigned* __restrict__ nsel,
-                                                         K128* __restrict__ merged, int* __restrict__ hkey,
-                                                         int* __restrict__ hval, int tsz, int* __restrict__ nbr,
-                                                         int W, DetectArgs a) {
+// which equals the sequential greedy walk.  Three kernels: placement of
+// every key in the merged (corners + edges) order plus a pixel hash, the
+// neighbour lists, and the MIS rounds with the ordered compaction (one CTA
+// per image).
+
+// merged position of each key (binary search in the other list; a corner
+// precedes an equal edge key, as in a merge taking ties from the first
+// list) and its pixel -> position hash entry
+__global__ void __launch_bounds__(256) k_merge_place(const K128* __restrict__ sorted, const unsigned* __restrict__ nsel,
+                                                     K128* __restrict__ merged, int* __restrict__ hkey,
+                                                     int* __restrict__ hval, int tsz, int W, int K) {
+  const int b = blockIdx.y;
+  const int nc = nsel[2 * b], ne = nsel[2 * b + 1];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nc + ne) return;
+  const K128* corners = sorted + (size_t)(2 * b) * K;
+  const K128* edges = sorted + (size_t)(2 * b + 1) * K;
+  const bool is_c = e < nc;
+  const int i = is_c ? e : e - nc;
+  const K128 k = is_c ? corners[i] : edges[i];
+  const K128* other = is_c ? edges : corners;
+  int lo = 0, hi = is_c ? ne : nc;
+  while (lo < hi) {                               // first other key not before k
+    const int m = (lo + hi) >> 1;
+    if (is_c ? k_less(other[m], k) : k_leq(other[m], k)) lo = m + 1; else hi = m;
+  }
+  const int pos = i + lo;
+  merged[(size_t)b * 2 * K + pos] = k;
+  const int pix = (int)(k.lo >> 32) * W + (int)((k.lo >> 8) & 0xffffffull);
+  int* hk = hkey + (size_t)b * tsz;
+  const unsigned mask = (unsigned)tsz - 1;
+  unsigned h = hash_pix((unsigned)pix, mask);
+  while (atomicCAS(&hk[h], -1, pix) != -1) h = (h + 1) & mask;
+  hval[(size_t)b * tsz + h] = pos;
+}
+
+// higher-priority keys within distance 2 of each key (-1 terminated)
+__global__ void __launch_bounds__(256) k_merge_nbr(const unsigned* __restrict__ nsel, const K128* __restrict__ merged,
+                                                   const int* __restrict__ hkey, const int* __restrict__ hval,
+                                                   int tsz, int* __restrict__ nbr, int W, int K) {
+  const int b = blockIdx.y;
+  const int n = nsel[2 * b] + nsel[2 * b + 1];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int* hk = hkey + (size_t)b * tsz;
+  const int* hv = hval + (size_t)b * tsz;
+  int* nb = nbr + ((size_t)b * 2 * K + i) * kMaxNbr;
+  const unsigned mask = (unsigned)tsz - 1;
+  const K128 k = merged[(size_t)b * 2 * K + i];
+  const int y = (int)(k.lo >> 32), x = (int)((k.lo >> 8) & 0xffffffull);
+  int cntn = 0;
+  for (int dy = -2; dy <= 2; ++dy)
+    for (int dx = -2; dx <= 2; ++dx) {
+      if (dx * dx + dy * dy > 4) continue;
+      const int yy = y + dy, xx = x + dx;
+      if (yy < 0 || xx < 0 || xx >= W) continue;
+      const int pix = yy * W + xx;
+      unsigned h = hash_pix((unsigned)pix, mask);
+      int key;
+      while ((key = hk[h]) != -1) {
+        if (key == pix) {
+          const int j = hv[h];
+          if (j < i && cntn < kMaxNbr) nb[cntn++] = j;
+        }
+        h = (h + 1) & mask;
+      }
+    }
+  if (cntn < kMaxNbr) nb[cntn] = -1;
+}
+
+__global__ void __launch_bounds__(1024) k_merge_mis(const unsigned* __restrict__ nsel, const K128* __restrict__ merged,
+                                                    const int* __restrict__ nbr, DetectArgs a) {
   extern __shared__ unsigned char s_status[];   // 0 undecided, 1 accepted, 2 rejected
   __shared__ int s_flag;
   __shared__ int s_base;
   __shared__ int s_warp[32];
   const int b = blockIdx.x;
   const int K = a.max_points;
-  const K128* corners = sorted + (size_t)(2 * b) * K;
-  const K128* edges = sorted + (size_t)(2 * b + 1) * K;
-  const int nc = nsel[2 * b], ne = nsel[2 * b + 1];
-  const int n = nc + ne;
-  K128* mg = merged + (size_t)b * 2 * K;
-  int* hk = hkey + (size_t)b * tsz;
-  int* hv = hval + (size_t)b * tsz;
-  int* nb = nbr + (size_t)b * 2 * K * kMaxNbr;
-  const unsigned mask = (unsigned)tsz - 1;
-  merge_path_block(corners, nc, edges, ne, mg);
-  for (int i = threadIdx.x; i < tsz; i += blockDim.x) hk[i] = -1;
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const K128 k = mg[i];
-    const int pix = (int)(k.lo >> 32) * W + (int)((k.lo >> 8) & 0xffffffull);
-    unsigned h = hash_pix((unsigned)pix, mask);
-    while (true) {
-      if (atomicCAS(&hk[h], -1, pix) == -1) { hv[h] = i; break; }
-      h = (h + 1) & mask;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const K128 k = mg[i];
-    const int y = (int)(k.lo >> 32), x = (int)((k.lo >> 8) & 0xffffffull);
-    int cntn = 0;
-    for (int dy = -2; dy <= 2; ++dy)
-      for (int dx = -2; dx <= 2; ++dx) {
-        if (dx * dx + dy * dy > 4) continue;
-        const int yy = y + dy, xx = x + dx;
-        if (yy < 0 || xx < 0 || xx >= W) continue;
-        const int pix = yy * W + xx;
-        unsigned h = hash_pix((unsigned)pix, mask);
-        while (hk[h] != -1) {
-          if (hk[h] == pix) {
-            const int j = hv[h];
-            if (j < i && cntn < kMaxNbr) nb[(size_t)i * kMaxNbr + cntn++] = j;
-          }
-          h = (h + 1) & mask;
-        }
-      }
-    if (cntn < kMaxNbr) nb[(size_t)i * kMaxNbr + cntn] = -1;
-    s_status[i] = cntn == 0 ? 1 : 0;
-  }
+  const int n = nsel[2 * b] + nsel[2 * b + 1];
+  const K128* mg = merged + (size_t)b * 2 * K;
+  const int* nb = nbr + (size_t)b * 2 * K * kMaxNbr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_status[i] = nb[(size_t)i * kMaxNbr] == -1 ? 1 : 0;
   __syncthreads();
   while (true) {
     if (threadIdx.x == 0) s_flag = 0;
@@ -581,8 +608,12 @@ int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, siz
     k_emit_single<<<a.B, 1024, 0, st>>>(sorted, nsel, a);
   } else {
     const size_t smem = (size_t)2 * a.max_points;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_merge_suppress, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_merge_suppress<<<a.B, 1024, smem, st>>>(sorted, nsel, merged, hk, hv, p.tsz, nbr, a.W, a);
+    const dim3 g2((2 * a.max_points + 255) / 256, a.B);
+    cudaMemsetAsync(hk, 0xFF, (size_t)a.B * p.tsz * sizeof(int), st);   // empty slots = -1
+    k_merge_place<<<g2, 256, 0, st>>>(sorted, nsel, merged, hk, hv, p.tsz, a.W, a.max_points);
+    k_merge_nbr<<<g2, 256, 0, st>>>(nsel, merged, hk, hv, p.tsz, nbr, a.W, a.max_points);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_merge_mis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_merge_mis<<<a.B, 1024, smem, st>>>(nsel, merged, nbr, a);
   }
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
