@@ -24,10 +24,13 @@ namespace r2 {
 
 namespace {
 
-constexpr int kTile = 32;
+constexpr int kTile = 32;                 // score tile width
+constexpr int kTileY = 64;                // score tile height (halves the border ring per pixel)
 constexpr int kHalo = 4;                  // 3 for the ring + 1 for NMS
 constexpr int kIn = kTile + 2 * kHalo;    // 40
+constexpr int kInY = kTileY + 2 * kHalo;  // 72
 constexpr int kSc = kTile + 2;            // 34
+constexpr int kScY = kTileY + 2;          // 66
 constexpr int kMaxNbr = 32;
 
 // Bresenham circle of radius 3 (ref: detector.py:21-26, _CIRCLE) is spelled
@@ -175,8 +178,8 @@ __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, co
                                                   const unsigned long long* __restrict__ mm, double thr,
                                                   int margin, int nm, K128* __restrict__ cand,
                                                   unsigned* __restrict__ cnt, size_t cap) {
-  __shared__ __align__(16) T sv[kIn][kIn + 1];
-  __shared__ double ss[kSc][kSc + 1];
+  __shared__ __align__(16) T sv[kInY][kIn + 1];
+  __shared__ double ss[kScY][kSc + 1];
   const int plane = blockIdx.z;
   const int kind = nm == 2 ? (plane & 1) : 0;
   const T* p = plane_ptr(mins, maxs, plane, nm, (size_t)H * W);
@@ -185,22 +188,22 @@ __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, co
   const double span = hi - lo;
   if (!(span > 0)) return;   // normalised map is all zeros: no keypoints
   const double rspan = 1.0 / span;
-  const int ty0 = blockIdx.y * kTile, tx0 = blockIdx.x * kTile;
+  const int ty0 = blockIdx.y * kTileY, tx0 = blockIdx.x * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // tile-uniform: the staged input lies inside the image / every scored
   // pixel is at least 3 pixels from the border
-  const bool in_img = ty0 - kHalo >= 0 && ty0 + kTile + kHalo <= H && tx0 - kHalo >= 0 && tx0 + kTile + kHalo <= W;
-  const bool inner = ty0 - 1 >= 3 && ty0 + kTile + 1 <= H - 3 && tx0 - 1 >= 3 && tx0 + kTile + 1 <= W - 3;
+  const bool in_img = ty0 - kHalo >= 0 && ty0 + kTileY + kHalo <= H && tx0 - kHalo >= 0 && tx0 + kTile + kHalo <= W;
+  const bool inner = ty0 - 1 >= 3 && ty0 + kTileY + 1 <= H - 3 && tx0 - 1 >= 3 && tx0 + kTile + 1 <= W - 3;
   if (sizeof(T) == 4 && in_img && (W & 3) == 0) {
     // 40 x 40 floats as 10 float4 per row (the row start tx0 - 4 is 16-byte aligned)
-    for (int i = threadIdx.x; i < kIn * (kIn / 4); i += 256) {
+    for (int i = threadIdx.x; i < kInY * (kIn / 4); i += 256) {
       const int r = i / (kIn / 4), q = i - r * (kIn / 4);
       const float4 f = __ldg(reinterpret_cast<const float4*>(p + (size_t)(ty0 - kHalo + r) * W + tx0 - kHalo) + q);
       T* d = &sv[r][4 * q];
       d[0] = f.x; d[1] = f.y; d[2] = f.z; d[3] = f.w;
     }
   } else {
-    for (int r = warp; r < kIn; r += 8) {
+    for (int r = warp; r < kInY; r += 8) {
       const int yy = ty0 - kHalo + r;
       const bool row_in = yy >= 0 && yy < H;
       const T* prow = p + (size_t)(row_in ? yy : 0) * W;
@@ -213,20 +216,20 @@ __global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, co
   __syncthreads();
   // interior 32 x 32 scores: warp = row group, lane = column
 #pragma unroll 1
-  for (int r = warp; r < kTile; r += 8)
+  for (int r = warp; r < kTileY; r += 8)
     ss[r + 1][lane + 1] = tile_score(sv, r + 1, lane + 1, ty0 + r, tx0 + lane, H, W, inner, lo, span, rspan);
-  // the one-pixel border ring of the score tile (132 positions)
-  if (threadIdx.x < 4 * kSc - 4) {
+  // the one-pixel border ring of the score tile (196 positions)
+  if (threadIdx.x < 2 * kSc + 2 * kTileY) {
     int sy, sx;
     const int i = threadIdx.x;
     if (i < kSc) { sy = 0; sx = i; }
-    else if (i < 2 * kSc) { sy = kSc - 1; sx = i - kSc; }
-    else if (i < 2 * kSc + kTile) { sy = 1 + i - 2 * kSc; sx = 0; }
-    else { sy = 1 + i - 2 * kSc - kTile; sx = kSc - 1; }
+    else if (i < 2 * kSc) { sy = kScY - 1; sx = i - kSc; }
+    else if (i < 2 * kSc + kTileY) { sy = 1 + i - 2 * kSc; sx = 0; }
+    else { sy = 1 + i - 2 * kSc - kTileY; sx = kSc - 1; }
     ss[sy][sx] = tile_score(sv, sy, sx, ty0 - 1 + sy, tx0 - 1 + sx, H, W, false, lo, span, rspan);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kTileY * kTile; i += blockDim.x) {
     const int ly = i >> 5, lx = i & 31;
     const int y = ty0 + ly, x = tx0 + lx;
     bool keep = false;
@@ -585,7 +588,7 @@ int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, siz
     k_minmax<T><<<grid, 256, 0, st>>>(mins, maxs, nm, n, mm);
   }
   {
-    dim3 grid((a.W + kTile - 1) / kTile, (a.H + kTile - 1) / kTile, planes);
+    dim3 grid((a.W + kTile - 1) / kTile, (a.H + kTileY - 1) / kTileY, planes);
     k_fast_nms<T><<<grid, 256, 0, st>>>(mins, maxs, a.H, a.W, mm, a.threshold, a.margin, nm, cand, cnt, p.cap);
   }
   {
