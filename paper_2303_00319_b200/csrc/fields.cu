@@ -25,6 +25,7 @@
 //   amp0  [B][O][H*W] f32
 //   outputs M, m [B][H][W] f32, MIM [B][H][W] u8, optional a_o/pc [B][O][H][W], amax [B][H][W]
 #include <algorithm>
+#include <cmath>
 
 #include "fft.cuh"
 #include "fields.h"
@@ -48,6 +49,12 @@ struct FieldsConst {
   float log_lambda[kMaxS];     // ln(lambda_s) = -ln(f0_s)
   float a2;                    // log2(e) / (2 ln(sigma_on_f)^2)
   float b2;                    // log2(e) / (2 sigma_theta^2)
+  // the fast column passes work on pre-scaled coordinates, so a transfer
+  // value is exp2(-(d^2 + dr^2)): ln r and ln(lambda) times sqrt(a2),
+  // angles times sqrt(b2)
+  float sa, sb;                // sqrt(a2), sqrt(b2)
+  float ll_s[kMaxS], ang_s[kMaxO];
+  float pi_s, two_pi_s;
   float ang[kMaxO], cos_a[kMaxO], sin_a[kMaxO];
   float spread_cutoff, spread_gain, inv_sm1;
   float lp_lncut;              // ln(0.45)
@@ -155,12 +162,14 @@ R2_DEV float transfer(float lnr, float L2, float th, float ll, float ang, float 
 }
 
 // transfer of filter (s, o) without the radius-only factor lowpass / (H*W),
-// which the fast column pass folds into the spectrum once per column
-R2_DEV float transfer_s(float lnr, float th, float ll, float ang, float a2, float b2) {
-  float d = fabsf(th - ang);
-  d = d > kPi ? kTwoPi - d : d;
-  const float dr = lnr + ll;
-  return ex2(fmaf(d * d, -b2, -a2 * (dr * dr)));
+// which the fast column pass folds into the spectrum once per column; all
+// arguments pre-scaled (FieldsConst::sa / sb): the wrapped angle distance is
+// min(d, 2 pi - d) and the exponent -(d^2 + dr^2)
+R2_DEV float transfer_s(float lnr_s, float th_s, float ll_s, float ang_s, float two_pi_s) {
+  float d = fabsf(th_s - ang_s);
+  d = fminf(d, two_pi_s - d);
+  const float dr = lnr_s + ll_s;
+  return ex2(-fmaf(d, d, dr * dr));
 }
 
 // Per-filter multiply + inverse column FFT + store for one column (direct or
@@ -181,20 +190,20 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* G
   const float2* sp = Sc + (mir ? (N + N / 32) - t - ((t + 31) >> 5) : t + (t >> 5));
   const int sstep = mir ? -PS : PS;
   const float tsg = mir ? -1.f : 1.f;                     // theta_m = +-pi - theta
-  const float tpi = mir ? kPi : 0.f;
+  const float tpi = mir ? c.pi_s : 0.f;
   const float ysg = mir ? 1.f : -1.f;                     // conj for the direct column
-  const float a2 = c.a2, b2 = c.b2;
+  const float two_pi_s = c.two_pi_s;
   float2 v[32];
   for (int f = 0; f < F; ++f) {
     const int s = f / c.O, o = f % c.O;
-    const float ll = c.log_lambda[s], ang = c.ang[o];
+    const float ll = c.ll_s[s], ang = c.ang_s[o];
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
       const int ky = t + G * m;
       const float2 sv = sp[sstep * m];
       const float2 gq = Geo[ky];                         // (ln r, theta): one 8-byte load
       const float th = fmaf(tsg, gq.y, m < 16 ? tpi : -tpi);
-      const float gv = transfer_s(gq.x, th, ll, ang, a2, b2);
+      const float gv = transfer_s(gq.x, th, ll, ang, two_pi_s);
       // conj(spectrum * G) for the inverse; the mirror reads S(-ky, kx) = conj S(ky, W - kx)
       v[m] = __fmul2_rn(sv, make_float2(gv, gv * ysg));
     }
@@ -250,7 +259,7 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     for (int i = threadIdx.x; i < NS * N; i += ColsCfg<G>::T) {
       float lnr, L2, th;
       geometry(c, i % N, min(kx0 + i / N, Wh - 1), lnr, L2, th);
-      geo[i] = make_float2(lnr, th);
+      geo[i] = make_float2(lnr * c.sa, th * c.sb);
       // the radius-only factor lowpass / (H*W) goes into the spectrum (the
       // mirror column has the same radius); 0 at DC
       const int cc = i / N, ky = i % N;
@@ -274,10 +283,9 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
       else cols_filters<G>(c, Sc, Geo, buf, Qb, xo, t, mir != 0, sn);
       return;
     } else {
-    const float a2 = c.a2, b2 = c.b2;
     for (int f = 0; f < F; ++f) {
       const int s = f / c.O, o = f % c.O;
-      const float ll = c.log_lambda[s], ang = c.ang[o];
+      const float ll = c.ll_s[s], ang = c.ang_s[o];
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const int ky = t + G * m;
@@ -285,12 +293,12 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
         float2 sv;
         if (mir) {
           sv = Sc[pad32((N - ky) & (N - 1))];       // S(-ky, kx) = conj S(ky, W - kx)
-          th = (ky < N / 2 ? kPi : -kPi) - th;
+          th = (ky < N / 2 ? c.pi_s : -c.pi_s) - th;
         } else {
           sv = Sc[pad32(ky)];
           sv.y = -sv.y;
         }
-        const float gv = transfer_s(Geo[ky].x, th, ll, ang, a2, b2);
+        const float gv = transfer_s(Geo[ky].x, th, ll, ang, c.two_pi_s);
         v[m] = make_float2(sv.x * gv, sv.y * gv);   // conj(spectrum * G) for the inverse
       }
       fft_fast<G>(v, buf, c.tw_h, t, sw);
@@ -1088,8 +1096,15 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   for (int s = 0; s < c.S; ++s) c.log_lambda[s] = (float)bk.log_lambda[s];
   c.a2 = (float)(bk.inv_den_r * log2e);
   c.b2 = (float)(bk.inv_den_a * log2e);
+  const double sa = std::sqrt(bk.inv_den_r * log2e), sb = std::sqrt(bk.inv_den_a * log2e);
+  c.sa = (float)sa;
+  c.sb = (float)sb;
+  for (int q = 0; q < c.S; ++q) c.ll_s[q] = (float)(bk.log_lambda[q] * sa);
+  c.pi_s = (float)(M_PI * sb);
+  c.two_pi_s = (float)(2.0 * M_PI * sb);
   for (int q = 0; q < c.O; ++q) {
     c.ang[q] = (float)bk.angle[q];
+    c.ang_s[q] = (float)(bk.angle[q] * sb);
     c.cos_a[q] = (float)bk.cos_a[q];
     c.sin_a[q] = (float)bk.sin_a[q];
   }
