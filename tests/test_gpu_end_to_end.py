@@ -82,3 +82,27 @@ def test_rotation_sweep_agreement(r2, theta):
     common = set(dw) & set(dg)
     assert len(common) >= 0.99 * len(dw)
     assert np.mean([dw[k] == dg[k] for k in common]) >= 0.99
+
+
+@pytest.mark.parametrize("seed,theta", [(4, 30.0), (7, 200.0)])
+def test_recovered_affine_agrees(r2, seed, theta):
+    """north_star: "the recovered affine agrees to within 0.5 px RMSE".  The
+    host RANSAC + least-squares stage (paper_2303_00319_b200.affine, the same
+    code for both) on the GPU and on the oracle match sets of one pair, on a
+    pair the oracle registers (no speckle).  Affines are compared
+    as the RMSE of their action over a 16 x 16 lattice spanning the image."""
+    from paper_2303_00319_b200 import affine_rmse, estimate_affine, synth
+    a, b, truth = synth.make_pair(512, seed=seed, theta_deg=theta, looks=None)
+    a, b = a.astype(np.float64), b.astype(np.float64)
+    want, _ = _oracle_matches(a, b, 5000)
+    got, _ = _gpu_matches(r2, a, b, 5000)
+    fits = []
+    for m in (want, got):
+        pts = np.array(sorted(m), np.float64)              # ((xr, yr), (xt, yt)), a fixed order
+        A, inl = estimate_affine(pts[:, 0], pts[:, 1])
+        assert A is not None and inl.sum() >= 50
+        fits.append(A)
+    err = affine_rmse(fits[1], fits[0], 512)
+    print(f"seed {seed}: affine RMSE GPU vs oracle {err:.4f} px, GPU vs truth {affine_rmse(fits[1], truth.matrix, 512):.3f} px")
+    assert err <= 0.5
+    assert affine_rmse(fits[1], truth.matrix, 512) < 2.0

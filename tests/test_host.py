@@ -169,3 +169,28 @@ def test_container_errors(tmp_path):
         read_descriptors(p)                                  # unknown mode code
     with pytest.raises(ParameterError):
         write_descriptors(p, [Descriptor(v[:100], 0, 1, "plain")])
+
+
+# ---- host affine stage (north_star "recovered affine") -----------
+def test_estimate_affine_recovers_transform_with_outliers():
+    from paper_2303_00319_b200 import affine_rmse, estimate_affine, synth
+    rng = np.random.default_rng(3)
+    gt = synth.similarity(1024, 37.0, 1.05, (12.0, -7.0))
+    ref = rng.uniform(0, 1024, (3000, 2))
+    tgt = ref @ gt[:, :2].T + gt[:, 2] + rng.normal(0, 0.5, (3000, 2))
+    bad = rng.random(3000) < 0.6                       # 60 % gross outliers
+    tgt[bad] = rng.uniform(0, 1024, (int(bad.sum()), 2))
+    a, inl = estimate_affine(ref, tgt)
+    assert a is not None and affine_rmse(a, gt, 1024) < 0.2
+    assert inl[~bad].mean() > 0.95 and inl[bad].mean() < 0.01
+    a2, inl2 = estimate_affine(ref, tgt)               # deterministic for a seed
+    assert np.array_equal(a, a2) and np.array_equal(inl, inl2)
+
+
+def test_estimate_affine_degenerate_inputs():
+    from paper_2303_00319_b200 import ParameterError, estimate_affine, fit_affine
+    assert estimate_affine(np.zeros((2, 2)), np.zeros((2, 2)))[0] is None
+    line = np.stack([np.arange(10.0), np.arange(10.0)], 1)          # collinear: every sample singular
+    assert estimate_affine(line, line)[0] is None
+    with pytest.raises(ParameterError):
+        fit_affine(np.zeros((2, 2)), np.zeros((2, 2)))
