@@ -159,3 +159,31 @@ def test_c4_pair_runs_and_matches(eng):
     t = np.array([p[1] for p in res.matches.pairs])
     resid = np.linalg.norm(truth.apply(rx[r]) - tx[t], axis=1)
     assert (resid < 3).sum() >= 1000
+
+
+def test_batch_pipeline_non_square_matches_pair_api(eng):
+    """The batched throughput path (BatchPipeline, CUDA graphs) on a
+    non-square size gives, pair for pair, the same keypoints and matches as
+    the per-pair drop-in API."""
+    import paper_2303_00319_b200 as r2
+    from paper_2303_00319_b200 import synth
+    H, W = 512, 768
+    imgs = []
+    for seed in (1, 2):
+        a, b, _ = synth.make_pair(768, seed=seed, looks=None)
+        imgs += [a[128:640].astype(np.float32), b[128:640].astype(np.float32)]
+    batch = np.stack(imgs)
+    cfg = r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=2000)
+    pipe = r2.BatchPipeline(2, H, W, cfg)
+    pipe.load(batch)
+    pipe.capture()
+    pipe.step()
+    torch.cuda.synchronize()
+    for p, (ri, ti, dist) in enumerate(pipe.matches_host()):
+        res = r2.match_pair(batch[2 * p].astype(np.float64), batch[2 * p + 1].astype(np.float64), cfg)
+        kr = pipe.keypoints_host(2 * p)
+        assert np.array_equal(kr["x"], [k.x for k in res.ref.keypoints])
+        assert np.array_equal(kr["y"], [k.y for k in res.ref.keypoints])
+        want = np.array([(r, t) for r, t, _ in res.matches.pairs]).reshape(-1, 2)
+        assert len(want) > 50 and np.array_equal(np.stack([ri, ti], 1), want)
+        assert np.array_equal(dist, [d for _, _, d in res.matches.pairs])
