@@ -178,7 +178,7 @@ class BatchPipeline:
         s = torch.cuda.Stream()
         side = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        graphs = []
+        graphs, feats = [], []
         with torch.cuda.stream(s):
             for p in (0, 1):
                 g = torch.cuda.CUDAGraph()
@@ -189,9 +189,16 @@ class BatchPipeline:
                     self.run_fields(imgs[p], fbuf[p], "p_")
                     s.wait_stream(side)
                 graphs.append(g)
+            # drain steps: the features of the last batch alone, on either buffer
+            for p in (0, 1):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self.run_features(fbuf[p], "p_")
+                feats.append(g)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         self.graphs["pipe"] = tuple(graphs)
+        self.graphs["pipe_features"] = tuple(feats)
         return self
 
     def pipelined_step(self, parity: int):
@@ -200,9 +207,10 @@ class BatchPipeline:
     def run_from_host_pipelined(self, host_images, steps: int, host_out: dict | None = None):
         """As run_from_host, pipelined: step i uploads batch i+1 on the copy
         stream, runs the filter bank of batch i next to the features of batch
-        i-1, and copies batch i-1's match arrays back.  A priming step (the
-        filter bank of batch 0) precedes the loop; the caller times `steps`
-        steps, each of which completes one batch.  Enqueues only."""
+        i-1, and copies batch i-1's match arrays back.  The first step is the
+        filter bank of batch 0 alone and the last the features of batch
+        steps-1 alone, so `steps` batches are processed with no other work.
+        Enqueues only."""
         if "pipe" not in (self.graphs or {}):
             self.capture_pipelined()
         if not isinstance(host_images, (list, tuple)):
@@ -218,14 +226,20 @@ class BatchPipeline:
             ready[0].record(xs)
         for i in range(steps + 1):
             b = i % 2
-            if i + 1 <= steps:
+            if i + 1 < steps:
                 with torch.cuda.stream(xs):
                     if i >= 1:
                         xs.wait_event(done[1 - b])
                     bufs[1 - b].copy_(host_images[(i + 1) % len(host_images)], non_blocking=True)
                     ready[1 - b].record(xs)
-            cs.wait_event(ready[b])
-            self.pipelined_step(b)
+            if i < steps:
+                cs.wait_event(ready[b])
+            if i == 0:
+                self.graphs["fields"][0].replay()          # fields(images -> f): the fields half of pipe[0]
+            elif i == steps:
+                self.graphs["pipe_features"][1 - b].replay()
+            else:
+                self.pipelined_step(b)
             done[b].record(cs)
             if i >= 1 and host_out is not None:            # batch i-1 is complete
                 for k, t in host_out.items():

@@ -254,3 +254,31 @@ def test_estimator_front_end(r2, pair512):
     assert np.array_equal(both[0], want) and len(both[1]) > 0
     feats = r2.RiftFeatureExtractor(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=1500).fit_transform([a, b])
     assert len(feats) == 2 and len(feats[0].keypoints) == len(rk) and len(feats[1].descriptors) == len(res.tgt.descriptors)
+
+
+def test_run_from_host_pipelined_results(r2):
+    """The end-to-end host path (double-buffered uploads, fields-only first
+    step, features-only last step): after `steps` steps the pinned output
+    holds the matches of batch steps-1, equal to the plain step's."""
+    from paper_2303_00319_b200 import synth
+    cfg = r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=800)
+    batches = [synth.make_batch(2, 256, seed0=s)[0] for s in (30, 40, 50)]
+    pipe = r2.BatchPipeline(2, 256, 256, cfg)
+    want = []
+    for imgs in batches:
+        pipe.load(imgs)
+        pipe.step()
+        torch.cuda.synchronize()
+        want.append({k: v.clone().cpu() for k, v in pipe.m.items()})
+    host = [torch.from_numpy(b).pin_memory() for b in batches]
+    out = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in pipe.m.items()}
+    for steps in (1, 2, 3):
+        for t in out.values():
+            t.zero_()
+        pipe.run_from_host_pipelined(host, steps, out)
+        torch.cuda.synchronize()
+        w = want[steps - 1]
+        assert torch.equal(w["count"], out["count"]), steps
+        for p, n in enumerate(w["count"].tolist()):            # rows past count are stale workspace
+            for k in ("ref", "tgt", "dist"):
+                assert torch.equal(w[k][p, :n], out[k][p, :n]), (steps, p, k)
