@@ -687,6 +687,15 @@ struct PcShape {
   static constexpr int PIX = G == 0 ? 16 : (G >= 64 ? 8 : (G >= 4 ? G / 4 : 1));
 };
 
+#ifndef R2_PC_PREFETCH
+#define R2_PC_PREFETCH 1
+#endif
+constexpr bool kPcPrefetch = R2_PC_PREFETCH;
+// bulk L2 prefetch of `bytes` (multiple of 16) from a 16-byte aligned address
+R2_DEV void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+
 R2_DEV float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -825,6 +834,21 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
         }
       }
       __syncthreads();
+      // prefetch the next stage's inputs into L2 while this stage's pixel
+      // phase runs: its Q row tiles (4 rows x W, contiguous) and R0 rows
+      if (G > 0 && kPcPrefetch && threadIdx.x == 0 && o0 + ops < O) {
+        const int o1 = o0 + ops, n1 = min(ops, O - o1);
+        for (int r = 0; r < rr; r += 4 - ((y0 + rbase + r) & 3)) {
+          const int y = y0 + rbase + r;
+          if (y >= H) break;
+          for (int oo = 0; oo < n1; ++oo)
+            for (int s = 1; s < S; ++s)
+              l2_prefetch(Qb + ((size_t)(s * O + o1 + oo) * c.Hp + (y & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
+        }
+        for (int oo = 0; oo < n1; ++oo)
+          l2_prefetch(Rb + ((size_t)(o1 + oo) * H + y0 + rbase) * W,
+                      (unsigned)(min(rr, H - (y0 + rbase)) * W * sizeof(float2)));
+      }
       // --- per-pixel phase congruency for the orientations of this stage
       for (int oo = 0; oo < no; ++oo) {
         const int o = o0 + oo;
