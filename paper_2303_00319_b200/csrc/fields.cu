@@ -362,6 +362,10 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
 // Scale-0 responses of orientation blockIdx.y for a block of rows: written
 // out (for K3b) with |response| and a 4096-bin histogram of its float bits
 // (radix-select level 1 of the median).
+// bulk L2 prefetch of `bytes` (multiple of 16) from a 16-byte aligned address
+R2_DEV void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
 R2_DEV float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -386,7 +390,11 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
     const int g = threadIdx.x / G, t = threadIdx.x % G;
     float2* buf = sm + g * PL;
     // kAmpRows row groups per CTA amortise the histogram zero / flush
-    for (int y = blockIdx.x * NG * kAmpRows + g; y < min(H, (blockIdx.x + 1) * NG * kAmpRows); y += NG) {
+    const int yend = min(H, (blockIdx.x + 1) * NG * kAmpRows);
+    for (int y = blockIdx.x * NG * kAmpRows + g; y < yend; y += NG) {
+      if (threadIdx.x == 0)                       // the next row group's Q tiles into L2
+        for (int yt = (y + NG) & ~3; yt < min(yend, y + 2 * NG); yt += 4)
+          l2_prefetch(Qp + (size_t)yt * W, (unsigned)(4 * W * sizeof(float2)));
       float2 v[32];
 #pragma unroll
       for (int m = 0; m < 32; ++m) v[m] = cconj(Qp[tq(y, t + G * m, W)]);
@@ -691,10 +699,6 @@ struct PcShape {
 #define R2_PC_PREFETCH 1
 #endif
 constexpr bool kPcPrefetch = R2_PC_PREFETCH;
-// bulk L2 prefetch of `bytes` (multiple of 16) from a 16-byte aligned address
-R2_DEV void l2_prefetch(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
-}
 
 R2_DEV float rcp_approx(float x) {
   float y;
@@ -784,6 +788,21 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
     for (int i = 0; i < PIX; ++i) { acc_a[i] = acc_b[i] = acc_c[i] = 0.f; best[i] = -1.f; bidx[i] = 1; }
     for (int o0 = 0; o0 < O; o0 += ops) {
       const int no = min(ops, O - o0);
+      // prefetch the next stage's inputs into L2 while this stage runs: its
+      // Q row tiles (4 rows x W, contiguous) and R0 rows
+      if (G > 0 && kPcPrefetch && threadIdx.x == 0 && o0 + ops < O) {
+        const int o1 = o0 + ops, n1 = min(ops, O - o1);
+        for (int r = 0; r < rr; r += 4 - ((y0 + rbase + r) & 3)) {
+          const int y = y0 + rbase + r;
+          if (y >= H) break;
+          for (int oo = 0; oo < n1; ++oo)
+            for (int s = 1; s < S; ++s)
+              l2_prefetch(Qb + ((size_t)(s * O + o1 + oo) * c.Hp + (y & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
+        }
+        for (int oo = 0; oo < n1; ++oo)
+          l2_prefetch(Rb + ((size_t)(o1 + oo) * H + y0 + rbase) * W,
+                      (unsigned)(min(rr, H - (y0 + rbase)) * W * sizeof(float2)));
+      }
       if constexpr (G > 0) {
         constexpr int NG = TPC / G;
         const int g = threadIdx.x / G, t = threadIdx.x % G;
@@ -834,21 +853,6 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
         }
       }
       __syncthreads();
-      // prefetch the next stage's inputs into L2 while this stage's pixel
-      // phase runs: its Q row tiles (4 rows x W, contiguous) and R0 rows
-      if (G > 0 && kPcPrefetch && threadIdx.x == 0 && o0 + ops < O) {
-        const int o1 = o0 + ops, n1 = min(ops, O - o1);
-        for (int r = 0; r < rr; r += 4 - ((y0 + rbase + r) & 3)) {
-          const int y = y0 + rbase + r;
-          if (y >= H) break;
-          for (int oo = 0; oo < n1; ++oo)
-            for (int s = 1; s < S; ++s)
-              l2_prefetch(Qb + ((size_t)(s * O + o1 + oo) * c.Hp + (y & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
-        }
-        for (int oo = 0; oo < n1; ++oo)
-          l2_prefetch(Rb + ((size_t)(o1 + oo) * H + y0 + rbase) * W,
-                      (unsigned)(min(rr, H - (y0 + rbase)) * W * sizeof(float2)));
-      }
       // --- per-pixel phase congruency for the orientations of this stage
       for (int oo = 0; oo < no; ++oo) {
         const int o = o0 + oo;
