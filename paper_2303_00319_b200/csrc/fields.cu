@@ -374,7 +374,7 @@ R2_DEV float sqrt_approx(float x) {
 template <int G>
 __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict__ Q, float2* __restrict__ R0,
                                                         float* __restrict__ amp0, unsigned* __restrict__ hist,
-                                                        const __grid_constant__ FieldsConst c) {
+                                                        const __grid_constant__ FieldsConst c, int ahead) {
   extern __shared__ float2 sm[];
   const int H = c.H, W = c.W, F = c.S * c.O;
   const int o = blockIdx.y, b = blockIdx.z;
@@ -392,9 +392,22 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
     // kAmpRows row groups per CTA amortise the histogram zero / flush
     const int yend = min(H, (blockIdx.x + 1) * NG * kAmpRows);
     for (int y = blockIdx.x * NG * kAmpRows + g; y < yend; y += NG) {
-      if (threadIdx.x == 0)                       // the next row group's Q tiles into L2
-        for (int yt = (y + NG) & ~3; yt < min(yend, y + 2 * NG); yt += 4)
-          l2_prefetch(Qp + (size_t)yt * W, (unsigned)(4 * W * sizeof(float2)));
+      if (threadIdx.x == 0) {
+        if (y + NG < yend) {                      // the next row group's Q tiles into L2
+          for (int yt = (y + NG) & ~3; yt < min(yend, y + 2 * NG); yt += 4)
+            l2_prefetch(Qp + (size_t)yt * W, (unsigned)(4 * W * sizeof(float2)));
+        } else if (ahead > 0) {                   // the first row group of the CTA `ahead` slots later
+          const long long lin = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x + ahead;
+          if (lin < (long long)gridDim.x * gridDim.y * gridDim.z) {
+            const int nx = (int)(lin % gridDim.x), no = (int)((lin / gridDim.x) % gridDim.y);
+            const int nbz = (int)(lin / ((long long)gridDim.x * gridDim.y));
+            const float2* nQ = Q + ((size_t)nbz * F + no) * c.Hp * W;
+            const int ny = nx * NG * kAmpRows;
+            for (int yt = ny & ~3; yt < min(H, ny + NG); yt += 4)
+              l2_prefetch(nQ + (size_t)yt * W, (unsigned)(4 * W * sizeof(float2)));
+          }
+        }
+      }
       float2 v[32];
 #pragma unroll
       for (int m = 0; m < 32; ++m) v[m] = cconj(Qp[tq(y, t + G * m, W)]);
@@ -762,7 +775,8 @@ R2_DEV void pc_pair(const float2* __restrict__ b0, const float2* __restrict__ b1
 template <int G, int SC>
 __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k_rows_pc(const float2* __restrict__ Q, const float2* __restrict__ R0,
                                                          const float* __restrict__ thr, PcOut out,
-                                                         const __grid_constant__ FieldsConst c, int rr, int ops) {
+                                                         const __grid_constant__ FieldsConst c, int rr, int ops,
+                                                         int ahead) {
   extern __shared__ float2 sm[];
   constexpr int SMAX = SC > 0 ? SC : kMaxS;
   const int H = c.H, O = c.O;
@@ -789,19 +803,37 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
     for (int o0 = 0; o0 < O; o0 += ops) {
       const int no = min(ops, O - o0);
       // prefetch the next stage's inputs into L2 while this stage runs: its
-      // Q row tiles (4 rows x W, contiguous) and R0 rows
-      if (G > 0 && kPcPrefetch && threadIdx.x == 0 && o0 + ops < O) {
-        const int o1 = o0 + ops, n1 = min(ops, O - o1);
-        for (int r = 0; r < rr; r += 4 - ((y0 + rbase + r) & 3)) {
-          const int y = y0 + rbase + r;
-          if (y >= H) break;
-          for (int oo = 0; oo < n1; ++oo)
-            for (int s = 1; s < S; ++s)
-              l2_prefetch(Qb + ((size_t)(s * O + o1 + oo) * c.Hp + (y & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
+      // Q row tiles (4 rows x W, contiguous) and R0 rows.  After the last
+      // stage comes the first stage of the CTA `ahead` positions later in
+      // launch order -- about the one that takes a slot when this CTA ends
+      // (L2 is shared, so which SM runs it does not matter)
+      if (G > 0 && kPcPrefetch && threadIdx.x == 0) {
+        int pb = b, py = y0 + rbase, o1 = o0 + ops;
+        bool go = o1 < O;
+        if (!go && rbase + rr < 2 && y0 + rbase + rr < H) { py = y0 + rbase + rr; o1 = 0; go = true; }
+        else if (!go && rbase + rr >= 2) {
+          const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + ahead;
+          if (ahead > 0 && lin < (long long)gridDim.x * gridDim.y) {
+            pb = (int)(lin / gridDim.x);
+            py = 2 * (int)(lin % gridDim.x);
+            o1 = 0;
+            go = py < H;
+          }
         }
-        for (int oo = 0; oo < n1; ++oo)
-          l2_prefetch(Rb + ((size_t)(o1 + oo) * H + y0 + rbase) * W,
-                      (unsigned)(min(rr, H - (y0 + rbase)) * W * sizeof(float2)));
+        if (go) {
+          const int n1 = min(ops, O - o1);
+          const float2* pQ = Q + (size_t)pb * F * c.Hp * W;
+          const float2* pR = R0 + (size_t)pb * O * H * W;
+          for (int r = 0; r < rr; r += 4 - ((py + r) & 3)) {
+            const int y = py + r;
+            if (y >= H) break;
+            for (int oo = 0; oo < n1; ++oo)
+              for (int s = 1; s < S; ++s)
+                l2_prefetch(pQ + ((size_t)(s * O + o1 + oo) * c.Hp + (y & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
+          }
+          for (int oo = 0; oo < n1; ++oo)
+            l2_prefetch(pR + ((size_t)(o1 + oo) * H + py) * W, (unsigned)(min(rr, H - py) * W * sizeof(float2)));
+        }
       }
       if constexpr (G > 0) {
         constexpr int NG = TPC / G;
@@ -1063,7 +1095,11 @@ static cudaError_t launch_amp0(const float2* Q, float2* R0, float* amp0, unsigne
   }
   cudaError_t e = set_smem(k_rows_amp0<G>, smem);
   if (e != cudaSuccess) return e;
-  k_rows_amp0<G><<<grid, kThreads, smem, st>>>(Q, R0, amp0, hist, c);
+  int per_sm = 0, dev = 0, n_sm = 0;                // resident CTA slots: the prefetch look-ahead
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_amp0<G>, kThreads, smem);
+  k_rows_amp0<G><<<grid, kThreads, smem, st>>>(Q, R0, amp0, hist, c, per_sm * n_sm);
   return cudaPeekAtLastError();
 }
 
@@ -1090,7 +1126,11 @@ static cudaError_t launch_pc_s(const float2* Q, const float2* R0, const float* t
   cudaError_t e = set_smem(k_rows_pc<G, SC>, smem);
   if (e != cudaSuccess) return e;
   dim3 grid((c.H + 1) / 2, c.B);
-  k_rows_pc<G, SC><<<grid, PcShape<G>::T, smem, st>>>(Q, R0, thr, out, c, rr, ops);
+  int per_sm = 0, dev = 0, n_sm = 0;                // resident CTA slots: the prefetch look-ahead
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_pc<G, SC>, PcShape<G>::T, smem);
+  k_rows_pc<G, SC><<<grid, PcShape<G>::T, smem, st>>>(Q, R0, thr, out, c, rr, ops, per_sm * n_sm);
   return cudaPeekAtLastError();
 }
 
