@@ -154,16 +154,30 @@ template <> struct DFT<5> {
 // ---- fast path --------------------------------------------------------------
 
 // Twiddle r = 1..R-1 inputs of one butterfly by W_N^{r*e}, e = k*step.
-// Powers come from a short recurrence refreshed from the table every 8 steps.
+// Powers come from a short recurrence refreshed from the table every 8
+// steps.  The table values a butterfly needs (W^e and W^{8qe}) are loaded
+// by tw_load before the pass's exchange, so their latency overlaps it.
+template <int R>
+struct TwPre {
+  float2 w[(R + 7) / 8];   // [0] = W^e, [q] = W^{8qe}
+};
 template <int R, int N>
-R2_DEV void apply_twiddles(float2* v, const float2* __restrict__ tw, int e) {
+R2_DEV TwPre<R> tw_load(const float2* __restrict__ tw, int e) {
+  TwPre<R> p;
+  p.w[0] = __ldg(&tw[e]);
+#pragma unroll
+  for (int q = 1; q < (R + 7) / 8; ++q) p.w[q] = __ldg(&tw[(8 * q * e) & (N - 1)]);
+  return p;
+}
+template <int R>
+R2_DEV void apply_twiddles(float2* v, const TwPre<R>& p, int e) {
   if (e == 0) return;
-  float2 base = __ldg(&tw[e]);
+  const float2 base = p.w[0];
   float2 w = base;
 #pragma unroll
   for (int r = 1; r < R; ++r) {
     if (r > 1) {
-      if ((r & 7) == 0) w = __ldg(&tw[(r * e) & (N - 1)]);
+      if ((r & 7) == 0) w = p.w[r / 8];
       else w = cmul(w, base);
     }
     v[r] = cmul(v[r], w);
@@ -176,6 +190,9 @@ R2_DEV void apply_twiddles(float2* v, const float2* __restrict__ tw, int e) {
 template <int G, int R, int NS, bool LAST, class Sync>
 R2_DEV void stockham_pass(float2 (&v)[32], float2* buf, const float2* __restrict__ tw, int t, Sync& sync) {
   constexpr int N = 32 * G, PER = 32 / R, NR = N / R, STEP = N / (NS * R);
+  TwPre<R> pre[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) pre[i] = tw_load<R, N>(tw, ((t + G * i) & (NS - 1)) * STEP);
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int j = t + G * i;
@@ -187,7 +204,7 @@ R2_DEV void stockham_pass(float2 (&v)[32], float2* buf, const float2* __restrict
   for (int i = 0; i < PER; ++i) {
     const int j = t + G * i;
     const int k = j & (NS - 1);
-    apply_twiddles<R, N>(&v[i * R], tw, k * STEP);
+    apply_twiddles<R>(&v[i * R], pre[i], k * STEP);
     DFT<R>::run(&v[i * R]);
   }
   if constexpr (!LAST) {
