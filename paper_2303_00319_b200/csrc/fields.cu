@@ -70,7 +70,15 @@ R2_DEV float fftfreq(int k, int n) { return (float)(k < (n + 1) / 2 ? k : k - n)
 
 // 4-row column-tile plane index: a 32-byte sector holds rows 4j..4j+3 of one
 // column, so a column FFT's stores fill whole sectors
-R2_DEV size_t tq(int y, int x, int W) { return ((size_t)(y >> 2) * W + x) * 4 + (y & 3); }
+#ifndef R2_QT
+#define R2_QT 4
+#endif
+// rows per column tile: 4 makes every k_cols store instruction write whole
+// 32-byte sectors; 2 would halve the row kernels' L1 wavefronts
+// (rows_pc -15 %, amp0 -13 % measured) but k_cols's half-sector stores then
+// force DRAM fill reads (k_cols 2.3 -> 9.3 ms) -- see DESIGN 7b
+constexpr int kQT = R2_QT;
+R2_DEV size_t tq(int y, int x, int W) { return ((size_t)(y / kQT) * W + x) * kQT + (y % kQT); }
 
 R2_DEV float ex2(float x) {
   float y;
@@ -213,7 +221,7 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* G
     // addresses across the loop (register spills)
     int wv;
     asm volatile("mov.b32 %0, %1;" : "=r"(wv) : "r"(W));
-    float2* q = Qb + (size_t)f * c.Hp * wv + ((size_t)(t >> 2) * wv + xo) * 4 + (t & 3);
+    float2* q = Qb + (size_t)f * c.Hp * wv + ((size_t)(t / kQT) * wv + xo) * kQT + (t % kQT);
     const size_t step = (size_t)G * wv;           // (G / 4) tile rows of 4 W elements
 #pragma unroll
     for (int m = 0; m < 32; ++m) q[m * step] = cconj(v[m]);
@@ -394,8 +402,8 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
     for (int y = blockIdx.x * NG * kAmpRows + g; y < yend; y += NG) {
       if (threadIdx.x == 0) {
         if (y + NG < yend) {                      // the next row group's Q tiles into L2
-          for (int yt = (y + NG) & ~3; yt < min(yend, y + 2 * NG); yt += 4)
-            l2_prefetch(Qp + (size_t)yt * W, (unsigned)(4 * W * sizeof(float2)));
+          for (int yt = (y + NG) & ~(kQT - 1); yt < min(yend, y + 2 * NG); yt += kQT)
+            l2_prefetch(Qp + (size_t)yt * W, (unsigned)(kQT * W * sizeof(float2)));
         } else if (ahead > 0) {                   // the first row group of the CTA `ahead` slots later
           const long long lin = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x + ahead;
           if (lin < (long long)gridDim.x * gridDim.y * gridDim.z) {
@@ -403,8 +411,8 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
             const int nbz = (int)(lin / ((long long)gridDim.x * gridDim.y));
             const float2* nQ = Q + ((size_t)nbz * F + no) * c.Hp * W;
             const int ny = nx * NG * kAmpRows;
-            for (int yt = ny & ~3; yt < min(H, ny + NG); yt += 4)
-              l2_prefetch(nQ + (size_t)yt * W, (unsigned)(4 * W * sizeof(float2)));
+            for (int yt = ny & ~(kQT - 1); yt < min(H, ny + NG); yt += kQT)
+              l2_prefetch(nQ + (size_t)yt * W, (unsigned)(kQT * W * sizeof(float2)));
           }
         }
       }
@@ -824,12 +832,13 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
           const int n1 = min(ops, O - o1);
           const float2* pQ = Q + (size_t)pb * F * c.Hp * W;
           const float2* pR = R0 + (size_t)pb * O * H * W;
-          for (int r = 0; r < rr; r += 4 - ((py + r) & 3)) {
+          for (int r = 0; r < rr; r += kQT - ((py + r) & (kQT - 1))) {
             const int y = py + r;
             if (y >= H) break;
             for (int oo = 0; oo < n1; ++oo)
               for (int s = 1; s < S; ++s)
-                l2_prefetch(pQ + ((size_t)(s * O + o1 + oo) * c.Hp + (y & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
+                l2_prefetch(pQ + ((size_t)(s * O + o1 + oo) * c.Hp + (y & ~(kQT - 1))) * W,
+                            (unsigned)(kQT * W * sizeof(float2)));
           }
           for (int oo = 0; oo < n1; ++oo)
             l2_prefetch(pR + ((size_t)(o1 + oo) * H + py) * W, (unsigned)(min(rr, H - py) * W * sizeof(float2)));
