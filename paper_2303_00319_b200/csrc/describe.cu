@@ -128,7 +128,8 @@ R2_DEV void widen(uint32_t acc, uint32_t& e, uint32_t& o) {
 // reduce the 4 threads of a cell, write its O counts and add their squares
 // to the descriptor's squared norm (recode only permutes bins)
 template <int OT>
-R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int O_rt, int* sq) {
+R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int O_rt, int* sq,
+                        unsigned* hist = nullptr) {
   const int O = OT ? OT : O_rt;
   e += __shfl_xor_sync(0xffffffffu, e, 1);
   o += __shfl_xor_sync(0xffffffffu, o, 1);
@@ -142,6 +143,7 @@ R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int 
       const unsigned n = (((v & 1) ? o : e) >> (10 * (v >> 1))) & 1023u;
       out[v] = n;
       q += (int)(n * n);
+      if (hist && n) atomicAdd(&hist[v], n);      // the patch histogram (axis patch only)
     }
     atomicAdd(sq, q);
   }
@@ -159,7 +161,7 @@ R2_DEV uint32_t one_hot(uint32_t s) {
 // axis-aligned patch: thread = (cell, quarter); 4 columns x CS rows per thread.
 // OT / GT: orientation count and grid fixed at compile time (0 = runtime)
 template <int CS, int OT, int GT>
-R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsigned* cnt, int* sq) {
+R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsigned* cnt, int* sq, unsigned* hist) {
   const int tpc = CS / 4;                       // threads per cell
   const int g = GT ? GT : c.g, O = OT ? OT : c.O;
   const int t = threadIdx.x;
@@ -180,7 +182,7 @@ R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsign
       if (r % 7 == 6 || r == CS - 1) { widen(acc, e, o); acc = 0; }   // 4 samples/row: <= 28 per field
     }
   }
-  reduce_cell<OT>(e, o, on && sub == 0, cnt + cell * O, O, sq);
+  reduce_cell<OT>(e, o, on && sub == 0, cnt + cell * O, O, sq, hist);
 }
 
 // rotated patch of angle table t: sample (i, j) at ctr + t[i*P + j]
@@ -256,7 +258,8 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   const int O = OT ? OT : c.O, cells = GT ? GT * GT : c.cells;
   unsigned* cnt = s_dyn + (c.rows * c.stride) / 4;
   unsigned* cnt_rot[2] = {cnt + cells * O, cnt + 2 * cells * O};
-  __shared__ int s_pick[16], s_np, s_sq[3];
+  __shared__ int s_sq[3];
+  __shared__ unsigned s_hist[8];                  // axis-patch histogram (ref: mim.py:58-66)
   const int b = blockIdx.y, k = blockIdx.x;
   const size_t slot0 = ((size_t)b * a.kp_stride + k) * c.per;
   int* meta = slot_meta + slot0 * 3;              // (valid, variant, sqnorm) per slot
@@ -287,6 +290,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
       mbar_expect_tx(&s_bar, (uint32_t)(c.rows * c.stride));
       tma_load_2d(sw, &tmap, ax0, b * c.H + y - c.R, &s_bar);
     }
+    if (threadIdx.x < 8) s_hist[threadIdx.x] = 0;
     if (threadIdx.x == 0) { s_sq[0] = 0; s_sq[1] = 0; s_sq[2] = 0; }
     __syncthreads();
     mbar_wait(&s_bar, 0);
@@ -330,67 +334,71 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
       sw[r * wpr + wq] = v;
     }
   }
+  if (!c.tma && threadIdx.x < 8) s_hist[threadIdx.x] = 0;
   if (!c.tma && threadIdx.x == 0) { s_sq[0] = 0; s_sq[1] = 0; s_sq[2] = 0; }
   __syncthreads();
   const int bx = x - ax0;                         // keypoint column within a staged row
   const uint8_t* ctr = sreg + c.R * c.stride + bx;   // keypoint pixel
   // ---- axis-aligned patch
-  count_axis<CS, OT, GT>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt, &s_sq[0]);
+  count_axis<CS, OT, GT>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt, &s_sq[0], s_hist);
   __syncthreads();
-  // ---- dominant index / runner-up (ref: mim.py:69-91)
-  if (threadIdx.x < 32) {
-    unsigned hs[16];
-    for (int v = 0; v < O; ++v) {
-      unsigned s = 0;
-      for (int q = threadIdx.x; q < cells; q += 32) s += cnt[q * O + v];
+  // ---- dominant index / runner-up (ref: mim.py:69-91), computed by every
+  // thread from the 6-bin patch histogram (no extra barrier)
+  constexpr int kMaxPick = OT ? (OT > 2 ? OT : 2) : 8;
+  int pick[kMaxPick];
+  int np = 0;
+  {
+    unsigned hs[8];
 #pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      hs[v] = s;
-    }
-    if (threadIdx.x == 0) {
-      int np = 0, skip = 0;
-      if (c.mode == 0) { s_pick[np++] = 1; }
-      else if (c.mode == 1) { for (int v = 1; v <= O; ++v) s_pick[np++] = v; }
-      else {
-        // first argmax; runner-up if >= ratio * peak (float64, inclusive);
-        // runner-up ties go to the bin cyclically closest after the peak
-        int pk = 0;
-        for (int v = 1; v < O; ++v) if (hs[v] > hs[pk]) pk = v;
-        double rv = -1.0;
-        for (int v = 0; v < O; ++v) if (v != pk && (double)hs[v] > rv) rv = (double)hs[v];
-        int picks[2] = {pk + 1, 0}, cand = 1;
-        if (rv >= c.ratio * (double)hs[pk]) {
-          int best = -1, bestd = 1 << 30;
-          for (int v = 0; v < O; ++v) {
-            if (v == pk || (double)hs[v] != rv) continue;
-            const int d = ((v - pk) % O + O) % O;
-            if (d < bestd) { bestd = d; best = v; }
-          }
-          picks[1] = best + 1;
-          cand = 2;
+    for (int v = 0; v < 8; ++v) hs[v] = v < O ? s_hist[v] : 0u;
+    int skip = 0;
+    if (c.mode == 0) { pick[np++] = 1; }
+    else if (c.mode == 1) {
+#pragma unroll
+      for (int v = 1; v <= kMaxPick; ++v) if (v <= O) pick[np++] = v;
+    } else {
+      // first argmax; runner-up if >= ratio * peak (float64, inclusive);
+      // runner-up ties go to the bin cyclically closest after the peak
+      int pk = 0;
+#pragma unroll
+      for (int v = 1; v < 8; ++v) if (v < O && hs[v] > hs[pk]) pk = v;
+      double rv = -1.0;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) if (v < O && v != pk && (double)hs[v] > rv) rv = (double)hs[v];
+      int picks[2] = {pk + 1, 0}, cand = 1;
+      if (rv >= c.ratio * (double)hs[pk]) {
+        int best = -1, bestd = 1 << 30;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          if (v >= O || v == pk || (double)hs[v] != rv) continue;
+          const int d = v > pk ? v - pk : v - pk + O;
+          if (d < bestd) { bestd = d; best = v; }
         }
-        for (int q = 0; q < cand; ++q) {
-          const int dom = picks[q];
-          if (c.rotate && dom != 1) {
-            const int4 bb = c.bbox[dom - 1];
-            if (x + bb.x < 0 || x + bb.y >= c.W || y + bb.z < 0 || y + bb.w >= c.H) { ++skip; continue; }
-          }
-          s_pick[np++] = dom;
-        }
+        picks[1] = best + 1;
+        cand = 2;
       }
-      s_np = np;
-      kp_skip[(size_t)b * a.kp_stride + k] = skip;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q >= cand) break;
+        const int dom = picks[q];
+        if (c.rotate && dom != 1) {
+          const int4 bb = c.bbox[dom - 1];
+          if (x + bb.x < 0 || x + bb.y >= c.W || y + bb.z < 0 || y + bb.w >= c.H) { ++skip; continue; }
+        }
+        pick[np++] = dom;
+      }
     }
+    if (threadIdx.x == 0) kp_skip[(size_t)b * a.kp_stride + k] = skip;
   }
-  __syncthreads();
-  const int np = s_np;
   // one phase: axis-patch rows are emitted from `cnt` while the rotated picks
   // (at most two) are counted into their own buffers; then one barrier
   const bool rot_mode = c.mode == 2 && c.rotate;
   int nrot = 0;
   const int dom90 = (O % 2 == 0 && c.P % 2 == 0) ? O / 2 + 1 : -1;
-  for (int q = 0; q < np; ++q) {
-    const int dom = s_pick[q];
+#pragma unroll
+  for (int q = 0; q < kMaxPick; ++q) {
+    if (q >= np) break;
+    const int dom = pick[q];
     if (rot_mode && dom == dom90) {
       emit_row_rot90<OT, GT>(a, c, cnt, dom, slot_rows + (slot0 + q) * a.stride);
       if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[0]; }
@@ -406,8 +414,10 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   if (nrot > 0) {
     __syncthreads();
     int r = 0;
-    for (int q = 0; q < np; ++q) {
-      const int dom = s_pick[q];
+#pragma unroll
+    for (int q = 0; q < kMaxPick; ++q) {
+      if (q >= np) break;
+      const int dom = pick[q];
       if (!(rot_mode && dom != 1 && dom != dom90)) continue;
       emit_row<OT, GT>(a, c, cnt_rot[r], dom, slot_rows + (slot0 + q) * a.stride);
       if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[1 + r]; }
