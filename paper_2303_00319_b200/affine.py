@@ -4,9 +4,9 @@ north_star: "the mutual/ratio checks and the FSC/RANSAC outlier stage stay
 on the host" and "the recovered affine agrees to within 0.5 px RMSE".  The
 reference ships no estimator (SURVEY D2: ref matcher.py:4-6, SPEC.md:12,429;
 parity unpinned), so this is the builder's host stage.  It is applied
-identically to GPU and oracle match sets: seeded RANSAC over minimal 3-point
-samples (vectorised over hypotheses), then least-squares refits on the
-inliers until the inlier set stops changing.
+identically to the GPU and the CPU-reference match sets: seeded RANSAC over
+minimal 3-point samples (vectorised over hypotheses), then least-squares
+refits on the inliers until the inlier set stops changing.
 """
 
 from __future__ import annotations
