@@ -81,8 +81,8 @@ class BatchPipeline:
         self.run_fields()
         self.run_features()
 
-    # our kernels per step: fields 9 + detect 10 + describe 3 + match 7
-    KERNELS_PER_STEP = 29
+    # our kernels per step: fields 9 + detect 10 + describe 1 + match 7
+    KERNELS_PER_STEP = 27
 
     # ---- graphs ------------------------------------------------------------
     def capture(self):

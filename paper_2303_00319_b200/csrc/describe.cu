@@ -17,12 +17,13 @@
 //                0xFF outside the image), so a sample counts as
 //                acc += 1 << s into six 5-bit fields.  Four threads share a
 //                cell (4 columns x cs rows each) and reduce with two shuffles.
-//                Then dominant index / runner-up, the rotated patch of each
-//                pick through a host-built int16 offset table, recode (a
-//                per-cell permutation) and a write into the fixed slot
-//                keypoint * per + pick.
-//   k_desc_scan  per image: exclusive scan of the slot valid flags
-//   k_desc_copy  order-preserving compaction of the slots
+//                Then dominant index / runner-up (every thread, from the
+//                patch histogram), the rotated patch of each pick through a
+//                host-built offset table, recode (a per-cell permutation), and
+//                the rows written straight to their final, reference-ordered
+//                slots: CTAs take keypoints in start order and find their
+//                output offset by a decoupled look-back over the descriptor
+//                counts the earlier keypoints publish.
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
@@ -245,10 +246,21 @@ R2_DEV void emit_row_rot90(const DescribeArgs& a, const DescConst& c, const unsi
   }
 }
 
+// decoupled look-back words: status in bits 63..62 (0 = not yet, 1 = this
+// keypoint's descriptor count, 2 = inclusive prefix), value in bits 31..0
+constexpr unsigned long long kChainAgg = 1, kChainPrefix = 2;
+R2_DEV void chain_publish(unsigned long long* w, unsigned long long status, unsigned v) {
+  atomicExch(w, (status << 62) | v);
+}
+R2_DEV unsigned long long chain_read(const unsigned long long* w) {
+  return *reinterpret_cast<const volatile unsigned long long*>(w);
+}
+
 template <int CS, int OT, int GT>
 __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ mim, DescribeArgs a,
-                                                  DescConst c, GatherTables tab, __half* __restrict__ slot_rows,
-                                                  int* __restrict__ slot_meta, int* __restrict__ kp_skip) {
+                                                  DescConst c, GatherTables tab,
+                                                  unsigned long long* __restrict__ chain,
+                                                  unsigned* __restrict__ ticket) {
   extern __shared__ __align__(128) uint32_t s_raw[];
   __shared__ uint64_t s_bar;
   // staged bytes (c.rows x c.stride, 128-byte aligned for the TMA box), then cnt
@@ -260,15 +272,24 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   unsigned* cnt_rot[2] = {cnt + cells * O, cnt + 2 * cells * O};
   __shared__ int s_sq[3];
   __shared__ unsigned s_hist[8];                  // axis-patch histogram (ref: mim.py:58-66)
-  const int b = blockIdx.y, k = blockIdx.x;
-  const size_t slot0 = ((size_t)b * a.kp_stride + k) * c.per;
-  int* meta = slot_meta + slot0 * 3;              // (valid, variant, sqnorm) per slot
-  if (k >= a.kp_count[b]) return;                 // k_desc_scan only reads live keypoints
+  __shared__ int s_k;
+  __shared__ unsigned s_excl;
+  const int b = blockIdx.y;
+  // keypoints are taken in CTA start order (a per-image ticket), so every
+  // keypoint before this one belongs to a CTA that has already started: the
+  // look-back below only waits on running CTAs
+  if (threadIdx.x == 0) s_k = (int)atomicAdd(&ticket[b], 1u);
+  __syncthreads();
+  const int k = s_k;
+  if (k >= a.kp_count[b]) return;                 // no live keypoint follows
+  unsigned long long* lb = chain + (size_t)b * a.kp_stride;
   const int x = a.kp_x[(size_t)b * a.kp_stride + k], y = a.kp_y[(size_t)b * a.kp_stride + k];
   const int x0 = x + 1 - (c.P + 1) / 2, y0 = y + 1 - (c.P + 1) / 2;   // floor(kp + 1 - P/2)
   if (x0 < 0 || y0 < 0 || x0 + c.P > c.W || y0 + c.P > c.H) {
-    for (int q = threadIdx.x; q < c.per; q += kT) meta[3 * q] = 0;
-    if (threadIdx.x == 0) kp_skip[(size_t)b * a.kp_stride + k] = 1;
+    if (threadIdx.x == 0) {                       // skipped (ref: descriptor.py:196-198): no rows
+      chain_publish(&lb[k], kChainAgg, 0u);
+      atomicAdd(&a.skipped[b], 1);
+    }
     return;
   }
   const uint8_t* m = mim + (size_t)b * c.H * c.W;
@@ -388,124 +409,89 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
         pick[np++] = dom;
       }
     }
-    if (threadIdx.x == 0) kp_skip[(size_t)b * a.kp_stride + k] = skip;
+    if (threadIdx.x == 0) {
+      chain_publish(&lb[k], kChainAgg, (unsigned)np);   // successors may look back through us now
+      if (skip) atomicAdd(&a.skipped[b], skip);
+      if (np) atomicAdd(&a.count[b], np);
+    }
   }
-  // one phase: axis-patch rows are emitted from `cnt` while the rotated picks
-  // (at most two) are counted into their own buffers; then one barrier
+  // count the rotated picks (at most two) into their own buffers
   const bool rot_mode = c.mode == 2 && c.rotate;
-  int nrot = 0;
   const int dom90 = (O % 2 == 0 && c.P % 2 == 0) ? O / 2 + 1 : -1;
+  int nrot = 0;
 #pragma unroll
   for (int q = 0; q < kMaxPick; ++q) {
     if (q >= np) break;
     const int dom = pick[q];
-    if (rot_mode && dom == dom90) {
-      emit_row_rot90<OT, GT>(a, c, cnt, dom, slot_rows + (slot0 + q) * a.stride);
-      if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[0]; }
-    } else if (rot_mode && dom != 1) {
+    if (rot_mode && dom != 1 && dom != dom90) {
       count_rotated<CS, OT, GT>(c, ctr, tab.soff + (size_t)(dom - 1) * c.P * c.P, cnt_rot[nrot], &s_sq[1 + nrot]);
       ++nrot;
-    } else {
-      const int var = c.mode == 0 ? 1 : dom;
-      emit_row<OT, GT>(a, c, cnt, var, slot_rows + (slot0 + q) * a.stride);
-      if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = var; meta[3 * q + 2] = s_sq[0]; }
     }
   }
-  if (nrot > 0) {
-    __syncthreads();
-    int r = 0;
+  // output position: exclusive prefix of the descriptor counts of the keypoints
+  // before this one (decoupled look-back over their published counts)
+  if (threadIdx.x < 32) {
+    // warp-wide look-back: 32 predecessors per step; stop at the nearest
+    // inclusive prefix, add the counts after it
+    const unsigned lane = threadIdx.x;
+    unsigned excl = 0;
+    for (int base = k - 1; base >= 0; base -= 32) {
+      const int j = base - (int)lane;
+      unsigned long long f = 2ull << 62;          // before keypoint 0: prefix 0
+      if (j >= 0) do { f = chain_read(&lb[j]); } while ((f >> 62) == 0);
+      const unsigned pre = __ballot_sync(0xffffffffu, (f >> 62) == kChainPrefix);
+      const int stop = pre ? __ffs(pre) - 1 : 32;   // nearest prefix: the lowest lane
+      unsigned v = (int)lane <= stop ? (unsigned)f : 0u;
 #pragma unroll
-    for (int q = 0; q < kMaxPick; ++q) {
-      if (q >= np) break;
-      const int dom = pick[q];
-      if (!(rot_mode && dom != 1 && dom != dom90)) continue;
-      emit_row<OT, GT>(a, c, cnt_rot[r], dom, slot_rows + (slot0 + q) * a.stride);
-      if (threadIdx.x == 0) { meta[3 * q] = 1; meta[3 * q + 1] = dom; meta[3 * q + 2] = s_sq[1 + r]; }
-      ++r;
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      excl += v;
+      if (pre) break;
+    }
+    if (lane == 0) {
+      chain_publish(&lb[k], kChainPrefix, excl + (unsigned)np);
+      s_excl = excl;
     }
   }
-  for (int q = np + threadIdx.x; q < c.per; q += kT) meta[3 * q] = 0;
-}
-
-// exclusive scan of the valid flags of one image's slots -> output positions
-__global__ void __launch_bounds__(1024) k_desc_scan(const int* __restrict__ slot_meta,
-                                                    const int* __restrict__ kp_skip, DescribeArgs a, int per,
-                                                    int* __restrict__ offs) {
-  __shared__ int s_warp[32];
-  __shared__ int s_base, s_skip, s_tot;
-  const int b = blockIdx.x;
-  const int n = a.kp_count[b] * per;
-  const int* meta = slot_meta + (size_t)b * a.kp_stride * per * 3;
-  int* of = offs + (size_t)b * a.kp_stride * per;
-  if (threadIdx.x == 0) { s_base = 0; s_skip = 0; }
   __syncthreads();
-  for (int i = threadIdx.x; i < a.kp_count[b]; i += blockDim.x) atomicAdd(&s_skip, kp_skip[(size_t)b * a.kp_stride + i]);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
-    const int i = c0 + threadIdx.x;
-    const int v = i < n ? meta[3 * i] : 0;
-    int incl = v;
+  // rows straight into their final slots, in pick order (ref: descriptor.py:199-216)
+  const unsigned excl = s_excl;
+  int r = 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += t;
+  for (int q = 0; q < kMaxPick; ++q) {
+    if (q >= np) break;
+    const int dom = pick[q];
+    const unsigned dst = excl + q;
+    const bool rotated = rot_mode && dom != 1 && dom != dom90;
+    if (dst < (unsigned)a.cap) {
+      const size_t o = (size_t)b * a.cap + dst;
+      __half* row = a.counts + o * a.stride;
+      const int var = c.mode == 0 ? 1 : dom;
+      if (rot_mode && dom == dom90) emit_row_rot90<OT, GT>(a, c, cnt, dom, row);
+      else emit_row<OT, GT>(a, c, rotated ? cnt_rot[r] : cnt, var, row);
+      if (threadIdx.x == 0) {
+        a.sqnorm[o] = rotated ? s_sq[1 + r] : s_sq[0];
+        a.kp[o] = k;
+        a.variant[o] = (uint8_t)var;
+      }
     }
-    if (lane == 31) s_warp[wid] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int run = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { const int t = s_warp[w]; s_warp[w] = run; run += t; }
-      s_tot = run;
-    }
-    __syncthreads();
-    if (i < n) of[i] = v ? s_base + s_warp[wid] + incl - v : -1;
-    __syncthreads();
-    if (threadIdx.x == 0) s_base += s_tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) { a.count[b] = s_base; a.skipped[b] = s_skip; }
-}
-
-// one warp per slot: copy the row (16-byte vectors) and metadata into place
-__global__ void __launch_bounds__(256) k_desc_copy(const __half* __restrict__ slot_rows,
-                                                   const int* __restrict__ slot_meta, const int* __restrict__ offs,
-                                                   DescribeArgs a, int per) {
-  const int b = blockIdx.y;
-  const int slot = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (slot >= a.kp_count[b] * per) return;
-  const size_t gs = (size_t)b * a.kp_stride * per + slot;
-  const int dst = offs[gs];
-  if (dst < 0 || dst >= a.cap) return;
-  const size_t o = (size_t)b * a.cap + dst;
-  const int4* src = reinterpret_cast<const int4*>(slot_rows + gs * a.stride);
-  int4* out = reinterpret_cast<int4*>(a.counts + o * a.stride);
-  for (int i = lane; i < a.stride / 8; i += 32) out[i] = src[i];
-  if (lane == 0) {
-    a.sqnorm[o] = slot_meta[3 * gs + 2];
-    a.kp[o] = slot / per;
-    a.variant[o] = (uint8_t)slot_meta[3 * gs + 1];
+    if (rotated) ++r;
   }
 }
 
 struct DescWs {
-  size_t off_rows, off_meta, off_skip, off_offs, total;
+  size_t off_chain, off_ticket, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int per_kp(int mode, int O) { return mode == 1 ? O : (mode == 2 ? 2 : 1); }
 
-DescWs plan_ws(int B, int S, int O, int stride) {
-  // sized for the largest mode (ring: O slots per keypoint)
+DescWs plan_ws(int B, int S) {
   DescWs p{};
-  const size_t slots = (size_t)B * S * O;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = al(off + bytes); return o; };
-  p.off_rows = take(slots * stride * sizeof(__half));
-  p.off_meta = take(slots * 3 * sizeof(int));
-  p.off_skip = take((size_t)B * S * sizeof(int));
-  p.off_offs = take(slots * sizeof(int));
+  p.off_chain = take((size_t)B * S * sizeof(unsigned long long));   // look-back words per keypoint
+  p.off_ticket = take((size_t)B * sizeof(unsigned));                  // start-order tickets per image
   p.total = off;
   return p;
 }
@@ -516,12 +502,13 @@ constexpr int kMaxStride = 256;
 
 size_t describe_workspace_bytes(int B, int kp_stride, int grid, int O) {
   (void)grid;
-  return plan_ws(B, kp_stride > 0 ? kp_stride : 1, O, kMaxStride).total;
+  (void)O;
+  return plan_ws(B, kp_stride > 0 ? kp_stride : 1).total;
 }
 
 int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int S = a.kp_stride > 0 ? a.kp_stride : 1;
-  const DescWs p = plan_ws(a.B, S, a.O, kMaxStride);
+  const DescWs p = plan_ws(a.B, S);
   if (ws_bytes < p.total) return 1;
   if (a.stride % 8 != 0 || a.stride > kMaxStride) return 2;
   const int cs = a.patch / a.grid;
@@ -538,15 +525,12 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
   c.stride = tab.stride;
   c.rows = 2 * c.R + 1;
   char* w = static_cast<char*>(ws);
-  auto* rows = reinterpret_cast<__half*>(w + p.off_rows);
-  auto* meta = reinterpret_cast<int*>(w + p.off_meta);
-  auto* skip = reinterpret_cast<int*>(w + p.off_skip);
-  auto* offs = reinterpret_cast<int*>(w + p.off_offs);
-  if (a.kp_stride == 0) {
-    cudaMemsetAsync(a.count, 0, sizeof(int32_t) * a.B, st);
-    cudaMemsetAsync(a.skipped, 0, sizeof(int32_t) * a.B, st);
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
-  }
+  auto* chain = reinterpret_cast<unsigned long long*>(w + p.off_chain);
+  auto* ticket = reinterpret_cast<unsigned*>(w + p.off_ticket);
+  cudaMemsetAsync(a.count, 0, sizeof(int32_t) * a.B, st);
+  cudaMemsetAsync(a.skipped, 0, sizeof(int32_t) * a.B, st);
+  if (a.kp_stride == 0) return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+  cudaMemsetAsync(w, 0, p.total, st);                 // look-back words and tickets
   const size_t smem = (size_t)c.rows * c.stride + 3 * (size_t)c.cells * c.O * sizeof(uint32_t) + 128;
   if (smem > 200 * 1024) return 2;
   dim3 grid(a.kp_stride, a.B);
@@ -568,10 +552,7 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
   // the BASELINE grid (6 orientations, 6 x 6 cells) with constant indexing
   auto kern = (c.O == 6 && c.g == 6) ? k_desc_main<16, 6, 6> : k_desc_main<16, 0, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, kT, smem, st>>>(tmap, mim, a, c, tab, rows, meta, skip);
-  k_desc_scan<<<a.B, 1024, 0, st>>>(meta, skip, a, c.per, offs);
-  dim3 g2((a.kp_stride * c.per + 7) / 8, a.B);
-  k_desc_copy<<<g2, 256, 0, st>>>(rows, meta, offs, a, c.per);
+  kern<<<grid, kT, smem, st>>>(tmap, mim, a, c, tab, chain, ticket);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }
 
