@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(1024) k_med_bins(const unsigned* __restrict__ 
 // gather the float bits of every value falling into one of the two bins;
 // hits are appended warp-aggregated into a per-CTA shared buffer and flushed
 // with one global atomic per CTA pass (16 values per thread per pass)
-constexpr int kCollectVec = 4;                  // float4 loads per thread per pass
+constexpr int kCollectVec = 8;                  // float4 loads per thread per pass (mask: 32 values)
 __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ amp0, const MedInfo* __restrict__ info,
                                                      unsigned* __restrict__ cand, unsigned* __restrict__ cnt,
                                                      unsigned n) {
