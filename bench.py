@@ -75,7 +75,8 @@ def _oracle_pair(args):
     (rc, rk), (tc, tk) = feats
     rv = rc / np.linalg.norm(rc, axis=1, keepdims=True)
     tv = tc / np.linalg.norm(tc, axis=1, keepdims=True)
-    O.match_nn(rv, rk, tv, tk)
+    if len(rk) and len(tk):
+        O.match_nn(rv, rk, tv, tk)
     return time.perf_counter() - t0
 
 
@@ -125,7 +126,8 @@ def _unit_worker(conn, size, seed0, stride):
             st[f"d{msg - 2}"] = (c / np.linalg.norm(c, axis=1, keepdims=True), k)
         else:
             (rv, rk), (tv, tk) = st["d0"], st["d1"]
-            O.match_nn(rv, rk, tv, tk)
+            if len(rk) and len(tk):                 # tiny images can leave a side without descriptors
+                O.match_nn(rv, rk, tv, tk)
             pair += 1
         conn.send(time.perf_counter() - t0)
 
