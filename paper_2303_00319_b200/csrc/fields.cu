@@ -29,6 +29,7 @@
 
 #include "fft.cuh"
 #include "fields.h"
+#include "tma.cuh"
 
 namespace r2 {
 
@@ -720,6 +721,10 @@ struct PcShape {
 #define R2_PC_PREFETCH 1
 #endif
 constexpr bool kPcPrefetch = R2_PC_PREFETCH;
+#ifndef R2_PC_TMA
+#define R2_PC_TMA 1
+#endif
+constexpr bool kPcTma = R2_PC_TMA;   // K3b inputs by TMA for 1,024-point rows
 
 R2_DEV float rcp_approx(float x) {
   float y;
@@ -733,6 +738,10 @@ R2_DEV float rcp_approx(float x) {
 // weight and 1 / (sum of amplitudes) share one reciprocal:
 // pc = en / ((1 + exp(g (cut - spread))) (sa + eps)).
 template <int SC>
+R2_DEV void pc_core(const float2 (&X)[SC], const float2 (&Y)[SC], float T, float inv_sm1, float gain, float cut,
+                    float2& sa, float2& pc);
+
+template <int SC>
 R2_DEV void pc_pair(const float2* __restrict__ b0, const float2* __restrict__ b1, int PL, float T, float inv_sm1,
                     float gain, float cut, float2& sa, float2& pc) {
   float2 X[SC], Y[SC];
@@ -742,6 +751,12 @@ R2_DEV void pc_pair(const float2* __restrict__ b0, const float2* __restrict__ b1
     X[s] = make_float2(z0.x, z1.x);
     Y[s] = make_float2(z0.y, z1.y);
   }
+  pc_core<SC>(X, Y, T, inv_sm1, gain, cut, sa, pc);
+}
+
+template <int SC>
+R2_DEV void pc_core(const float2 (&X)[SC], const float2 (&Y)[SC], float T, float inv_sm1, float gain, float cut,
+                    float2& sa, float2& pc) {
   float2 se = make_float2(0.f, 0.f), so = se;
   sa = se;
   float mx0 = 0.f, mx1 = 0.f;
@@ -991,6 +1006,142 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
   }
 }
 
+
+// K3b for 1,024-point rows with 4 scales (the BASELINE path), inputs by TMA.
+// One CTA per row pair (y0, y0+1): each orientation stage's inputs arrive in
+// shared memory by the tensor-memory accelerator -- the two rows of every
+// scale >= 1 as 3-D boxes {2 rows of a 4-row column tile, 256 columns} (the
+// rows the CTA needs, 16 of every 32 bytes of the tile's sectors, gathered
+// without load instructions), the two scale-0 rows of R0 as 1-D bulk copies
+// -- so the six FFT warps start from shared memory and the load-store pipe
+// carries only the FFT exchange and the pixel phase.  Buffers: scale s >= 1,
+// row r at (s-1)*2 + r (the pair is contiguous: the staging of the boxes as
+// [x][row]); R0 row r at 6 + r (unpadded).  Same arithmetic as k_rows_pc.
+constexpr int kPcTmaBox = 256;
+__global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_constant__ CUtensorMap qmap,
+                                                             const float2* __restrict__ Q,
+                                                             const float2* __restrict__ R0,
+                                                             const float* __restrict__ thr, PcOut out,
+                                                             const __grid_constant__ FieldsConst c, int ahead) {
+  // buffer pitch rounded to 128 bytes: TMA destinations must be 128-byte aligned
+  constexpr int G = 32, S = 4, W = 1024, PL = (padded_len(W) + 15) & ~15, PIX = 8;
+  extern __shared__ float2 sm_raw[];
+  __shared__ uint64_t s_bar;
+  float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
+  const int H = c.H, O = c.O, F = S * O;
+  const int b = blockIdx.y, y0 = 2 * blockIdx.x;
+  const float* thr_b = thr + (size_t)b * O;
+  const float2* Rb = R0 + (size_t)b * O * H * W;
+  const float inv_sm1 = c.inv_sm1, gain = c.spread_gain, cut = c.spread_cutoff;
+  const int g = threadIdx.x / G, t = threadIdx.x % G;
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&qmap) : "memory");
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  float acc_a[PIX], acc_b[PIX], acc_c[PIX], best[PIX];
+  int bidx[PIX];
+#pragma unroll
+  for (int i = 0; i < PIX; ++i) { acc_a[i] = acc_b[i] = acc_c[i] = 0.f; best[i] = -1.f; bidx[i] = 1; }
+  for (int o = 0; o < O; ++o) {
+    if (threadIdx.x == 0) {
+      // this stage's inputs (the previous stage's pixel phase is done with
+      // the buffers: the barrier at the end of the loop, then the proxy fence)
+      fence_proxy_async();
+      mbar_expect_tx(&s_bar, (uint32_t)(3 * (W / kPcTmaBox) * kPcTmaBox * 2 * sizeof(float2) + 2 * W * sizeof(float2)));
+      const int tile = y0 >> 2;
+      for (int s = 1; s < S; ++s) {
+        const int z = (b * F + s * O + o) * (c.Hp >> 2) + tile;
+        float2* dst = sm + (s - 1) * 2 * PL;
+        for (int k = 0; k < W / kPcTmaBox; ++k) tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, &s_bar);
+      }
+      for (int r = 0; r < 2; ++r)
+        bulk_load(sm + (6 + r) * PL, Rb + ((size_t)o * H + y0 + r) * W, W * sizeof(float2), &s_bar);
+      // and the next stage's (or the CTA one resident wave later's first stage) into L2
+      int pb = b, py = y0, o1 = o + 1;
+      bool go = o1 < O;
+      if (!go && ahead > 0) {
+        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + ahead;
+        if (lin < (long long)gridDim.x * gridDim.y) { pb = (int)(lin / gridDim.x); py = 2 * (int)(lin % gridDim.x); o1 = 0; go = true; }
+      }
+      if (go) {
+        const float2* pQ = Q + (size_t)pb * F * c.Hp * W;
+        for (int s = 1; s < S; ++s)
+          l2_prefetch(pQ + ((size_t)(s * O + o1) * c.Hp + (py & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
+        l2_prefetch(R0 + ((size_t)pb * O + o1) * H * W + (size_t)py * W, (unsigned)(2 * W * sizeof(float2)));
+      }
+    }
+    mbar_wait(&s_bar, (uint32_t)(o & 1));
+    if (g < 6) {                                   // FFT warps: scale 1 + g / 2, row g % 2
+      const int s = 1 + (g >> 1), r = g & 1;
+      const float2* st = sm + (s - 1) * 2 * PL;    // [x][row]
+      float2 v[32];
+#pragma unroll
+      for (int m = 0; m < 32; ++m) v[m] = cconj(st[2 * (t + 32 * m) + r]);
+      SyncNamed pair{8 + (s - 1), 2 * G};          // both rows read before the FFT reuses the staging
+      pair();
+      float2* buf = sm + ((s - 1) * 2 + r) * PL;
+      SyncWarp sw{0xffffffffu};
+      fft_fast<G>(v, buf, c.tw_w, t, sw);
+      sw();
+#pragma unroll
+      for (int m = 0; m < 32; ++m) buf[pad32(t + G * m)] = cconj(v[m]);
+    }
+    __syncthreads();
+    // pixel phase: pixel pairs (i, i + 1) of the two rows in the fp32x2 lanes
+    const float T = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
+#pragma unroll
+    for (int i = 0; i < PIX; i += 2) {
+      const int p0 = threadIdx.x + kThreads * i, p1 = p0 + kThreads;
+      const int r0 = p0 / W, x0 = p0 % W, r1 = p1 / W, x1 = p1 % W;
+      float2 X[S], Y[S];
+      {
+        const float2 z0 = sm[(6 + r0) * PL + x0], z1 = sm[(6 + r1) * PL + x1];
+        X[0] = make_float2(z0.x, z1.x);
+        Y[0] = make_float2(z0.y, z1.y);
+      }
+#pragma unroll
+      for (int s = 1; s < S; ++s) {
+        const float2 z0 = sm[((s - 1) * 2 + r0) * PL + pad32(x0)], z1 = sm[((s - 1) * 2 + r1) * PL + pad32(x1)];
+        X[s] = make_float2(z0.x, z1.x);
+        Y[s] = make_float2(z0.y, z1.y);
+      }
+      float2 sa2, pc2;
+      pc_core<S>(X, Y, T, inv_sm1, gain, cut, sa2, pc2);
+      const float2 pcc = __fmul2_rn(pc2, make_float2(ca, ca)), pcs = __fmul2_rn(pc2, make_float2(sa_o, sa_o));
+      acc_a[i] = fmaf(pcc.x, pcc.x, acc_a[i]);
+      acc_a[i + 1] = fmaf(pcc.y, pcc.y, acc_a[i + 1]);
+      acc_b[i] = fmaf(pcc.x, pcs.x, acc_b[i]);
+      acc_b[i + 1] = fmaf(pcc.y, pcs.y, acc_b[i + 1]);
+      acc_c[i] = fmaf(pcs.x, pcs.x, acc_c[i]);
+      acc_c[i + 1] = fmaf(pcs.y, pcs.y, acc_c[i + 1]);
+      if (sa2.x > best[i]) { best[i] = sa2.x; bidx[i] = o + 1; }
+      if (sa2.y > best[i + 1]) { best[i + 1] = sa2.y; bidx[i + 1] = o + 1; }
+      if (out.a_o || out.pc) {
+        const size_t q0 = (((size_t)b * O + o) * H + y0 + r0) * W + x0;
+        const size_t q1 = (((size_t)b * O + o) * H + y0 + r1) * W + x1;
+        if (out.a_o) { out.a_o[q0] = sa2.x; out.a_o[q1] = sa2.y; }
+        if (out.pc) { out.pc[q0] = pc2.x; out.pc[q1] = pc2.y; }
+      }
+    }
+    __syncthreads();                               // the next stage's TMA rewrites the buffers
+  }
+#pragma unroll
+  for (int i = 0; i < PIX; ++i) {
+    const int p = threadIdx.x + kThreads * i;
+    const int r = p / W, x = p % W;
+    const int y = y0 + r;
+    const float a = acc_a[i], bq = 2.f * acc_b[i], cq = acc_c[i];
+    const float root = sqrtf(bq * bq + (a - cq) * (a - cq));
+    const size_t po = ((size_t)b * H + y) * W + x;
+    out.mmax[po] = 0.5f * (cq + a + root);
+    out.mmin[po] = fmaxf(0.5f * (cq + a - root), 0.f);
+    out.mim[po] = (uint8_t)bidx[i];
+    if (out.amax) out.amax[po] = best[i];
+  }
+}
+
 // ================================================================ host side
 
 static int fast_g(int n) {
@@ -1143,9 +1294,43 @@ static cudaError_t launch_pc_s(const float2* Q, const float2* R0, const float* t
   return cudaPeekAtLastError();
 }
 
+// the TMA variant of K3b for 1,024-point rows, 4 scales, even H; false when
+// it does not apply (or the tensor map cannot be encoded)
+static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
+                          const FieldsConst& c, cudaStream_t st, cudaError_t& e) {
+  if (!kPcTma || c.W != 1024 || c.S != 4 || (c.H & 1) || (c.Hp & 3) || ((uintptr_t)Q & 15)) return false;
+  auto enc = get_encode();
+  if (!enc) return false;
+  // Q as 8-byte elements (row-in-tile, x, tile of all planes)
+  CUtensorMap map{};
+  // Q as 32-bit words: (component of the row-in-tile, x, tile of all planes);
+  // a box of 4 words = the two rows y0, y0+1 of one column
+  cuuint64_t dims[3] = {8, (cuuint64_t)c.W, (cuuint64_t)c.B * c.S * c.O * (c.Hp / 4)};
+  cuuint64_t strides[2] = {4 * sizeof(float2), (cuuint64_t)c.W * 4 * sizeof(float2)};
+  cuuint32_t box[3] = {4, (cuuint32_t)kPcTmaBox, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float2*>(Q), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  const size_t smem = (size_t)8 * ((padded_len(1024) + 15) & ~15) * sizeof(float2) + 128;
+  if ((e = set_smem(k_rows_pc_tma, smem)) != cudaSuccess) return true;
+  int per_sm = 0, dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_pc_tma, kThreads, smem);
+  k_rows_pc_tma<<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, R0, thr, out, c, per_sm * n_sm);
+  e = cudaPeekAtLastError();
+  return true;
+}
+
 template <int G>
 static cudaError_t launch_pc(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
                              const FieldsConst& c, cudaStream_t st) {
+  if constexpr (G == 32) {
+    cudaError_t e = cudaSuccess;
+    if (launch_pc_tma(Q, R0, thr, out, c, st, e)) return e;
+  }
   if (c.S == 4 && G >= 8 && G <= 128) return launch_pc_s<G, 4>(Q, R0, thr, out, c, st);
   return launch_pc_s<G, 0>(Q, R0, thr, out, c, st);
 }

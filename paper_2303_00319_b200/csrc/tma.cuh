@@ -41,6 +41,15 @@ R2_DEV void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, 
       :: "r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)) : "memory");
 }
 
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16)
+R2_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// order earlier generic-proxy accesses of shared memory before async-proxy (TMA) writes
+R2_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 inline PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
