@@ -40,6 +40,7 @@ template <int G>
 struct ColsCfg { static constexpr int T = G == 0 ? 256 : (G >= 64 ? 2 * G : 128); };
 constexpr int kHistBins = 4096;   // float bits >> 19 of a non-negative float
 constexpr int kAmpRows = 4;       // row groups per k_rows_amp0 CTA
+constexpr int kPcTmaBox = 256;    // columns per TMA box of the row passes (box dims <= 256)
 constexpr int kMaxS = 8;
 constexpr int kMaxO = 16;
 constexpr float kPi = 3.14159265358979f;
@@ -455,6 +456,85 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
   __syncthreads();
   unsigned* gh = hist + ((size_t)b * c.O + o) * kHistBins;
   for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&gh[i], sh[i]);
+}
+
+
+// K3a for 1,024-point rows with TMA inputs: per row group (8 rows) the four
+// row pairs arrive as 3-D boxes {2 rows of a 4-row column tile, 256 columns}
+// in the FFT buffers of the pair's two groups (128-byte pitch), so the
+// groups read their rows from shared memory; otherwise as k_rows_amp0<32>.
+__global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constant__ CUtensorMap qmap,
+                                                            const float2* __restrict__ Q, float2* __restrict__ R0,
+                                                            float* __restrict__ amp0, unsigned* __restrict__ hist,
+                                                            const __grid_constant__ FieldsConst c, int ahead) {
+  constexpr int G = 32, W = 1024, NG = kThreads / G, PL = (padded_len(W) + 15) & ~15;
+  extern __shared__ float2 sm_raw[];
+  __shared__ uint64_t s_bar;
+  float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
+  const int H = c.H, F = c.S * c.O;
+  const int o = blockIdx.y, b = blockIdx.z;
+  const float2* Qp = Q + ((size_t)b * F + o) * c.Hp * W;   // filter (s=0, o)
+  float* A = amp0 + ((size_t)b * c.O + o) * H * W;
+  float2* Rp = R0 + ((size_t)b * c.O + o) * H * W;
+  unsigned* sh = reinterpret_cast<unsigned*>(sm + NG * PL);
+  for (int i = threadIdx.x; i < kHistBins; i += kThreads) sh[i] = 0;
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&qmap) : "memory");
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int g = threadIdx.x / G, t = threadIdx.x % G;
+  float2* buf = sm + g * PL;
+  const int y_lo = blockIdx.x * NG * kAmpRows, yend = min(H, y_lo + NG * kAmpRows);
+  int it = 0;
+  for (int yg = y_lo; yg < yend; yg += NG, ++it) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async();                         // the previous group's buffers are free (barrier below)
+      mbar_expect_tx(&s_bar, (uint32_t)(NG * W * sizeof(float2)));
+      for (int p = 0; p < NG / 2; ++p) {
+        const int y = yg + 2 * p;
+        const int z = (b * F + o) * (c.Hp >> 2) + (y >> 2);
+        for (int k = 0; k < W / kPcTmaBox; ++k)
+          tma_load_3d(sm + 2 * p * PL + 2 * kPcTmaBox * k, &qmap, 2 * (y & 3), kPcTmaBox * k, z, &s_bar);
+      }
+      if (yg + NG < yend) {                        // the next row group's Q tiles into L2
+        l2_prefetch(Qp + (size_t)(yg + NG) * W, (unsigned)(NG * W * sizeof(float2)));
+      } else if (ahead > 0) {                      // the first row group of the CTA `ahead` slots later
+        const long long lin = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x + ahead;
+        if (lin < (long long)gridDim.x * gridDim.y * gridDim.z) {
+          const int nx = (int)(lin % gridDim.x), no = (int)((lin / gridDim.x) % gridDim.y);
+          const int nbz = (int)(lin / ((long long)gridDim.x * gridDim.y));
+          const int ny = nx * NG * kAmpRows;
+          if (ny < H) l2_prefetch(Q + ((size_t)nbz * F + no) * c.Hp * W + (size_t)ny * W, (unsigned)(NG * W * sizeof(float2)));
+        }
+      }
+    }
+    mbar_wait(&s_bar, (uint32_t)(it & 1));
+    const int y = yg + g;
+    const float2* st = sm + (g & ~1) * PL;         // [x][row] of the pair (g & ~1, g | 1)
+    float2 v[32];
+#pragma unroll
+    for (int m = 0; m < 32; ++m) v[m] = cconj(st[2 * (t + 32 * m) + (g & 1)]);
+    SyncNamed pair{8 + (g >> 1), 2 * G};           // both rows read before the FFT reuses the staging
+    pair();
+    SyncWarp sw{0xffffffffu};
+    fft_fast<G>(v, buf, c.tw_w, t, sw);
+    if (y < yend) {
+#pragma unroll
+      for (int m = 0; m < 32; ++m) {
+        const float2 zz = cconj(v[m]);
+        const float a = sqrt_approx(fmaf(zz.x, zz.x, zz.y * zz.y));   // as k_rows_amp0
+        Rp[(size_t)y * W + t + G * m] = zz;
+        A[(size_t)y * W + t + G * m] = a;
+        atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
+      }
+    }
+    __syncthreads();                               // the next group's TMA rewrites the buffers
+  }
+  unsigned* gh = hist + ((size_t)b * c.O + o) * kHistBins;
+  for (int i = threadIdx.x; i < kHistBins; i += kThreads)
     if (sh[i]) atomicAdd(&gh[i], sh[i]);
 }
 
@@ -1017,7 +1097,6 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
 // carries only the FFT exchange and the pixel phase.  Buffers: scale s >= 1,
 // row r at (s-1)*2 + r (the pair is contiguous: the staging of the boxes as
 // [x][row]); R0 row r at 6 + r (unpadded).  Same arithmetic as k_rows_pc.
-constexpr int kPcTmaBox = 256;
 __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_constant__ CUtensorMap qmap,
                                                              const float2* __restrict__ Q,
                                                              const float2* __restrict__ R0,
@@ -1240,9 +1319,16 @@ static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c,
   return cudaPeekAtLastError();
 }
 
+static bool launch_amp0_tma(const float2* Q, float2* R0, float* amp0, unsigned* hist, const FieldsConst& c,
+                            cudaStream_t st, cudaError_t& e);
+
 template <int G>
 static cudaError_t launch_amp0(const float2* Q, float2* R0, float* amp0, unsigned* hist, const FieldsConst& c,
                                cudaStream_t st) {
+  if constexpr (G == 32) {
+    cudaError_t e = cudaSuccess;
+    if (launch_amp0_tma(Q, R0, amp0, hist, c, st, e)) return e;
+  }
   size_t smem;
   dim3 grid;
   if constexpr (G > 0) {
@@ -1294,32 +1380,55 @@ static cudaError_t launch_pc_s(const float2* Q, const float2* R0, const float* t
   return cudaPeekAtLastError();
 }
 
-// the TMA variant of K3b for 1,024-point rows, 4 scales, even H; false when
-// it does not apply (or the tensor map cannot be encoded)
-static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
-                          const FieldsConst& c, cudaStream_t st, cudaError_t& e) {
-  if (!kPcTma || c.W != 1024 || c.S != 4 || (c.H & 1) || (c.Hp & 3) || ((uintptr_t)Q & 15)) return false;
+// Q (4-row column tiles of 1,024-wide planes) as a 3-D tensor of 32-bit words:
+// (component of the row-in-tile, x, tile of all planes); a box of 4 words =
+// the two rows y0, y0+1 of one column
+static bool make_qmap(const float2* Q, const FieldsConst& c, CUtensorMap& map) {
+  if (!kPcTma || c.W != 1024 || (c.Hp & 3) || ((uintptr_t)Q & 15)) return false;
   auto enc = get_encode();
   if (!enc) return false;
-  // Q as 8-byte elements (row-in-tile, x, tile of all planes)
-  CUtensorMap map{};
-  // Q as 32-bit words: (component of the row-in-tile, x, tile of all planes);
-  // a box of 4 words = the two rows y0, y0+1 of one column
   cuuint64_t dims[3] = {8, (cuuint64_t)c.W, (cuuint64_t)c.B * c.S * c.O * (c.Hp / 4)};
   cuuint64_t strides[2] = {4 * sizeof(float2), (cuuint64_t)c.W * 4 * sizeof(float2)};
   cuuint32_t box[3] = {4, (cuuint32_t)kPcTmaBox, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float2*>(Q), dims, strides, box, es,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
-  const size_t smem = (size_t)8 * ((padded_len(1024) + 15) & ~15) * sizeof(float2) + 128;
-  if ((e = set_smem(k_rows_pc_tma, smem)) != cudaSuccess) return true;
+  return enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float2*>(Q), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int resident_ctas(const void* kern, int threads, size_t smem) {
   int per_sm = 0, dev = 0, n_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_pc_tma, kThreads, smem);
-  k_rows_pc_tma<<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, R0, thr, out, c, per_sm * n_sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  return per_sm * n_sm;
+}
+
+// the TMA variant of K3b for 1,024-point rows, 4 scales, even H; false when
+// it does not apply (or the tensor map cannot be encoded)
+static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
+                          const FieldsConst& c, cudaStream_t st, cudaError_t& e) {
+  CUtensorMap map{};
+  if (c.S != 4 || (c.H & 1) || !make_qmap(Q, c, map)) return false;
+  const size_t smem = (size_t)8 * ((padded_len(1024) + 15) & ~15) * sizeof(float2) + 128;
+  if ((e = set_smem(k_rows_pc_tma, smem)) != cudaSuccess) return true;
+  k_rows_pc_tma<<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, R0, thr, out, c,
+                                                            resident_ctas((const void*)k_rows_pc_tma, kThreads, smem));
+  e = cudaPeekAtLastError();
+  return true;
+}
+
+// the TMA variant of K3a for 1,024-point rows, H a multiple of 8
+static bool launch_amp0_tma(const float2* Q, float2* R0, float* amp0, unsigned* hist, const FieldsConst& c,
+                            cudaStream_t st, cudaError_t& e) {
+  CUtensorMap map{};
+  if ((c.H & 7) || !make_qmap(Q, c, map)) return false;
+  constexpr int NG = kThreads / 32;
+  const size_t smem = (size_t)NG * ((padded_len(1024) + 15) & ~15) * sizeof(float2) + kHistBins * sizeof(unsigned) + 128;
+  if ((e = set_smem(k_rows_amp0_tma, smem)) != cudaSuccess) return true;
+  const dim3 grid((c.H + NG * kAmpRows - 1) / (NG * kAmpRows), c.O, c.B);
+  k_rows_amp0_tma<<<grid, kThreads, smem, st>>>(map, Q, R0, amp0, hist, c,
+                                               resident_ctas((const void*)k_rows_amp0_tma, kThreads, smem));
   e = cudaPeekAtLastError();
   return true;
 }
