@@ -1105,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
   // buffer pitch rounded to 128 bytes: TMA destinations must be 128-byte aligned
   constexpr int G = 32, S = 4, W = 1024, PL = (padded_len(W) + 15) & ~15, PIX = 8;
   extern __shared__ float2 sm_raw[];
-  __shared__ uint64_t s_bar;
+  __shared__ uint64_t s_bar[4];                   // scales 1..3, then R0: the FFT warps of a scale start on its own rows
   float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
   const int H = c.H, O = c.O, F = S * O;
   const int b = blockIdx.y, y0 = 2 * blockIdx.x;
@@ -1115,7 +1115,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
   const int g = threadIdx.x / G, t = threadIdx.x % G;
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(&qmap) : "memory");
-    mbar_init(&s_bar, 1);
+    for (int q = 0; q < 4; ++q) mbar_init(&s_bar[q], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -1128,15 +1128,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
       // this stage's inputs (the previous stage's pixel phase is done with
       // the buffers: the barrier at the end of the loop, then the proxy fence)
       fence_proxy_async();
-      mbar_expect_tx(&s_bar, (uint32_t)(3 * (W / kPcTmaBox) * kPcTmaBox * 2 * sizeof(float2) + 2 * W * sizeof(float2)));
       const int tile = y0 >> 2;
       for (int s = 1; s < S; ++s) {
         const int z = (b * F + s * O + o) * (c.Hp >> 2) + tile;
         float2* dst = sm + (s - 1) * 2 * PL;
-        for (int k = 0; k < W / kPcTmaBox; ++k) tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, &s_bar);
+        mbar_expect_tx(&s_bar[s - 1], (uint32_t)(2 * W * sizeof(float2)));
+        for (int k = 0; k < W / kPcTmaBox; ++k)
+          tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, &s_bar[s - 1]);
       }
+      mbar_expect_tx(&s_bar[3], (uint32_t)(2 * W * sizeof(float2)));
       for (int r = 0; r < 2; ++r)
-        bulk_load(sm + (6 + r) * PL, Rb + ((size_t)o * H + y0 + r) * W, W * sizeof(float2), &s_bar);
+        bulk_load(sm + (6 + r) * PL, Rb + ((size_t)o * H + y0 + r) * W, W * sizeof(float2), &s_bar[3]);
       // and the next stage's (or the CTA one resident wave later's first stage) into L2
       int pb = b, py = y0, o1 = o + 1;
       bool go = o1 < O;
@@ -1151,9 +1153,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
         l2_prefetch(R0 + ((size_t)pb * O + o1) * H * W + (size_t)py * W, (unsigned)(2 * W * sizeof(float2)));
       }
     }
-    mbar_wait(&s_bar, (uint32_t)(o & 1));
     if (g < 6) {                                   // FFT warps: scale 1 + g / 2, row g % 2
       const int s = 1 + (g >> 1), r = g & 1;
+      mbar_wait(&s_bar[s - 1], (uint32_t)(o & 1));
       const float2* st = sm + (s - 1) * 2 * PL;    // [x][row]
       float2 v[32];
 #pragma unroll
@@ -1167,6 +1169,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
 #pragma unroll
       for (int m = 0; m < 32; ++m) buf[pad32(t + G * m)] = cconj(v[m]);
     }
+    mbar_wait(&s_bar[3], (uint32_t)(o & 1));       // R0 rows
     __syncthreads();
     // pixel phase: pixel pairs (i, i + 1) of the two rows in the fp32x2 lanes
     const float T = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
