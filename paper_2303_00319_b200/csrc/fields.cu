@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constan
                                                             const __grid_constant__ FieldsConst c, int ahead) {
   constexpr int G = 32, W = 1024, NG = kThreads / G, PL = (padded_len(W) + 15) & ~15;
   extern __shared__ float2 sm_raw[];
-  __shared__ uint64_t s_bar;
+  __shared__ uint64_t s_bar[NG / 2];              // one per row pair: its two groups start on their own rows
   float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
   const int H = c.H, F = c.S * c.O;
   const int o = blockIdx.y, b = blockIdx.z;
@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constan
   for (int i = threadIdx.x; i < kHistBins; i += kThreads) sh[i] = 0;
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(&qmap) : "memory");
-    mbar_init(&s_bar, 1);
+    for (int q = 0; q < NG / 2; ++q) mbar_init(&s_bar[q], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -492,12 +492,12 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constan
   for (int yg = y_lo; yg < yend; yg += NG, ++it) {
     if (threadIdx.x == 0) {
       fence_proxy_async();                         // the previous group's buffers are free (barrier below)
-      mbar_expect_tx(&s_bar, (uint32_t)(NG * W * sizeof(float2)));
       for (int p = 0; p < NG / 2; ++p) {
         const int y = yg + 2 * p;
         const int z = (b * F + o) * (c.Hp >> 2) + (y >> 2);
+        mbar_expect_tx(&s_bar[p], (uint32_t)(2 * W * sizeof(float2)));
         for (int k = 0; k < W / kPcTmaBox; ++k)
-          tma_load_3d(sm + 2 * p * PL + 2 * kPcTmaBox * k, &qmap, 2 * (y & 3), kPcTmaBox * k, z, &s_bar);
+          tma_load_3d(sm + 2 * p * PL + 2 * kPcTmaBox * k, &qmap, 2 * (y & 3), kPcTmaBox * k, z, &s_bar[p]);
       }
       if (yg + NG < yend) {                        // the next row group's Q tiles into L2
         l2_prefetch(Qp + (size_t)(yg + NG) * W, (unsigned)(NG * W * sizeof(float2)));
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constan
         }
       }
     }
-    mbar_wait(&s_bar, (uint32_t)(it & 1));
+    mbar_wait(&s_bar[g >> 1], (uint32_t)(it & 1));
     const int y = yg + g;
     const float2* st = sm + (g & ~1) * PL;         // [x][row] of the pair (g & ~1, g | 1)
     float2 v[32];
