@@ -16,7 +16,7 @@ import json
 import re
 import sys
 
-FIELDS_KERNELS = ("k_rows_fwd", "k_cols", "k_rows_amp0", "k_med_bins", "k_med_collect", "k_med_h2", "k_med_h3", "k_med_final",
+FIELDS_KERNELS = ("k_rows_fwd", "k_cols", "k_rows_amp0", "k_rows_amp0_tma", "k_med_bins", "k_med_collect", "k_med_h2", "k_med_h3", "k_med_final", "k_rows_pc_tma",
                   "k_rows_pc")
 
 
