@@ -192,7 +192,8 @@ R2_DEV float transfer_s(float lnr_s, float th_s, float ll_s, float ang_s, float 
 // buffer holds the periodic copy S[N] = S[0], so the mirror index needs no wrap.
 template <int G, class Sync>
 R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* Geo,
-                         float2* buf, float2* Qb, int xo, int t, bool mir, Sync& sync) {
+                         float2* buf, float2* Qb, int xo, int t, bool mir, Sync& sync,
+                         const CUtensorMap* qst, int b) {
   constexpr int N = 32 * G;
   constexpr int PS = G + G / 32;                          // padded stride of one m step
   const int W = c.W, F = c.S * c.O;
@@ -217,7 +218,26 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* G
       // conj(spectrum * G) for the inverse; the mirror reads S(-ky, kx) = conj S(ky, W - kx)
       v[m] = __fmul2_rn(sv, make_float2(gv, gv * ysg));
     }
+    if (G == 32 && qst) {
+      // the previous filter's tensor store has read buf before the FFT reuses it
+      if (t == 0) bulk_wait_read0();
+      __syncwarp();
+    }
     fft_fast<G>(v, buf, c.tw_h, t, sync);
+    if (G == 32 && qst) {
+      // the column in natural row order is one {4 rows x 1 column x 256 tiles}
+      // box of the 4-row tile plane: stage it, one lane stores it by TMA
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < 32; ++m) buf[t + G * m] = cconj(v[m]);
+      fence_proxy_async();
+      __syncwarp();
+      if (t == 0) {
+        tma_store_3d(qst, 0, xo, (b * c.S * c.O + f) * (c.Hp >> 2), buf);
+        bulk_commit();
+      }
+      continue;
+    }
     // y = t + G m: tile row (t >> 2) + (G / 4) m, lane t & 3.  W is re-read
     // opaquely each filter so the compiler does not hoist 32 64-bit store
     // addresses across the loop (register spills)
@@ -228,12 +248,16 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* G
 #pragma unroll
     for (int m = 0; m < 32; ++m) q[m * step] = cconj(v[m]);
   }
+  if (G == 32 && qst && t == 0) bulk_wait0();   // the last store has left shared memory
 }
 
 template <int G>
-__global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k_cols(const float2* __restrict__ P, float2* __restrict__ Q,
-                                                   const __grid_constant__ FieldsConst c) {
-  extern __shared__ float2 sm[];
+__global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k_cols(const __grid_constant__ CUtensorMap qst,
+                                                   const float2* __restrict__ P, float2* __restrict__ Q,
+                                                   const __grid_constant__ FieldsConst c, int use_tma) {
+  extern __shared__ float2 sm_raw[];
+  // 128-byte aligned base (TMA store sources)
+  float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
   const int H = c.H, W = c.W, Wh = c.Wh, F = c.S * c.O;
   const int b = blockIdx.y;
   const float2* Pb = P + (size_t)b * H * Wh;
@@ -244,12 +268,12 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     // A CTA owns direct columns kx0..kx0+CG-1 and their mirrors W-kx.
     constexpr int CG = NG / 2;
     constexpr int NS = CG;           // spectrum columns held
-    constexpr int PL = padded_len(N);
-    float2* S = sm;                                              // [NS][PL]
-    float2* geo = sm + NS * PL;                                  // [NS][N] (ln r, theta)
-    float2* bufs = geo + NS * N;                                 // [NG][PL]
+    constexpr int PL = padded_len(N), PLA = (PL + 15) & ~15;   // buffer pitch: 128-byte multiple
+    float2* bufs = sm;                                           // [NG][PLA]
+    float2* S = bufs + NG * PLA;                                 // [NS][PL]
+    float2* geo = S + NS * PL;                                   // [NS][N] (ln r, theta)
     const int g = threadIdx.x / G, t = threadIdx.x % G;
-    float2* buf = bufs + g * PL;
+    float2* buf = bufs + g * PLA;
     const int kx0 = blockIdx.x * CG;
     SyncWarp sw{group_mask(G)};
     SyncNamed sn{1 + g, G};
@@ -289,8 +313,9 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
     const float2* Sc = S + cc * PL;
     const float2* Geo = geo + cc * N;
     if constexpr (G >= 32) {
-      if constexpr (G <= 32) cols_filters<G>(c, Sc, Geo, buf, Qb, xo, t, mir != 0, sw);
-      else cols_filters<G>(c, Sc, Geo, buf, Qb, xo, t, mir != 0, sn);
+      const CUtensorMap* qs = use_tma ? &qst : nullptr;
+      if constexpr (G <= 32) cols_filters<G>(c, Sc, Geo, buf, Qb, xo, t, mir != 0, sw, qs, b);
+      else cols_filters<G>(c, Sc, Geo, buf, Qb, xo, t, mir != 0, sn, qs, b);
       return;
     } else {
     for (int f = 0; f < F; ++f) {
@@ -805,6 +830,10 @@ constexpr bool kPcPrefetch = R2_PC_PREFETCH;
 #define R2_PC_TMA 1
 #endif
 constexpr bool kPcTma = R2_PC_TMA;   // K3b inputs by TMA for 1,024-point rows
+#ifndef R2_COLS_TMA
+#define R2_COLS_TMA 1
+#endif
+constexpr bool kColsTma = R2_COLS_TMA;   // K2 stores by TMA for 1,024-row columns
 
 R2_DEV float rcp_approx(float x) {
   float y;
@@ -1307,18 +1336,34 @@ template <int G>
 static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c, cudaStream_t st) {
   size_t smem;
   dim3 grid;
+  CUtensorMap map{};
+  int use_tma = 0;
   if constexpr (G > 0) {
-    const int N = 32 * G, NG = ColsCfg<G>::T / G, CG = NG / 2, PL = padded_len(N);
-    smem = ((size_t)CG * PL + (size_t)NG * PL) * sizeof(float2) + 2 * (size_t)CG * N * sizeof(float);
+    const int N = 32 * G, NG = ColsCfg<G>::T / G, CG = NG / 2, PL = padded_len(N), PLA = (PL + 15) & ~15;
+    smem = ((size_t)CG * PL + (size_t)NG * PLA) * sizeof(float2) + 2 * (size_t)CG * N * sizeof(float) + 128;
     grid = dim3((c.Wh + CG - 1) / CG, c.B);
+    if constexpr (G == 32) {
+      // 1,024-row columns leave by TMA: Q as 32-bit words (4 rows x 2
+      // components, x, tile of all planes); a box is one column, 256 tiles
+      auto enc = get_encode();
+      if (kColsTma && enc && ((uintptr_t)Q & 15) == 0 && (c.Hp >> 2) == 256) {
+        cuuint64_t dims[3] = {8, (cuuint64_t)c.W, (cuuint64_t)c.B * c.S * c.O * (c.Hp / 4)};
+        cuuint64_t strides[2] = {4 * sizeof(float2), (cuuint64_t)c.W * 4 * sizeof(float2)};
+        cuuint32_t box[3] = {8, 1, 256};
+        cuuint32_t es[3] = {1, 1, 1};
+        use_tma = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, Q, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      }
+    }
   } else {
     const int PL = padded_len(c.H);
-    smem = (size_t)(4 * PL + 2 * PL) * sizeof(float2);
+    smem = (size_t)(4 * PL + 2 * PL) * sizeof(float2) + 128;
     grid = dim3((c.Wh + 3) / 4, c.B);
   }
   cudaError_t e = set_smem(k_cols<G>, smem);
   if (e != cudaSuccess) return e;
-  k_cols<G><<<grid, ColsCfg<G>::T, smem, st>>>(P, Q, c);
+  k_cols<G><<<grid, ColsCfg<G>::T, smem, st>>>(map, P, Q, c, use_tma);
   return cudaPeekAtLastError();
 }
 
