@@ -218,22 +218,23 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* G
       // conj(spectrum * G) for the inverse; the mirror reads S(-ky, kx) = conj S(ky, W - kx)
       v[m] = __fmul2_rn(sv, make_float2(gv, gv * ysg));
     }
-    if (G == 32 && qst) {
-      // the previous filter's tensor store has read buf before the FFT reuses it
+    if (qst) {
+      // the previous filter's tensor stores have read buf before the FFT reuses it
       if (t == 0) bulk_wait_read0();
-      __syncwarp();
+      sync();
     }
     fft_fast<G>(v, buf, c.tw_h, t, sync);
-    if (G == 32 && qst) {
-      // the column in natural row order is one {4 rows x 1 column x 256 tiles}
-      // box of the 4-row tile plane: stage it, one lane stores it by TMA
-      __syncwarp();
+    if (qst) {
+      // the column in natural row order is N / 1,024 {4 rows x 1 column x 256
+      // tiles} boxes of the 4-row tile plane: stage it, one thread stores them
+      sync();
 #pragma unroll
       for (int m = 0; m < 32; ++m) buf[t + G * m] = cconj(v[m]);
       fence_proxy_async();
-      __syncwarp();
+      sync();
       if (t == 0) {
-        tma_store_3d(qst, 0, xo, (b * c.S * c.O + f) * (c.Hp >> 2), buf);
+        for (int k = 0; k < N / 1024; ++k)
+          tma_store_3d(qst, 0, xo, (b * c.S * c.O + f) * (c.Hp >> 2) + 256 * k, buf + 1024 * k);
         bulk_commit();
       }
       continue;
@@ -248,7 +249,7 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* G
 #pragma unroll
     for (int m = 0; m < 32; ++m) q[m * step] = cconj(v[m]);
   }
-  if (G == 32 && qst && t == 0) bulk_wait0();   // the last store has left shared memory
+  if (qst && t == 0) bulk_wait0();               // the last stores have left shared memory
 }
 
 template <int G>
@@ -833,7 +834,7 @@ constexpr bool kPcTma = R2_PC_TMA;   // K3b inputs by TMA for 1,024-point rows
 #ifndef R2_COLS_TMA
 #define R2_COLS_TMA 1
 #endif
-constexpr bool kColsTma = R2_COLS_TMA;   // K2 stores by TMA for 1,024-row columns
+constexpr bool kColsTma = R2_COLS_TMA;   // K2 stores by TMA for columns of >= 1,024 rows
 
 R2_DEV float rcp_approx(float x) {
   float y;
@@ -1342,11 +1343,11 @@ static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c,
     const int N = 32 * G, NG = ColsCfg<G>::T / G, CG = NG / 2, PL = padded_len(N), PLA = (PL + 15) & ~15;
     smem = ((size_t)CG * PL + (size_t)NG * PLA) * sizeof(float2) + 2 * (size_t)CG * N * sizeof(float) + 128;
     grid = dim3((c.Wh + CG - 1) / CG, c.B);
-    if constexpr (G == 32) {
-      // 1,024-row columns leave by TMA: Q as 32-bit words (4 rows x 2
+    if constexpr (G >= 32) {
+      // columns of >= 1,024 rows leave by TMA: Q as 32-bit words (4 rows x 2
       // components, x, tile of all planes); a box is one column, 256 tiles
       auto enc = get_encode();
-      if (kColsTma && enc && ((uintptr_t)Q & 15) == 0 && (c.Hp >> 2) == 256) {
+      if (kColsTma && enc && ((uintptr_t)Q & 15) == 0 && c.Hp == N) {
         cuuint64_t dims[3] = {8, (cuuint64_t)c.W, (cuuint64_t)c.B * c.S * c.O * (c.Hp / 4)};
         cuuint64_t strides[2] = {4 * sizeof(float2), (cuuint64_t)c.W * 4 * sizeof(float2)};
         cuuint32_t box[3] = {8, 1, 256};
