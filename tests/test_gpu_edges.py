@@ -27,7 +27,7 @@ def eng():
     return engine
 
 
-@pytest.mark.parametrize("shape", [(48, 64), (600, 800), (250, 120), (45, 75)])
+@pytest.mark.parametrize("shape", [(48, 64), (600, 800), (250, 120), (45, 75), (768, 1024), (1000, 1024), (1024, 768)])
 def test_fields_odd_shapes_vs_oracle(eng, shape):
     rng = np.random.default_rng(11)
     img = rng.random(shape)
