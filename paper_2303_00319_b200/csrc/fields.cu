@@ -493,7 +493,8 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
 __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constant__ CUtensorMap qmap,
                                                             const float2* __restrict__ Q, float2* __restrict__ R0,
                                                             float* __restrict__ amp0, unsigned* __restrict__ hist,
-                                                            const __grid_constant__ FieldsConst c, int ahead) {
+                                                            const __grid_constant__ FieldsConst c, int ahead,
+                                                            int write_r0) {
   constexpr int G = 32, W = 1024, NG = kThreads / G, PL = (padded_len(W) + 15) & ~15;
   extern __shared__ float2 sm_raw[];
   __shared__ uint64_t s_bar[NG / 2];              // one per row pair: its two groups start on their own rows
@@ -552,7 +553,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constan
       for (int m = 0; m < 32; ++m) {
         const float2 zz = cconj(v[m]);
         const float a = sqrt_approx(fmaf(zz.x, zz.x, zz.y * zz.y));   // as k_rows_amp0
-        Rp[(size_t)y * W + t + G * m] = zz;
+        if (write_r0) Rp[(size_t)y * W + t + G * m] = zz;   // not needed when K3b recomputes scale 0
         A[(size_t)y * W + t + G * m] = a;
         atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
       }
@@ -1120,27 +1121,26 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
 // K3b for 1,024-point rows with 4 scales (the BASELINE path), inputs by TMA.
 // One CTA per row pair (y0, y0+1): each orientation stage's inputs arrive in
 // shared memory by the tensor-memory accelerator -- the two rows of every
-// scale >= 1 as 3-D boxes {2 rows of a 4-row column tile, 256 columns} (the
-// rows the CTA needs, 16 of every 32 bytes of the tile's sectors, gathered
-// without load instructions), the two scale-0 rows of R0 as 1-D bulk copies
-// -- so the six FFT warps start from shared memory and the load-store pipe
-// carries only the FFT exchange and the pixel phase.  Buffers: scale s >= 1,
-// row r at (s-1)*2 + r (the pair is contiguous: the staging of the boxes as
-// [x][row]); R0 row r at 6 + r (unpadded).  Same arithmetic as k_rows_pc.
+// scale as 3-D boxes {2 rows of a 4-row column tile, 256 columns} (the rows
+// the CTA needs, 16 of every 32 bytes of the tile's sectors, gathered without
+// load instructions), one mbarrier per scale -- and all eight warps run one
+// row FFT each: scale 0 is transformed here again rather than read back from
+// K3a, so K3a writes no R0 plane (1.6 GB per 32 images) and no warp idles in
+// the FFT phase.  Buffers: scale s, row r at s*2 + r (a scale's pair is
+// contiguous: the staging of its boxes as [x][row]).  Same arithmetic as
+// k_rows_pc, and bit-identical scale-0 responses (same FFT, same input).
 __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_constant__ CUtensorMap qmap,
                                                              const float2* __restrict__ Q,
-                                                             const float2* __restrict__ R0,
                                                              const float* __restrict__ thr, PcOut out,
                                                              const __grid_constant__ FieldsConst c, int ahead) {
   // buffer pitch rounded to 128 bytes: TMA destinations must be 128-byte aligned
   constexpr int G = 32, S = 4, W = 1024, PL = (padded_len(W) + 15) & ~15, PIX = 8;
   extern __shared__ float2 sm_raw[];
-  __shared__ uint64_t s_bar[4];                   // scales 1..3, then R0: the FFT warps of a scale start on its own rows
+  __shared__ uint64_t s_bar[4];                   // one per scale: its FFT warps start on their own rows
   float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
   const int H = c.H, O = c.O, F = S * O;
   const int b = blockIdx.y, y0 = 2 * blockIdx.x;
   const float* thr_b = thr + (size_t)b * O;
-  const float2* Rb = R0 + (size_t)b * O * H * W;
   const float inv_sm1 = c.inv_sm1, gain = c.spread_gain, cut = c.spread_cutoff;
   const int g = threadIdx.x / G, t = threadIdx.x % G;
   if (threadIdx.x == 0) {
@@ -1159,16 +1159,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
       // the buffers: the barrier at the end of the loop, then the proxy fence)
       fence_proxy_async();
       const int tile = y0 >> 2;
-      for (int s = 1; s < S; ++s) {
+      for (int s = 0; s < S; ++s) {
         const int z = (b * F + s * O + o) * (c.Hp >> 2) + tile;
-        float2* dst = sm + (s - 1) * 2 * PL;
-        mbar_expect_tx(&s_bar[s - 1], (uint32_t)(2 * W * sizeof(float2)));
+        float2* dst = sm + s * 2 * PL;
+        mbar_expect_tx(&s_bar[s], (uint32_t)(2 * W * sizeof(float2)));
         for (int k = 0; k < W / kPcTmaBox; ++k)
-          tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, &s_bar[s - 1]);
+          tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, &s_bar[s]);
       }
-      mbar_expect_tx(&s_bar[3], (uint32_t)(2 * W * sizeof(float2)));
-      for (int r = 0; r < 2; ++r)
-        bulk_load(sm + (6 + r) * PL, Rb + ((size_t)o * H + y0 + r) * W, W * sizeof(float2), &s_bar[3]);
       // and the next stage's (or the CTA one resident wave later's first stage) into L2
       int pb = b, py = y0, o1 = o + 1;
       bool go = o1 < O;
@@ -1178,28 +1175,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
       }
       if (go) {
         const float2* pQ = Q + (size_t)pb * F * c.Hp * W;
-        for (int s = 1; s < S; ++s)
+        for (int s = 0; s < S; ++s)
           l2_prefetch(pQ + ((size_t)(s * O + o1) * c.Hp + (py & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
-        l2_prefetch(R0 + ((size_t)pb * O + o1) * H * W + (size_t)py * W, (unsigned)(2 * W * sizeof(float2)));
       }
     }
-    if (g < 6) {                                   // FFT warps: scale 1 + g / 2, row g % 2
-      const int s = 1 + (g >> 1), r = g & 1;
-      mbar_wait(&s_bar[s - 1], (uint32_t)(o & 1));
-      const float2* st = sm + (s - 1) * 2 * PL;    // [x][row]
+    {                                              // eight FFT warps: scale g / 2 (0 included), row g % 2
+      const int s = g >> 1, r = g & 1;
+      mbar_wait(&s_bar[s], (uint32_t)(o & 1));
+      const float2* st = sm + s * 2 * PL;          // [x][row]
       float2 v[32];
 #pragma unroll
       for (int m = 0; m < 32; ++m) v[m] = cconj(st[2 * (t + 32 * m) + r]);
-      SyncNamed pair{8 + (s - 1), 2 * G};          // both rows read before the FFT reuses the staging
+      SyncNamed pair{8 + s, 2 * G};                // both rows read before the FFT reuses the staging
       pair();
-      float2* buf = sm + ((s - 1) * 2 + r) * PL;
+      float2* buf = sm + (s * 2 + r) * PL;
       SyncWarp sw{0xffffffffu};
       fft_fast<G>(v, buf, c.tw_w, t, sw);
       sw();
 #pragma unroll
       for (int m = 0; m < 32; ++m) buf[pad32(t + G * m)] = cconj(v[m]);
     }
-    mbar_wait(&s_bar[3], (uint32_t)(o & 1));       // R0 rows
     __syncthreads();
     // pixel phase: pixel pairs (i, i + 1) of the two rows in the fp32x2 lanes
     const float T = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
@@ -1208,14 +1203,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
       const int p0 = threadIdx.x + kThreads * i, p1 = p0 + kThreads;
       const int r0 = p0 / W, x0 = p0 % W, r1 = p1 / W, x1 = p1 % W;
       float2 X[S], Y[S];
-      {
-        const float2 z0 = sm[(6 + r0) * PL + x0], z1 = sm[(6 + r1) * PL + x1];
-        X[0] = make_float2(z0.x, z1.x);
-        Y[0] = make_float2(z0.y, z1.y);
-      }
 #pragma unroll
-      for (int s = 1; s < S; ++s) {
-        const float2 z0 = sm[((s - 1) * 2 + r0) * PL + pad32(x0)], z1 = sm[((s - 1) * 2 + r1) * PL + pad32(x1)];
+      for (int s = 0; s < S; ++s) {
+        const float2 z0 = sm[(s * 2 + r0) * PL + pad32(x0)], z1 = sm[(s * 2 + r1) * PL + pad32(x1)];
         X[s] = make_float2(z0.x, z1.x);
         Y[s] = make_float2(z0.y, z1.y);
       }
@@ -1453,6 +1443,12 @@ static int resident_ctas(const void* kern, int threads, size_t smem) {
   return per_sm * n_sm;
 }
 
+// whether K3b runs as k_rows_pc_tma (which recomputes scale 0, so K3a may skip R0)
+static bool pc_tma_applies(const float2* Q, const FieldsConst& c) {
+  CUtensorMap map{};
+  return c.S == 4 && !(c.H & 1) && make_qmap(Q, c, map);
+}
+
 // the TMA variant of K3b for 1,024-point rows, 4 scales, even H; false when
 // it does not apply (or the tensor map cannot be encoded)
 static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
@@ -1461,7 +1457,7 @@ static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, c
   if (c.S != 4 || (c.H & 1) || !make_qmap(Q, c, map)) return false;
   const size_t smem = (size_t)8 * ((padded_len(1024) + 15) & ~15) * sizeof(float2) + 128;
   if ((e = set_smem(k_rows_pc_tma, smem)) != cudaSuccess) return true;
-  k_rows_pc_tma<<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, R0, thr, out, c,
+  k_rows_pc_tma<<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, thr, out, c,
                                                             resident_ctas((const void*)k_rows_pc_tma, kThreads, smem));
   e = cudaPeekAtLastError();
   return true;
@@ -1477,7 +1473,8 @@ static bool launch_amp0_tma(const float2* Q, float2* R0, float* amp0, unsigned* 
   if ((e = set_smem(k_rows_amp0_tma, smem)) != cudaSuccess) return true;
   const dim3 grid((c.H + NG * kAmpRows - 1) / (NG * kAmpRows), c.O, c.B);
   k_rows_amp0_tma<<<grid, kThreads, smem, st>>>(map, Q, R0, amp0, hist, c,
-                                               resident_ctas((const void*)k_rows_amp0_tma, kThreads, smem));
+                                               resident_ctas((const void*)k_rows_amp0_tma, kThreads, smem),
+                                               pc_tma_applies(Q, c) ? 0 : 1);
   e = cudaPeekAtLastError();
   return true;
 }
