@@ -10,9 +10,11 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OBJ = os.path.join(ROOT, "paper_2303_00319_b200", "_lib", "obj")
-PAT = re.compile(r"\b(UTC[A-Z]*MMA[A-Z0-9._]*|UTCBAR[A-Z0-9._]*|UTMALDG[A-Z0-9._]*|UTMACCTL[A-Z0-9._]*|"
+PAT = re.compile(r"\b(UTC[A-Z]*MMA[A-Z0-9._]*|UTCBAR[A-Z0-9._]*|UTMALDG[A-Z0-9._]*|UTMASTG[A-Z0-9._]*|UTMAPF[A-Z0-9._]*|"
+                 r"UBLKCP[A-Z0-9._]*|UBLKPF[A-Z0-9._]*|UTMACCTL[A-Z0-9._]*|"
                  r"LDTM[A-Z0-9._]*|STTM[A-Z0-9._]*|SYNCS\.[A-Z0-9._]*|FMUL2|FFMA2|FADD2|FMNMX3|HMMA[A-Z0-9._]*)\b")
-KERNELS = ("k_match_gemm", "k_desc_main", "k_cols", "k_rows_pc", "k_rows_amp0", "k_fast_nms")
+KERNELS = ("k_match_gemm", "k_desc_main", "k_rows_pc_tma", "k_rows_amp0_tma", "k_cols", "k_rows_pc",
+           "k_rows_amp0", "k_fast_nms", "k_med_collect")
 print("# SASS evidence (cuobjdump -sass of the committed build; mnemonics per the B200 profiling guide)")
 for obj in ("match.o", "describe.o", "fields.o", "detect.o"):
     sass = subprocess.run(["cuobjdump", "-sass", os.path.join(OBJ, obj)], capture_output=True, text=True).stdout
@@ -29,9 +31,10 @@ for obj in ("match.o", "describe.o", "fields.o", "detect.o"):
     for f in funcs[1:]:
         name = f.split("\n", 1)[0].strip()
         short = next((k for k in KERNELS if k in name), None)
-        if short is None or ("ILi32" not in name and short in ("k_cols", "k_rows_pc", "k_rows_amp0")):
+        if short is None or ("ILi32" not in name and short in ("k_cols", "k_rows_pc", "k_rows_amp0")
+                              and "_tma" not in name):
             continue
-        if short == "k_rows_pc" and "Li4E" not in name:
+        if short == "k_rows_pc" and "_tma" not in name and "Li4E" not in name:
             continue
         cnt = collections.Counter(m.group(1).split(".")[0] if not m.group(1).startswith("SYNCS") else m.group(1)
                                   for m in PAT.finditer(f))
