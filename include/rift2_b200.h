@@ -212,6 +212,26 @@ int32_t rift2_evaluate(const int32_t* kp_x, const int32_t* kp_y, const int32_t* 
                        int32_t* out_n_correct, double* out_rmse, uint8_t* out_success, int32_t* out_bad,
                        void* stream);
 
+/* ---- on-device target synthesis ----------------------
+ * The BASELINE generator's target side on the GPU.  The reference ships no
+ * generator; the warp keeps ref: pkg/src/rift2/imaging.py:208-247
+ * (`warp_rigid`) semantics, generalised to any 2x3 map.  For image i:
+ *   src  + i*src_image_stride : float64 [height][width] source (device)
+ *   params[i][8] (device float64): the target->source map i00 i01 i02 i10
+ *     i11 i12 (source x = i00 x + i01 y + i02, ...), gamma, flags (bit 0
+ *     inverted, bit 1 radiometric: inversion, gamma, speckle, renormalise)
+ *   looks[i] (device int32): Gamma(L, 1/L) speckle looks, 0 = none; the
+ *     draws are Philox4x32-10 with counter (pixel, first_image + i, j) and
+ *     key seed
+ *   dst + i*dst_image_stride : float32 target (device)
+ *   dst_src_copy + i*copy_image_stride : optional float32 copy of the source
+ *     (NULL = none), e.g. the reference slot of a [ref, tgt, ...] batch. */
+int32_t rift2_synth_workspace_size(int32_t n_images, int32_t height, int32_t width, size_t* bytes);
+int32_t rift2_synth_targets(const double* src, int64_t src_image_stride, int32_t n_images, int32_t height,
+                            int32_t width, const double* params, const int32_t* looks, uint64_t seed,
+                            int32_t first_image, float* dst, int64_t dst_image_stride, float* dst_src_copy,
+                            int64_t copy_image_stride, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- diagnostics ----------------------------------------------------------
  * The filter bank's exact-median stage (the Rayleigh noise estimate, ref:
  * loggabor.py:222, np.median) on caller-given complex64 planes

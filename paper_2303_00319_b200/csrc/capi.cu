@@ -17,6 +17,7 @@
 #include "detect.h"
 #include "describe.h"
 #include "evaluate.h"
+#include "synth.h"
 #include "fields.h"
 #include "match.h"
 
@@ -340,6 +341,29 @@ int32_t rift2_evaluate(const int32_t* kp_x, const int32_t* kp_y, const int32_t* 
                  match_stride, n_pairs, gt, residual_threshold, rmse_cap, success_min_matches,
                  out_n_correct, out_rmse, out_success, out_bad};
   return map_internal(r2::evaluate_run(a, static_cast<cudaStream_t>(stream)), "rift2_evaluate");
+}
+
+int32_t rift2_synth_workspace_size(int32_t n_images, int32_t height, int32_t width, size_t* bytes) {
+  if (n_images < 0 || height < 2 || width < 2 || !bytes) return fail(RIFT2_BAD_ARGUMENT, "bad synthesis sizes");
+  *bytes = r2::synth_workspace_bytes(n_images, height, width);
+  return RIFT2_OK;
+}
+
+int32_t rift2_synth_targets(const double* src, int64_t src_image_stride, int32_t n_images, int32_t height,
+                            int32_t width, const double* params, const int32_t* looks, uint64_t seed,
+                            int32_t first_image, float* dst, int64_t dst_image_stride, float* dst_src_copy,
+                            int64_t copy_image_stride, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_images < 0 || height < 2 || width < 2 || (int64_t)height * width >= (1ll << 31))
+    return fail(RIFT2_BAD_ARGUMENT, "bad synthesis sizes");
+  const int64_t n = (int64_t)height * width;
+  if (n_images > 1 && (src_image_stride < n || dst_image_stride < n || (dst_src_copy && copy_image_stride < n)))
+    return fail(RIFT2_BAD_ARGUMENT, "image strides must be >= height * width");
+  if (n_images > 0 && (!src || !params || !looks || !dst || !workspace))
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  r2::SynthArgs a{src, src_image_stride, n_images, height, width, params, looks, (unsigned long long)seed,
+                  first_image, dst, dst_image_stride, dst_src_copy, copy_image_stride};
+  return map_internal(r2::synth_run(a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream)),
+                      "rift2_synth_targets");
 }
 
 int32_t rift2_debug_median_workspace_size(int32_t planes, int32_t n, size_t* bytes) {

@@ -282,3 +282,32 @@ def debug_median(z: torch.Tensor):
     _lib.check(lib.rift2_debug_median(_ptr(z), planes, n, _ptr(amps), _ptr(med), _ptr(ws), ws.numel(), _stream()),
                "rift2_debug_median")
     return amps, med
+
+
+def synth_targets(src: torch.Tensor, params: torch.Tensor, looks: torch.Tensor, seed: int, dst: torch.Tensor,
+                  first_image: int = 0, src_copy: torch.Tensor | None = None):
+    """Target synthesis (rift2_synth_targets): src (n, H, W) float64 CUDA
+    sources; params (n, 8) float64 = target->source map (6), gamma, flags;
+    looks (n,) int32; dst (n, H, W) float32 views (any image stride, rows
+    contiguous), src_copy likewise or None."""
+    lib = _lib.load(require_gpu=True)
+    if src.dim() != 3 or src.dtype != torch.float64 or not src.is_cuda:
+        raise ParameterError("src must be an (n, H, W) float64 CUDA tensor")
+    n, H, W = src.shape
+    if params.dtype != torch.float64 or tuple(params.shape) != (n, 8) or not params.is_contiguous():
+        raise ParameterError("params must be a contiguous (n, 8) float64 tensor")
+    if looks.dtype != torch.int32 or tuple(looks.shape) != (n,):
+        raise ParameterError("looks must be an (n,) int32 tensor")
+    for name, t in (("src", src), ("dst", dst), ("src_copy", src_copy)):
+        if t is not None and (tuple(t.shape) != (n, H, W) or t.stride(1) != W or t.stride(2) != 1):
+            raise ParameterError(f"{name} must be (n, {H}, {W}) with contiguous rows")
+    if dst.dtype != torch.float32 or (src_copy is not None and src_copy.dtype != torch.float32):
+        raise ParameterError("dst / src_copy must be float32")
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_synth_workspace_size(n, H, W, ctypes.byref(nbytes)), "synth_targets")
+    ws = WORKSPACES.get("synth", nbytes.value)
+    rc = lib.rift2_synth_targets(_ptr(src), src.stride(0), n, H, W, _ptr(params), _ptr(looks.contiguous()),
+                                 int(seed) & (2**64 - 1), int(first_image), _ptr(dst), dst.stride(0), _ptr(src_copy),
+                                 src_copy.stride(0) if src_copy is not None else 0, _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "rift2_synth_targets")
+    return dst

@@ -90,8 +90,8 @@ def warp(img: np.ndarray, m: np.ndarray) -> np.ndarray:
     """Output p samples img at m^-1(p), bilinear, zero outside
     (ref: imaging.py:208-247 semantics, generalised to a similarity)."""
     h, w = img.shape
-    a_inv = np.linalg.inv(m[:, :2])
-    t_inv = -a_inv @ m[:, 2]
+    inv = inverse_map(m)
+    a_inv, t_inv = inv[:, :2], inv[:, 2]
     xs, ys = np.meshgrid(np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64))
     sx = a_inv[0, 0] * xs + a_inv[0, 1] * ys + t_inv[0]
     sy = a_inv[1, 0] * xs + a_inv[1, 1] * ys + t_inv[1]
@@ -109,21 +109,35 @@ def warp(img: np.ndarray, m: np.ndarray) -> np.ndarray:
     return out
 
 
-def make_pair(size: int = 1024, seed: int = 0, theta_deg: float | None = None,
-              scale_jitter: float = 0.0, looks: int | None = 4,
-              sigma_scale: float | None = None, radiometric: bool = True):
-    """(image1, image2, truth) per the BASELINE.json generator, float64."""
+def _pair_draws(size: int, seed: int, theta_deg, scale_jitter: float, looks):
+    """The per-pair parameter draws of make_pair, in its order; returns the
+    truth and the generator (positioned at the speckle draws)."""
     rng = np.random.default_rng(10_000 + seed)
-    if sigma_scale is None:
-        sigma_scale = 4.0 if size >= 4096 else 1.0
-    img1 = blob_field(size, seed, sigma_scale=sigma_scale)
     theta = float(rng.uniform(0.0, 360.0)) if theta_deg is None else float(theta_deg)
     scale = float(rng.uniform(1.0 - scale_jitter, 1.0 + scale_jitter)) if scale_jitter else 1.0
     t = tuple(float(v) for v in rng.uniform(-20.0, 20.0, 2))
     m = similarity(size, theta, scale, t)
-    img2 = warp(img1, m)
     inverted = bool(rng.uniform() < 0.5)
     gamma = float(rng.uniform(0.4, 2.5))
+    return PairTruth(theta, scale, t, inverted, gamma, looks or 0, size, m), rng
+
+
+def inverse_map(m: np.ndarray) -> np.ndarray:
+    """2x3 target->source map of a 2x3 source->target affine, as `warp` forms it."""
+    a_inv = np.linalg.inv(m[:, :2])
+    return np.concatenate([a_inv, (-a_inv @ m[:, 2])[:, None]], axis=1)
+
+
+def make_pair(size: int = 1024, seed: int = 0, theta_deg: float | None = None,
+              scale_jitter: float = 0.0, looks: int | None = 4,
+              sigma_scale: float | None = None, radiometric: bool = True):
+    """(image1, image2, truth) per the BASELINE.json generator, float64."""
+    if sigma_scale is None:
+        sigma_scale = 4.0 if size >= 4096 else 1.0
+    img1 = blob_field(size, seed, sigma_scale=sigma_scale)
+    truth, rng = _pair_draws(size, seed, theta_deg, scale_jitter, looks)
+    img2 = warp(img1, truth.matrix)
+    inverted, gamma = truth.inverted, truth.gamma
     if radiometric:
         if inverted:
             img2 = 1.0 - img2
@@ -131,7 +145,6 @@ def make_pair(size: int = 1024, seed: int = 0, theta_deg: float | None = None,
         if looks:
             img2 = img2 * rng.gamma(float(looks), 1.0 / looks, img2.shape)
         img2 = (img2 - img2.min()) / max(img2.max() - img2.min(), 1e-12)
-    truth = PairTruth(theta, scale, t, inverted, gamma, looks or 0, size, m)
     return img1, img2, truth
 
 
@@ -143,4 +156,37 @@ def make_batch(n_pairs: int, size: int = 1024, seed0: int = 0, dtype=np.float32,
         a, b, tr = make_pair(size, seed0 + i, **kw)
         out[2 * i], out[2 * i + 1] = a, b
         truths.append(tr)
+    return out, truths
+
+
+def make_batch_device(n_pairs: int, size: int = 1024, seed0: int = 0, device="cuda", speckle_seed: int | None = None,
+                      theta_deg: float | None = None, scale_jitter: float = 0.0, looks: int | None = 4,
+                      sigma_scale: float | None = None, radiometric: bool = True):
+    """make_batch with the target side synthesised on the GPU
+    (rift2_synth_targets): image 1 and the per-pair draws (hence the truths)
+    are the host generator's; the warp, inversion, gamma and renormalisation
+    match make_pair to float32 rounding (pow on the device is within 2 ulp);
+    the speckle is drawn from Philox4x32-10 (key speckle_seed, default
+    seed0; counter word 2 = pair index) instead of numpy's stream.
+    Returns the (2 * n_pairs, size, size) float32 CUDA stack and the truths."""
+    import torch
+    from . import engine
+    if sigma_scale is None:
+        sigma_scale = 4.0 if size >= 4096 else 1.0
+    src = np.empty((n_pairs, size, size))
+    params = np.zeros((n_pairs, 8))
+    truths = []
+    for i in range(n_pairs):
+        src[i] = blob_field(size, seed0 + i, sigma_scale=sigma_scale)
+        tr, _ = _pair_draws(size, seed0 + i, theta_deg, scale_jitter, looks)
+        params[i, :6] = inverse_map(tr.matrix).ravel()
+        params[i, 6] = tr.gamma
+        params[i, 7] = (1 if tr.inverted else 0) | (2 if radiometric else 0)
+        truths.append(tr)
+    out = torch.empty((2 * n_pairs, size, size), dtype=torch.float32, device=device)
+    d_src = torch.from_numpy(src).to(device)
+    d_par = torch.from_numpy(params).to(device)
+    d_looks = torch.full((n_pairs,), int(looks or 0), dtype=torch.int32, device=device)
+    engine.synth_targets(d_src, d_par, d_looks, seed0 if speckle_seed is None else speckle_seed, out[1::2],
+                         src_copy=out[0::2])
     return out, truths

@@ -1,0 +1,134 @@
+"""On-device target synthesis (rift2_synth_targets) against
+the CPU checker oracle/synth_oracle.py and the host generator.
+
+Bars: the warp alone (no radiometry) is bit-exact; with the radiometry the
+float32 targets agree within one float32 ulp of 1.0 (2^-24 ... 2^-23: the
+device pow / log are within 2 ulp of the host libm, which can flip a float32
+rounding) and the large majority of pixels are bit-equal."""
+
+import numpy as np
+import pytest
+
+from oracle import synth_oracle as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2.0 ** -23
+
+
+@pytest.fixture(scope="module")
+def eng():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2303_00319_b200 import engine
+    return engine
+
+
+def _run(eng, srcs, params, looks, seed=7, first_image=0, copy=False):
+    n, H, W = srcs.shape
+    d_src = torch.from_numpy(np.ascontiguousarray(srcs, np.float64)).cuda()
+    d_par = torch.from_numpy(np.asarray(params, np.float64).reshape(n, 8)).cuda()
+    d_looks = torch.tensor(looks, dtype=torch.int32, device="cuda")
+    out = torch.full((2 * n, H, W), -1.0, dtype=torch.float32, device="cuda")
+    eng.synth_targets(d_src, d_par, d_looks, seed, out[1::2], first_image=first_image,
+                      src_copy=out[0::2] if copy else None)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    return o[1::2], o[0::2]
+
+
+def _params(inv, gamma, inverted, radiometric=True):
+    return list(np.asarray(inv, np.float64).ravel()) + [gamma, (1 if inverted else 0) | (2 if radiometric else 0)]
+
+
+def _check(got, want):
+    d = np.abs(got.astype(np.float64) - want.astype(np.float32).astype(np.float64))
+    assert d.max() <= TOL, d.max()
+    assert (d == 0).mean() >= 0.99
+
+
+@pytest.mark.parametrize("theta,jitter,seed", [(0.0, 0.0, 0), (90.0, 0.0, 1), (37.5, 0.1, 2), (180.0, 0.05, 3),
+                                               (271.0, 0.1, 4)])
+def test_warp_only_bit_exact(eng, theta, jitter, seed):
+    from paper_2303_00319_b200 import synth
+    img = synth.blob_field(128, seed)
+    tr, _ = synth._pair_draws(128, seed, theta, jitter, None)
+    got, _ = _run(eng, img[None], [_params(synth.inverse_map(tr.matrix), 1.0, False, radiometric=False)], [0])
+    assert np.array_equal(got[0], synth.warp(img, tr.matrix).astype(np.float32))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4, 5])
+def test_radiometry_matches_make_pair(eng, seed):
+    from paper_2303_00319_b200 import synth
+    img1, img2, tr = synth.make_pair(128, seed, theta_deg=None, scale_jitter=0.1, looks=None)
+    got, _ = _run(eng, img1[None], [_params(synth.inverse_map(tr.matrix), tr.gamma, tr.inverted)], [0])
+    _check(got[0], img2)
+
+
+@pytest.mark.parametrize("looks", [1, 4, 16])
+def test_speckle_matches_checker(eng, looks):
+    from paper_2303_00319_b200 import synth
+    n = 3
+    srcs, params, want = [], [], []
+    for i in range(n):
+        img = synth.blob_field(96, 40 + i)
+        tr, _ = synth._pair_draws(96, 40 + i, None, 0.1, looks)
+        inv = synth.inverse_map(tr.matrix)
+        srcs.append(img)
+        params.append(_params(inv, tr.gamma, tr.inverted))
+        want.append(S.synth_target(img, inv, tr.inverted, tr.gamma, looks, seed=99, image=10 + i))
+    got, _ = _run(eng, np.stack(srcs), params, [looks] * n, seed=99, first_image=10)
+    for i in range(n):
+        _check(got[i], want[i])
+
+
+def test_non_square_and_copy(eng):
+    rng = np.random.default_rng(0)
+    H, W = 70, 133
+    srcs = rng.random((2, H, W))
+    th = np.radians(23.0)
+    inv = np.array([[np.cos(th), np.sin(th), -8.5], [-np.sin(th), np.cos(th), 20.25]]) * [[0.95], [0.95]]
+    inv[:, 2] = [-8.5, 20.25]
+    params = [_params(inv, 0.7, True), _params(inv, 1.9, False)]
+    got, copy = _run(eng, srcs, params, [4, 0], seed=5, copy=True)
+    assert np.array_equal(copy, srcs.astype(np.float32))
+    for i, (g, inverted, looks) in enumerate([(0.7, True, 4), (1.9, False, 0)]):
+        _check(got[i], S.synth_target(srcs[i], inv, inverted, g, looks, seed=5, image=i))
+
+
+def test_seeds_and_determinism(eng):
+    from paper_2303_00319_b200 import synth
+    img = synth.blob_field(64, 1)
+    p = [_params(synth.inverse_map(synth.similarity(64, 10.0, 1.0, (1.0, 2.0))), 1.2, False)]
+    a, _ = _run(eng, img[None], p, [4], seed=1)
+    b, _ = _run(eng, img[None], p, [4], seed=1)
+    c, _ = _run(eng, img[None], p, [4], seed=2)
+    assert np.array_equal(a, b)
+    assert not np.array_equal(a, c)
+    assert a.min() == 0.0 and a.max() == 1.0
+
+
+def test_make_batch_device(eng):
+    from paper_2303_00319_b200 import synth
+    host, th = synth.make_batch(3, 128, seed0=11, looks=None, scale_jitter=0.1)
+    dev, td = synth.make_batch_device(3, 128, seed0=11, looks=None, scale_jitter=0.1)
+    dev = dev.cpu().numpy()
+    assert np.array_equal(dev[0::2], host[0::2])
+    d = np.abs(dev[1::2].astype(np.float64) - host[1::2].astype(np.float64))
+    assert d.max() <= TOL and (d == 0).mean() >= 0.99
+    for a, b in zip(th, td):
+        assert np.array_equal(a.matrix, b.matrix) and (a.gamma, a.inverted) == (b.gamma, b.inverted)
+    spk, _ = synth.make_batch_device(2, 128, seed0=11, looks=4)
+    assert torch.isfinite(spk).all() and float(spk[1::2].min()) == 0.0 and float(spk[1::2].max()) == 1.0
+
+
+def test_argument_errors(eng):
+    from paper_2303_00319_b200.errors import ParameterError
+    src = torch.zeros((2, 16, 16), dtype=torch.float64, device="cuda")
+    dst = torch.zeros((2, 16, 16), dtype=torch.float32, device="cuda")
+    looks = torch.zeros(2, dtype=torch.int32, device="cuda")
+    with pytest.raises(ParameterError):
+        eng.synth_targets(src, torch.zeros((2, 7), dtype=torch.float64, device="cuda"), looks, 0, dst)
+    with pytest.raises(ParameterError):
+        eng.synth_targets(src.float(), torch.zeros((2, 8), dtype=torch.float64, device="cuda"), looks, 0, dst)
