@@ -625,6 +625,8 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
   __shared__ unsigned s_n, s_base;
   const int plane = blockIdx.y;
   const unsigned b0 = info[plane].bin[0], b1 = info[plane].bin[1];
+  const unsigned lo_bits = (b0 < b1 ? b0 : b1) << 19;
+  const unsigned rng_bits = ((b0 < b1 ? b1 - b0 : b0 - b1) + 1u) << 19;
   const float* Ap = amp0 + (size_t)plane * n;
   const float4* A = reinterpret_cast<const float4*>(Ap);
   unsigned* out = cand + (size_t)plane * n;
@@ -633,32 +635,44 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
   const unsigned lane = threadIdx.x & 31;
   const unsigned per_pass = kCollectVec * blockDim.x;
   for (unsigned base = blockIdx.x * per_pass; base < n4; base += gridDim.x * per_pass) {
-    if (threadIdx.x == 0) s_n = 0;
+    if (threadIdx.x == 0) {
+      s_n = 0;
+      // this CTA's next pass streams into L2 while this one filters / writes
+      const unsigned next = base + gridDim.x * per_pass;
+      if (vec && next < n4) l2_prefetch(A + next, (n4 - next < per_pass ? n4 - next : per_pass) * 16u);
+    }
     __syncthreads();
     float4 qv[kCollectVec];
+    if (vec && base + per_pass <= n4) {
 #pragma unroll
-    for (int k = 0; k < kCollectVec; ++k) {
-      const unsigned i = base + k * blockDim.x + threadIdx.x;
-      qv[k] = make_float4(-1.f, -1.f, -1.f, -1.f);
-      if (vec && 4 * i + 3 < n) qv[k] = __ldg(&A[i]);
-      else if (i < n4) {
-        qv[k].x = Ap[4 * i];
-        if (4 * i + 1 < n) qv[k].y = Ap[4 * i + 1];
-        if (4 * i + 2 < n) qv[k].z = Ap[4 * i + 2];
-        if (4 * i + 3 < n) qv[k].w = Ap[4 * i + 3];
+      for (int k = 0; k < kCollectVec; ++k) qv[k] = __ldg(&A[base + k * blockDim.x + threadIdx.x]);
+    } else {
+      // tail: padding bits 0xFFFFFFFF never fall in the bin range below
+      const float pad = __uint_as_float(0xFFFFFFFFu);
+#pragma unroll
+      for (int k = 0; k < kCollectVec; ++k) {
+        const unsigned i = base + k * blockDim.x + threadIdx.x;
+        qv[k] = make_float4(pad, pad, pad, pad);
+        if (vec && 4 * i + 3 < n) qv[k] = __ldg(&A[i]);
+        else if (i < n4) {
+          qv[k].x = Ap[4 * i];
+          if (4 * i + 1 < n) qv[k].y = Ap[4 * i + 1];
+          if (4 * i + 2 < n) qv[k].z = Ap[4 * i + 2];
+          if (4 * i + 3 < n) qv[k].w = Ap[4 * i + 3];
+        }
       }
     }
-    // per-thread hit mask over its 16 values, one warp prefix sum, one
+    // per-thread hit mask over its 32 values: one unsigned range test on the
+    // float bits (bins b_lo..b_hi; bins between them are empty, so the range
+    // holds exactly the values of the two bins), one warp prefix sum, one
     // shared atomic per warp, then each thread writes its own hits
     unsigned mask = 0;
 #pragma unroll
     for (int k = 0; k < kCollectVec; ++k) {
       const float vals[4] = {qv[k].x, qv[k].y, qv[k].z, qv[k].w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const unsigned hb = __float_as_uint(vals[e]) >> 19;
-        mask |= (vals[e] >= 0.f && (hb == b0 || hb == b1)) ? (1u << (4 * k + e)) : 0u;
-      }
+      for (int e = 0; e < 4; ++e)
+        mask |= (__float_as_uint(vals[e]) - lo_bits < rng_bits ? 1u : 0u) << (4 * k + e);
     }
     const unsigned cntt = __popc(mask);
     unsigned incl = cntt;
@@ -675,6 +689,7 @@ __global__ void __launch_bounds__(256) k_med_collect(const float* __restrict__ a
     if (mask) {                                     // static indices: qv stays in registers
 #pragma unroll
       for (int k = 0; k < kCollectVec; ++k) {
+        if (!((mask >> (4 * k)) & 0xFu)) continue;  // ~3 % of values hit: most groups are empty
         const float vals[4] = {qv[k].x, qv[k].y, qv[k].z, qv[k].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e)
@@ -727,6 +742,8 @@ __global__ void __launch_bounds__(256) k_med_h2(const unsigned* __restrict__ can
   const int plane = blockIdx.y;
   const unsigned c = cnt[plane];
   const unsigned b0 = info[plane].bin[0], b1 = info[plane].bin[1];
+  const unsigned lo_bits = (b0 < b1 ? b0 : b1) << 19;
+  const unsigned rng_bits = ((b0 < b1 ? b1 - b0 : b0 - b1) + 1u) << 19;
   const unsigned* cd = cand + (size_t)plane * n;
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -1560,7 +1577,11 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   const unsigned n = (unsigned)((size_t)H * W);
   k_med_bins<<<B * c.O, 1024, 0, st>>>(hist, info, n);
   {
-    dim3 grid((unsigned)min((size_t)64, ((size_t)n / 4 + 255) / 256 + 1), B * c.O);
+    // one resident wave: each CTA streams many passes of its plane
+    const int waves = resident_ctas((const void*)k_med_collect, 256, 0);
+    const size_t gx = std::max<size_t>(1, std::min<size_t>(((size_t)n / 4 + 255) / 256 + 1,
+                                                           (size_t)waves / (size_t)(B * c.O)));
+    dim3 grid((unsigned)gx, B * c.O);
     k_med_collect<<<grid, 256, 0, st>>>(amp0, info, cand, cnt, n);
   }
   launch_med_select(cand, cnt, info, reinterpret_cast<unsigned*>(w + p.off_mh), thr, B * c.O, n, c.thr_factor, st);
