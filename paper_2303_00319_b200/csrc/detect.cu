@@ -174,7 +174,7 @@ R2_DEV double tile_score(const T (*sv)[kIn + 1], int sy, int sx, int y, int x, i
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k_fast_nms(const T* __restrict__ mins, const T* __restrict__ maxs, int H, int W,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 6 : 1) k_fast_nms(const T* __restrict__ mins, const T* __restrict__ maxs, int H, int W,
                                                   const unsigned long long* __restrict__ mm, double thr,
                                                   int margin, int nm, K128* __restrict__ cand,
                                                   unsigned* __restrict__ cnt, size_t cap) {
@@ -589,6 +589,10 @@ int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, siz
   }
   {
     dim3 grid((a.W + kTile - 1) / kTile, (a.H + kTileY - 1) / kTileY, planes);
+    // 6 resident CTAs of ~30 KB static shared memory: ask for the full carveout
+    static const bool carveout = cudaFuncSetAttribute(k_fast_nms<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                      cudaSharedmemCarveoutMaxShared) == cudaSuccess;
+    (void)carveout;
     k_fast_nms<T><<<grid, 256, 0, st>>>(mins, maxs, a.H, a.W, mm, a.threshold, a.margin, nm, cand, cnt, p.cap);
   }
   {
