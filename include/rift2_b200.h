@@ -113,7 +113,10 @@ int32_t rift2_detect_f64(const double* min_maps, const double* max_maps, int32_t
  *   desc_variant [batch][desc_capacity] uint8 out: dominant index / layer
  *   desc_count   [batch] int32 out, desc_skipped [batch] int32 out
  * Descriptors are ordered by keypoint, then [peak, runner-up] (rift2) or
- * layer 1..n (ring).  mode: 0 plain, 1 ring, 2 rift2. */
+ * layer 1..n (ring).  mode: 0 plain, 1 ring, 2 rift2.
+ * desc_capacity must be >= rows-per-keypoint (1 plain, n_orient ring,
+ * 2 rift2) x kp_stride, else RIFT2_CAPACITY; kp_count values above
+ * kp_stride are clamped to it. */
 int32_t rift2_describe_workspace_size(int32_t batch, int32_t kp_stride, int32_t grid, int32_t n_orient,
                                       size_t* bytes);
 int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
@@ -160,10 +163,14 @@ int32_t rift2_match(const void* desc_counts, const int32_t* desc_sqnorm, const i
  *   Reference keypoint ids are taken from desc_kp, so a slice must carry
  *   global keypoint ids.  No workspace.
  * rift2_match_finish: parts [n_parts][n_pairs][desc_capacity] (the gathered
- *   partial arrays, any order of ranks); the descriptor arrays must hold the
- *   FULL reference and target sets (for variant grouping and the float64
- *   distance of each winner); outputs and workspace as rift2_match
- *   (rift2_match_workspace_size). */
+ *   partial arrays, any order of ranks); the target block must hold the
+ *   FULL target set, the reference block may hold only this rank's slice
+ *   (global keypoint ids, desc_capacity > every keypoint id): the winner of
+ *   every target keypoint is exact and identical on all ranks, its float64
+ *   distance is computed where the winner's reference rows are present and
+ *   reported as +inf elsewhere (the rank owning the row supplies it, so
+ *   reference rows never cross ranks); outputs and workspace as
+ *   rift2_match (rift2_match_workspace_size). */
 typedef struct rift2_match_part {
   int32_t dot;          /* integer dot product of the count vectors */
   int32_t ref_sqnorm;   /* sum of squared reference counts */

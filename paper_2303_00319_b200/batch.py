@@ -15,12 +15,17 @@ later, with results identical to `step()`.
 
 from __future__ import annotations
 
+import itertools
+
 import numpy as np
 import torch
 
 from . import engine
 from .config import RiftConfig
 from .errors import ParameterError
+
+
+_INSTANCE_IDS = itertools.count()
 
 
 class BatchPipeline:
@@ -58,16 +63,21 @@ class BatchPipeline:
         self.rb = torch.arange(0, B, 2, dtype=torch.int32, device=d)
         self.tb = self.rb + 1
         self.dim = self.cfg.grid * self.cfg.grid * self.cfg.n_orient
+        # workspace keys private to this pipeline: its captured graphs hold
+        # the scratch addresses, so no other caller may grow or share them
+        self._ws = f"bp{next(_INSTANCE_IDS)}_"
         self.graphs = None
         self._alt = None
         self._copy_stream = None
 
     # ---- stages (eager) --------------------------------------------------
     def run_fields(self, images=None, f=None, ws: str = "b_"):
+        ws = self._ws + ws
         engine.fields(self.images if images is None else images, self.bank, out=self.f if f is None else f,
                       ws_key=ws + "fields")
 
     def run_features(self, f=None, ws: str = "b_"):
+        ws = self._ws + ws
         f = self.f if f is None else f
         c = self.cfg
         engine.detect(f["mmin"], f["mmax"], c.fast_threshold, self.K, c.patch_size // 2, ws_key=ws + "detect",

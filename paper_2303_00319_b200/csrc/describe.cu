@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   if (threadIdx.x == 0) s_k = (int)atomicAdd(&ticket[b], 1u);
   __syncthreads();
   const int k = s_k;
-  if (k >= a.kp_count[b]) return;                 // no live keypoint follows
+  if (k >= min(a.kp_count[b], a.kp_stride)) return;   // no live keypoint follows
   unsigned long long* lb = chain + (size_t)b * a.kp_stride;
   const int x = a.kp_x[(size_t)b * a.kp_stride + k], y = a.kp_y[(size_t)b * a.kp_stride + k];
   const int x0 = x + 1 - (c.P + 1) / 2, y0 = y + 1 - (c.P + 1) / 2;   // floor(kp + 1 - P/2)

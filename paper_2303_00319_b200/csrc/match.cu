@@ -205,7 +205,8 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
   const int split = blockIdx.x % p.splits;
   const int mt = blockIdx.x / p.splits;
   const int rb = p.ref_block[pair], tb = p.tgt_block[pair];
-  const int n_t = p.count[tb], n_r = p.count[rb];
+  // counts past the buffer capacity are clamped (the rows do not exist)
+  const int n_t = min(p.count[tb], p.cap), n_r = min(p.count[rb], p.cap);
   if (mt * BM >= n_t) return;
   const int n_tiles_all = (n_r + BN - 1) / BN;
   const int per = (n_tiles_all + p.splits - 1) / p.splits;
@@ -446,13 +447,14 @@ __global__ void __launch_bounds__(1024) k_match_index(MatchArgs a, IdxWs w) {
   __shared__ int s_base, s_tot;
   const int pair = blockIdx.x;
   const int tb = a.tgt_block[pair], rb = a.ref_block[pair];
-  const int n_t = a.count[tb], n_r = a.count[rb];
+  const int n_t = min(a.count[tb], a.cap), n_r = min(a.count[rb], a.cap);
   const int* tk = a.kp + (size_t)tb * a.cap;
   const int* rk = a.kp + (size_t)rb * a.cap;
   int* gs = w.gstart + (size_t)pair * (a.cap + 1);
   int* rs = w.rstart + (size_t)pair * a.cap;
   int* re = w.rend + (size_t)pair * a.cap;
   for (int i = threadIdx.x; i < n_r; i += blockDim.x) {
+    if ((unsigned)rk[i] >= (unsigned)a.cap) continue;   // ids outside [0, cap) break the ABI precondition
     if (i == 0 || rk[i] != rk[i - 1]) rs[rk[i]] = i;
     if (i == n_r - 1 || rk[i + 1] != rk[i]) re[rk[i]] = i + 1;
   }
@@ -523,8 +525,10 @@ __global__ void __launch_bounds__(256) k_match_combine(MatchArgs a, IdxWs w, con
   const int tkp = a.kp[(size_t)tb * a.cap + t0];
   double dmin = 0.0;
   if (best.kp >= 0) {
+    // a winner outside this call's reference rows (row-sharded finish: the
+    // rank owning it computes the distance) reports +inf
     const int r0 = w.rstart[(size_t)pair * a.cap + best.kp], r1 = w.rend[(size_t)pair * a.cap + best.kp];
-    dmin = 1e300;
+    dmin = r1 > r0 ? 1e300 : INFINITY;
     for (int r = r0; r < r1; ++r) {
       const double ir = 1.0 / sqrt((double)a.sqnorm[(size_t)rb * a.cap + r]);
       const __half* cr = a.counts + ((size_t)rb * a.cap + r) * a.stride;
@@ -562,6 +566,7 @@ constexpr int kMsCtas = 16;
 R2_DEV int ms_bin(const K128& k) {
   // distances of unit vectors lie in [0, 2]: linear bins, monotone in the key
   const double d = __longlong_as_double((long long)k.hi);
+  if (!(d < 2.0)) return kMsBins - 1;             // includes the +inf of a non-local winner
   const int v = (int)(d * (kMsBins / 2));
   return v < 0 ? 0 : (v >= kMsBins ? kMsBins - 1 : v);
 }
@@ -875,6 +880,9 @@ int match_finish_run(const MatchArgs& a, const void* parts, int n_parts, void* w
                      cudaStream_t st) {
   const MatchWs p = plan_match(a.n_pairs, a.cap);
   if (ws_bytes < p.total) return 1;
+  // the reference rows may be a slice: keypoints without rows get empty ranges
+  cudaMemsetAsync(static_cast<char*>(ws) + p.off_rstart, 0, (size_t)a.n_pairs * a.cap * sizeof(int), st);
+  cudaMemsetAsync(static_cast<char*>(ws) + p.off_rend, 0, (size_t)a.n_pairs * a.cap * sizeof(int), st);
   finish_launch(a, static_cast<const Part*>(parts), n_parts,
                 PartLayout{(size_t)a.cap, 1, (size_t)a.n_pairs * a.cap}, p, static_cast<char*>(ws), st);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;

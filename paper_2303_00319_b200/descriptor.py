@@ -55,7 +55,8 @@ class DescriptorSet:
 
 def _mim_device(mim):
     import torch
-    dev = getattr(mim, "device", None)
+    from . import _devcache
+    dev = _devcache.lookup(mim.indices)
     if dev is not None:
         return dev
     idx = np.asarray(mim.indices)

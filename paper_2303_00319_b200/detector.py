@@ -14,6 +14,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _devcache
 from .errors import ParameterError
 
 ARC_LENGTH = 9
@@ -98,9 +99,9 @@ def detect_keypoints(pc, threshold: float = 0.001, max_points: int = 5000, patch
         raise ParameterError(f"image {h}x{w} smaller than the {patch_size}-pixel descriptor patch")
     if threshold <= 0:
         raise ParameterError("FAST threshold must be positive")
-    dev = getattr(pc, "device", None)
-    if dev is not None and "mmin" in dev:
-        mins, maxs = dev["mmin"][None], dev["mmax"][None]
+    dmin, dmax = _devcache.lookup(pc.moment_min), _devcache.lookup(pc.moment_max)
+    if dmin is not None and dmax is not None:
+        mins, maxs = dmin[None], dmax[None]
     else:
         mins, maxs = _device_map(pc.moment_min)[None], _device_map(pc.moment_max)[None]
         if mins.dtype != maxs.dtype:

@@ -28,13 +28,23 @@ def _stream() -> int:
 
 
 class _Workspaces:
+    """Scratch buffers per (device, key), grown on demand.  A grown buffer's
+    predecessor is retired, not freed: a CUDA graph captured earlier may
+    still hold its address, and replaying it must not touch memory the
+    caching allocator has handed to someone else.  Callers that run
+    concurrently (e.g. two BatchPipelines on different streams) use distinct
+    keys, so they never share scratch."""
+
     def __init__(self):
         self._bufs = {}
+        self._retired = []
 
     def get(self, key: str, nbytes: int) -> torch.Tensor:
         dev = torch.cuda.current_device()
         buf = self._bufs.get((dev, key))
         if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                self._retired.append(buf)
             buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=f"cuda:{dev}")
             self._bufs[(dev, key)] = buf
         return buf

@@ -5,7 +5,7 @@ module holds the parameter/result types the callers exchange."""
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -56,14 +56,13 @@ class BankParams:
 @dataclass(frozen=True)
 class PCField:
     """Per-orientation amplitude sums, phase congruency and moment maps
-    (ref: loggabor.py:106-119).  `device` optionally carries the GPU's own
-    float32 moment maps so a following detect_keypoints skips the upload."""
+    (ref: loggabor.py:106-119).  Maps produced by compute_fields are
+    read-only and keep a device copy (_devcache) that detect_keypoints reuses."""
 
     a_o: np.ndarray
     pc_per_orientation: np.ndarray
     moment_max: np.ndarray
     moment_min: np.ndarray
-    device: dict | None = field(default=None, compare=False, repr=False)
 
     @property
     def shape(self):

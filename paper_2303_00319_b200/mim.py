@@ -4,7 +4,7 @@ argmax over orientation amplitude sums of ref: mim.py:43-55)."""
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -16,7 +16,6 @@ class IndexMap:
     indices: np.ndarray        # int32 in [1, n_orient]
     max_amplitude: np.ndarray  # float64
     n_orient: int
-    device: object = field(default=None, compare=False, repr=False)   # uint8 CUDA copy
 
     def __post_init__(self):
         if np.shape(self.indices) != np.shape(self.max_amplitude):

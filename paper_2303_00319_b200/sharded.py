@@ -7,23 +7,28 @@ keypoints per image, the distance matrix row-sharded across GPUs):
    deterministic, so all ranks hold identical keypoint lists.
 2. Rank r describes only its contiguous slice [n*r/G, n*(r+1)/G) of each
    image's keypoints (keypoint ids stay global).
-3. The descriptor slices are all-gathered.  Image 2's (the targets) are
-   needed in full by every rank; image 1's reference rows are needed for
-   the float64 distance of each winner.  Concatenating slices in rank order
-   reproduces the single-GPU descriptor order exactly.
+3. Image 2's descriptor slices (the targets) are all-gathered -- the one
+   data-path collective `north_star` names.  Concatenating slices in rank
+   order reproduces the single-GPU descriptor order exactly.  Image 1's
+   reference rows never leave their rank.
 4. Each rank matches all target descriptors against its own reference slice
    (rift2_match_partial: the tensor-core GEMM with the exact running argmax).
 5. The per-target partial bests (16 bytes per target row) are all-gathered
-   and combined exactly (rift2_match_finish: variant groups, exact integer
-   comparison, ties to the smallest reference keypoint id, float64
-   distances, (dist, ref, tgt) order).  The result equals the single-GPU
-   match_nn bit for bit.
+   and combined exactly on every rank (rift2_match_finish on the local
+   reference slice: variant groups, exact integer comparison, ties to the
+   smallest reference keypoint id).  The winner of each target keypoint is
+   the same on every rank; its float64 distance is computed by the rank
+   that owns the winner's reference rows (+inf elsewhere).
+6. The (ref, tgt, dist) triples (16 bytes per target keypoint) are
+   all-gathered, each target keeps the finite distance, and the set is
+   sorted by (dist, ref, tgt).  The result equals the single-GPU match_nn
+   bit for bit.
 
-Collectives: four all-gathers of sizes/rows per image plus one of the
-partials; no reduction touches floating point.  The kernels and the
-collective are injected (`backend`, `group`), so the same orchestration runs
-the GPU path (NCCL) and, in tests/test_multirank.py, a CPU backend under
-gloo.
+Collectives: all-gathers of image 2's descriptor rows, of the partials and
+of the per-target triples; no reduction touches floating point.  The kernels
+and the collective are injected (`backend`, `group`), so the same
+orchestration runs the GPU path (NCCL) and, in tests/test_multirank.py, a
+CPU backend under gloo.
 """
 
 from __future__ import annotations
@@ -132,19 +137,71 @@ class GpuBackend:
         parts = engine.match_partial(desc, dim, rb, tb)
         return parts[0, :n_t].contiguous()
 
-    def finish(self, parts_all: torch.Tensor, ref_full: dict, tgt_full: dict, n_ref_kp: int, n_tgt_kp: int,
-               dim: int):
+    def finish_local(self, parts_all: torch.Tensor, ref_local: dict, tgt_full: dict, n_ref_kp: int,
+                     n_tgt_kp: int, dim: int):
+        """Exact combine of the gathered partials against this rank's
+        reference slice -> (ref, tgt, dist) numpy arrays, one per target
+        keypoint; dist is +inf where the winner's rows live on another rank."""
         from . import engine
         G, n_t = parts_all.shape[:2]
+        n_r = ref_local["counts"].shape[0]
+        if n_r == 0 or n_t == 0:
+            return np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.float64)
         # keypoint ids index per-pair tables of `cap` entries
-        cap = max(ref_full["counts"].shape[0], n_t, n_ref_kp, n_tgt_kp, 1)
-        desc, rb, tb = self._pack(ref_full, tgt_full, cap)
+        cap = max(n_r, n_t, n_ref_kp, n_tgt_kp, 1)
+        desc, rb, tb = self._pack(ref_local, tgt_full, cap)
         parts = torch.zeros((G, 1, cap, 4), dtype=torch.int32, device=parts_all.device)
         parts[:, 0, :n_t] = parts_all
         out = engine.match_finish(parts, desc, dim, rb, tb, n_tgt_kp)
         m = int(out["count"][0])
         return (out["ref"][0, :m].cpu().numpy(), out["tgt"][0, :m].cpu().numpy(),
                 out["dist"][0, :m].cpu().numpy())
+
+
+def merge_triples(parts) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Every rank's (ref, tgt, dist) triples -> one per target keypoint with
+    the finite distance (supplied by the winner's owner), sorted by (dist,
+    ref, tgt) like ref: matcher.py:143-146."""
+    ref = np.concatenate([np.asarray(p[0], np.int64) for p in parts]) if parts else np.zeros(0, np.int64)
+    tgt = np.concatenate([np.asarray(p[1], np.int64) for p in parts]) if parts else np.zeros(0, np.int64)
+    dst = np.concatenate([np.asarray(p[2], np.float64) for p in parts]) if parts else np.zeros(0)
+    best = {}
+    for r, t, d in zip(ref.tolist(), tgt.tolist(), dst.tolist()):
+        cur = best.get(t)
+        if cur is not None and cur[0] != r:
+            raise RuntimeError(f"ranks disagree on the winner of target keypoint {t}: {cur[0]} vs {r}")
+        if cur is None or d < cur[1]:
+            best[t] = (r, d)
+    trip = sorted(((r, t, d) for t, (r, d) in best.items()), key=lambda p: (p[2], p[0], p[1]))
+    if any(not np.isfinite(d) for _, _, d in trip):
+        raise RuntimeError("a winner's distance was supplied by no rank")
+    return (np.array([p[0] for p in trip], np.int64), np.array([p[1] for p in trip], np.int64),
+            np.array([p[2] for p in trip], np.float64))
+
+
+def gather_triples(ref, tgt, dst, group=None):
+    """All-gather each rank's triples (sizes may differ) as a list per rank."""
+    rank, world = _world(group)
+    if world == 1:
+        return [(ref, tgt, dst)]
+    packed = torch.from_numpy(np.stack([np.asarray(ref, np.float64), np.asarray(tgt, np.float64),
+                                        np.asarray(dst, np.float64)], 1)) if len(ref) else torch.zeros((0, 3),
+                                                                                                       dtype=torch.float64)
+    dev = torch.device("cuda", torch.cuda.current_device()) if (dist.get_backend(group) == "nccl") else torch.device("cpu")
+    n = torch.tensor([packed.shape[0]], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(x.item()) for x in sizes]
+    m = max(max(sizes), 1)
+    pad = torch.zeros((m, 3), dtype=torch.float64, device=dev)
+    pad[:packed.shape[0]] = packed.to(dev)
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    out = []
+    for b, k in zip(bufs, sizes):
+        a = b[:k].cpu().numpy()
+        out.append((a[:, 0].astype(np.int64), a[:, 1].astype(np.int64), a[:, 2]))
+    return out
 
 
 def match_pair_sharded(ref_image, tgt_image, cfg: RiftConfig | None = None, group=None, backend=None):
@@ -156,17 +213,18 @@ def match_pair_sharded(ref_image, tgt_image, cfg: RiftConfig | None = None, grou
     rank, world = _world(group)
     dim = cfg.grid * cfg.grid * cfg.n_orient
     feats = [backend.features(img, cfg) for img in (ref_image, tgt_image)]   # replicated
-    local, full = [], []
-    for f in feats:
-        k0, k1 = kp_range(f["n"], rank, world)
-        loc = backend.describe_slice(f, k0, k1, cfg)
-        local.append(loc)
-        full.append({k: gather_rows(v, group) for k, v in loc.items()})
-    parts = backend.partial(local[0], full[1], dim)
+    slices = [kp_range(f["n"], rank, world) for f in feats]
+    ref_local = backend.describe_slice(feats[0], *slices[0], cfg)
+    tgt_local = backend.describe_slice(feats[1], *slices[1], cfg)
+    tgt_full = {k: gather_rows(v, group) for k, v in tgt_local.items()}     # image 2 only
+    parts = backend.partial(ref_local, tgt_full, dim)
     parts_all = gather_equal(parts, group)
-    ref, tgt, dst = backend.finish(parts_all, full[0], full[1], feats[0]["n"], feats[1]["n"], dim)
-    n_r, n_t = full[0]["counts"].shape[0], full[1]["counts"].shape[0]
+    mine = backend.finish_local(parts_all, ref_local, tgt_full, feats[0]["n"], feats[1]["n"], dim)
+    ref, tgt, dst = merge_triples(gather_triples(*mine, group=group))
+    n_r_local = int(ref_local["counts"].shape[0])
+    n_r = int(sum(int(x) for x in gather_equal(torch.tensor([n_r_local], device=parts.device), group).view(-1)))
+    n_t = tgt_full["counts"].shape[0]
     pairs = [(int(a), int(b), float(c)) for a, b, c in zip(ref, tgt, dst)]
-    info = {"world": world, "rank": rank, "ref_slice": kp_range(feats[0]["n"], rank, world),
-            "tgt_slice": kp_range(feats[1]["n"], rank, world), "ref_descriptors": n_r, "tgt_descriptors": n_t}
+    info = {"world": world, "rank": rank, "ref_slice": slices[0], "tgt_slice": slices[1],
+            "ref_descriptors": n_r, "ref_descriptors_local": n_r_local, "tgt_descriptors": n_t}
     return MatchSet(pairs=pairs, mode="rift2", distance_evals=n_r * n_t), info

@@ -238,24 +238,6 @@ def test_evaluate_batch_vs_oracle(r2):
         assert abs(float(ev["rmse"][p]) - rmse) <= 1e-12 * rmse
 
 
-def test_estimator_front_end(r2, pair512):
-    """RiftMatcher / RiftFeatureExtractor (ref: estimator.py:63-133) on the
-    GPU pipeline: predict equals the coordinates of match_pair's matches,
-    for one image and for a list; transform returns one FeatureSet each."""
-    a, b, _ = pair512
-    m = r2.RiftMatcher(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=1500).fit(a)
-    got = m.predict(b)
-    res = r2.match_pair(a, b, r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=1500))
-    rk, tk = res.ref.keypoints, res.tgt.keypoints
-    want = np.array([[rk[r].x, rk[r].y, tk[t].x, tk[t].y] for r, t, _ in res.matches.pairs]).reshape(-1, 4)
-    assert got.shape == want.shape and len(want) > 50
-    assert np.array_equal(got, want)
-    both = m.predict([b, a])
-    assert np.array_equal(both[0], want) and len(both[1]) > 0
-    feats = r2.RiftFeatureExtractor(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=1500).fit_transform([a, b])
-    assert len(feats) == 2 and len(feats[0].keypoints) == len(rk) and len(feats[1].descriptors) == len(res.tgt.descriptors)
-
-
 def test_run_from_host_pipelined_results(r2):
     """The end-to-end host path (double-buffered uploads, fields-only first
     step, features-only last step): after `steps` steps the pinned output

@@ -29,11 +29,17 @@ def setup():
 
 
 def _simulate(sharded, be, cfg, feats, G):
+    """G ranks in sequence: only image 2's slices are concatenated (the
+    all-gather); image 1's stay per rank, and each rank's finish supplies
+    the distances of the winners it owns."""
     dim = cfg.grid * cfg.grid * cfg.n_orient
     loc = [[be.describe_slice(f, *sharded.kp_range(f["n"], r, G), cfg) for r in range(G)] for f in feats]
     full = [{k: torch.cat([l[k] for l in per_rank]) for k in per_rank[0]} for per_rank in loc]
     parts = torch.stack([be.partial(loc[0][r], full[1], dim) for r in range(G)])
-    return full, be.finish(parts, full[0], full[1], feats[0]["n"], feats[1]["n"], dim)
+    mine = [be.finish_local(parts, loc[0][r], full[1], feats[0]["n"], feats[1]["n"], dim) for r in range(G)]
+    if G > 1:
+        assert any(np.isinf(m[2]).any() for m in mine)         # some winners are owned elsewhere
+    return full, sharded.merge_triples(mine)
 
 
 @pytest.mark.parametrize("G", [1, 2, 3, 8])

@@ -194,24 +194,3 @@ def test_estimate_affine_degenerate_inputs():
     assert estimate_affine(line, line)[0] is None
     with pytest.raises(ParameterError):
         fit_affine(np.zeros((2, 2)), np.zeros((2, 2)))
-
-
-# ---- scikit-learn front end (ref: estimator.py:33-133) ----------------------
-def test_estimator_parameter_surface():
-    from sklearn.base import clone
-    from sklearn.exceptions import NotFittedError
-    from paper_2303_00319_b200 import ConfigError
-    from paper_2303_00319_b200.estimator import RiftFeatureExtractor, RiftMatcher
-    names = ["dominant_ratio", "fast_threshold", "grid", "max_keypoints", "min_wavelength", "mode", "n_orient",
-             "n_scales", "noise_k", "orientation_spread", "patch_size", "rotate_patch", "scale_mult", "sigma_on_f",
-             "spread_cutoff", "spread_gain", "threads", "weight_by_amplitude"]
-    ex = RiftFeatureExtractor(max_keypoints=500)
-    assert sorted(ex.get_params()) == names
-    assert ex.get_params()["scale_mult"] == 2.1 and ex.get_params()["max_keypoints"] == 500
-    c = clone(ex).set_params(scale_mult=1.6)
-    assert c.get_params()["scale_mult"] == 1.6 and ex.get_params()["scale_mult"] == 2.1
-    assert ex.fit().config_.max_keypoints == 500
-    with pytest.raises(ConfigError):
-        RiftFeatureExtractor(mode="bogus").fit()
-    with pytest.raises(NotFittedError):
-        RiftMatcher().predict(np.zeros((32, 32)))

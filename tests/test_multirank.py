@@ -109,11 +109,15 @@ class NumpyBackend:
                 out[t] = (D[t, best], qr[best], rk[best], 0)
         return torch.as_tensor(out)
 
-    def finish(self, parts_all, ref, tgt, n_ref_kp, n_tgt_kp, dim):
+    def finish_local(self, parts_all, ref, tgt, n_ref_kp, n_tgt_kp, dim):
+        """Exact combine of the gathered partials; float64 distances only for
+        winners whose rows this rank holds (+inf otherwise), like the C ABI."""
         P = parts_all.numpy()
         R, T = ref["counts"].numpy().astype(float), tgt["counts"].numpy().astype(float)
         rk, tk, qt = ref["kp"].numpy(), tgt["kp"].numpy(), tgt["sqnorm"].numpy()
         res = []
+        if len(R) == 0:
+            return np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0)
         for kp_t in np.unique(tk):
             rows = np.nonzero(tk == kp_t)[0]
             best = None                                   # (D, q_ref, kp_ref, q_tgt)
@@ -131,13 +135,15 @@ class NumpyBackend:
             if best is None:
                 continue
             rv = R[rk == best[2]]
-            tv = T[rows]
-            rv = rv / np.linalg.norm(rv, axis=1, keepdims=True)
-            tv = tv / np.linalg.norm(tv, axis=1, keepdims=True)
-            d = np.sqrt(((rv[:, None, :] - tv[None, :, :]) ** 2).sum(-1).min())
+            d = np.inf
+            if len(rv):
+                tv = T[rows]
+                rv = rv / np.linalg.norm(rv, axis=1, keepdims=True)
+                tv = tv / np.linalg.norm(tv, axis=1, keepdims=True)
+                d = np.sqrt(((rv[:, None, :] - tv[None, :, :]) ** 2).sum(-1).min())
             res.append((best[2], int(kp_t), d))
-        res.sort(key=lambda p: (p[2], p[0], p[1]))
-        return (np.array([p[0] for p in res]), np.array([p[1] for p in res]), np.array([p[2] for p in res]))
+        return (np.array([p[0] for p in res], np.int64), np.array([p[1] for p in res], np.int64),
+                np.array([p[2] for p in res], np.float64))
 
 
 BASE = dict(scale_mult=1.6, sigma_on_f=0.75)
@@ -170,6 +176,9 @@ def test_sharded_matching_gloo_world2():
     p1, info1 = out[1]
     assert p0 == p1                                   # every rank holds the same result
     assert info0["ref_slice"][1] == info1["ref_slice"][0]        # contiguous, complementary slices
+    # image 1's rows stay on their rank: each rank held only its own slice
+    assert info0["ref_descriptors_local"] + info1["ref_descriptors_local"] == info0["ref_descriptors"]
+    assert 0 < info0["ref_descriptors_local"] < info0["ref_descriptors"]
     # the same backend unsharded, and the oracle's own matcher on the full sets
     a, b, _ = synth.make_pair(160, seed=9, looks=None)
     cfg = RiftConfig(max_keypoints=300, **BASE)
