@@ -178,7 +178,7 @@ class BatchPipeline:
         if self.graphs is None:
             self.capture()
         if getattr(self, "_f2", None) is None:
-            self._f2 = {k: torch.empty_like(v) for k, v in self.f.items()}
+            self._f2 = {k: torch.zeros_like(v) for k, v in self.f.items()}
         fbuf = (self.f, self._f2)
         imgs = (self.images, self._alt)
         for p in (0, 1):                                   # warm-up: allocate workspaces

@@ -76,6 +76,8 @@ def _device_map(arr):
         raise ParameterError(f"expected a 2-D map, got shape {a.shape}")
     if not np.all(np.isfinite(a)):
         raise ParameterError("score map contains non-finite values")
+    if not a.flags.writeable:             # read-only maps of compute_fields: torch wants a writable source
+        a = a.copy()
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
