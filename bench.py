@@ -57,97 +57,157 @@ def workload(args, n):
 
 
 # ----------------------------------------------------------------- CPU side
-def _oracle_pair(args):
-    """One pair through the CPU oracle (test infrastructure; baseline only)."""
-    seed, size = args
-    os.environ["OMP_NUM_THREADS"] = "1"
-    from oracle import rift2_oracle as O
-    from paper_2303_00319_b200 import synth
-    a, b, _ = synth.make_pair(size, seed)
-    p = O.Bank(**BASE_PARAMS)
-    t0 = time.perf_counter()
-    feats = []
-    for img in (a, b):
-        f = O.fields(img, p, workers=1)
-        kp = O.detect_keypoints(f["moment_min"], f["moment_max"], 0.001, 5000, 96)
-        c, k, v, _ = O.describe_rift2(f["mim"], kp)
-        feats.append((c, k))
-    (rc, rk), (tc, tk) = feats
-    rv = rc / np.linalg.norm(rc, axis=1, keepdims=True)
-    tv = tc / np.linalg.norm(tc, axis=1, keepdims=True)
-    if len(rk) and len(tk):
-        O.match_nn(rv, rk, tv, tk)
-    return time.perf_counter() - t0
+# The CPU baseline is the UNMODIFIED reference package (pure Python/numpy/
+# scipy), installed into baseline/_ref by oracle/build_ref.sh and run through
+# its own public API (rift2.compute_fields / detect_keypoints / describe /
+# match_nn -- the stages rift2.match_pair chains, ref pipeline.py:67-99).
+# Only if that install is missing does the oracle port stand in ("port").
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def cpu_sample(size, n_workers, seed0=0):
-    ctx = mp.get_context("spawn")
-    t0 = time.perf_counter()
-    with ctx.Pool(n_workers) as pool:
-        per = pool.map(_oracle_pair, [(seed0 + i, size) for i in range(n_workers)])
-    wall = time.perf_counter() - t0
-    return n_workers / wall, wall, per
+def reference_available() -> bool:
+    return os.path.exists(os.path.join(REF_DIR, "rift2", "__init__.py"))
+
+
+def host_info() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = os.cpu_count() or 1
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cpus": aff}
 
 
 def cpu_workers():
-    n = os.cpu_count() or 1
-    try:
-        n = len(os.sched_getaffinity(0))
-    except AttributeError:
-        pass
-    return max(1, min(n, 16))
+    """One single-threaded worker per usable host core: the
+    reference's FFTs and BLAS are pinned to one thread per process."""
+    return max(1, host_info()["affinity_cpus"])
+
+
+def _single_thread_env():
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "RIFT2_THREADS"):
+        os.environ[k] = "1"
+
+
+class _Stages:
+    """The path's stages on the CPU: the reference's own functions, or the
+    oracle port when the reference is not installed."""
+
+    def __init__(self, max_kp):
+        _single_thread_env()
+        self.kind = "reference" if reference_available() else "port"
+        if self.kind == "reference":
+            if REF_DIR not in sys.path:
+                sys.path.insert(0, REF_DIR)
+            import rift2
+            self.r = rift2
+            self.cfg = rift2.RiftConfig(max_keypoints=max_kp, threads=1, **BASE_PARAMS)
+        else:
+            from oracle import rift2_oracle as O
+            self.O = O
+            self.bank = O.Bank(**BASE_PARAMS)
+            self.max_kp = max_kp
+
+    def fields(self, img):
+        if self.kind == "reference":
+            return self.r.compute_fields(img, self.cfg)
+        return self.O.fields(img, self.bank, workers=1)
+
+    def features(self, f, side):
+        if self.kind == "reference":
+            pc, mim = f
+            c = self.cfg
+            kps = self.r.detect_keypoints(pc, c.fast_threshold, c.max_keypoints, c.patch_size)
+            return self.r.pipeline.describe(mim, kps, c, side=side).descriptors
+        kp = self.O.detect_keypoints(f["moment_min"], f["moment_max"], 0.001, self.max_kp, 96)
+        c, k, _, _ = self.O.describe_rift2(f["mim"], kp)
+        return (c / np.linalg.norm(c, axis=1, keepdims=True), k)
+
+    def match(self, d_ref, d_tgt):
+        if self.kind == "reference":
+            if d_ref and d_tgt:
+                return self.r.match_nn(d_ref, d_tgt, mode=self.cfg.mode)
+            return None
+        (rv, rk), (tv, tk) = d_ref, d_tgt
+        if len(rk) and len(tk):                 # tiny images can leave a side without descriptors
+            return self.O.match_nn(rv, rk, tv, tk)
+        return None
+
+
+def _cpu_pair(args):
+    """One whole pair through the CPU stages (wall time of the pipeline, not
+    of the generator)."""
+    seed, size, max_kp = args
+    st = _Stages(max_kp)
+    from paper_2303_00319_b200 import synth
+    a, b, _ = synth.make_pair(size, seed)
+    t0 = time.perf_counter()
+    fa, fb = st.fields(a), st.fields(b)
+    st.match(st.features(fa, "reference"), st.features(fb, "target"))
+    return time.perf_counter() - t0, st.kind
+
+
+def cpu_sample(size, n_workers, max_kp, seed0=0):
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(n_workers) as pool:
+        res = pool.map(_cpu_pair, [(seed0 + i, size, max_kp) for i in range(n_workers)])
+    wall = time.perf_counter() - t0
+    return n_workers / wall, wall, [r[0] for r in res], res[0][1]
 
 
 UNITS = ("fields(ref)", "fields(tgt)", "features(ref)", "features(tgt)", "match")
 
 
-def _unit_worker(conn, size, seed0, stride):
+def _unit_worker(conn, size, seed0, stride, max_kp):
     """Persistent CPU worker for --impl reference: holds one pair's state and
-    runs one pipeline unit per request (test infrastructure: the oracle)."""
-    from oracle import rift2_oracle as O
+    runs one stage of it per request."""
+    st = _Stages(max_kp)
     from paper_2303_00319_b200 import synth
-    bank = O.Bank(**BASE_PARAMS)
-    pair, st = 0, {}
+    pair, state = 0, {}
+    conn.send(st.kind)
     while True:
         msg = conn.recv()
         if msg is None:
             return
         if msg == "gen":
-            st = {"img": synth.make_pair(size, seed0 + pair * stride)[:2]}
+            state = {"img": synth.make_pair(size, seed0 + pair * stride)[:2]}
             conn.send(0.0)
             continue
         t0 = time.perf_counter()
         if msg in (0, 1):
-            st[f"f{msg}"] = O.fields(st["img"][msg], bank, workers=1)
+            state[f"f{msg}"] = st.fields(state["img"][msg])
         elif msg in (2, 3):
-            f = st[f"f{msg - 2}"]
-            kp = O.detect_keypoints(f["moment_min"], f["moment_max"], 0.001, 5000, 96)
-            c, k, _, _ = O.describe_rift2(f["mim"], kp)
-            st[f"d{msg - 2}"] = (c / np.linalg.norm(c, axis=1, keepdims=True), k)
+            state[f"d{msg - 2}"] = st.features(state[f"f{msg - 2}"], "reference" if msg == 2 else "target")
         else:
-            (rv, rk), (tv, tk) = st["d0"], st["d1"]
-            if len(rk) and len(tk):                 # tiny images can leave a side without descriptors
-                O.match_nn(rv, rk, tv, tk)
+            st.match(state["d0"], state["d1"])
             pair += 1
         conn.send(time.perf_counter() - t0)
 
 
 class UnitPool:
-    def __init__(self, n, size):
-        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "RIFT2_THREADS"):
-            os.environ[k] = "1"
+    def __init__(self, n, size, max_kp):
         ctx = mp.get_context("spawn")
         self.conns, self.procs = [], []
         for w in range(n):
             a, b = ctx.Pipe()
-            p = ctx.Process(target=_unit_worker, args=(b, size, w, n), daemon=True)
+            p = ctx.Process(target=_unit_worker, args=(b, size, w, n, max_kp), daemon=True)
             p.start()
             self.conns.append(a)
             self.procs.append(p)
+        self.kind = [c.recv() for c in self.conns][0]
         self.unit = 0
 
     def step(self):
-        """One step = the next unit on every worker; returns the wall time."""
+        """One step = the next stage on every worker; returns the wall time."""
         if self.unit == 0:
             for c in self.conns:                  # generation is outside the timed step
                 c.send("gen")
@@ -170,14 +230,14 @@ class UnitPool:
 
 
 def run_reference(args, rank, world):
-    """The reference's CPU path (the oracle port, pinned to the reference by
-    golden vectors) on all host cores.  A step is one fifth of a pair on
-    every worker (UNITS, round robin) so the run stays within minutes;
-    pairs/s = workers / sum over units of the mean unit wall time."""
+    """The reference's CPU implementation on all host cores: one
+    single-threaded worker per core, each stepping through its own pairs one
+    stage per step (UNITS, round robin) so the run stays within minutes;
+    pairs/s = workers / sum over stages of the mean stage wall time."""
     if rank != 0:
         return
     n = cpu_workers()
-    pool = UnitPool(n, args.size)
+    pool = UnitPool(n, args.size, args.max_kp)
     try:
         for _ in range(args.warmup):
             pool.step()
@@ -190,16 +250,19 @@ def run_reference(args, rank, world):
             walls.append(w)
     finally:
         pool.close()
-    per_pair = sum(statistics.mean(v) for v in by_unit.values())
+    per_pair = sum(statistics.mean(v) for v in by_unit.values() if v)
     value = n / per_pair
-    sample = (f"{n} worker processes x 1 thread; each step runs one of {len(UNITS)} units of a {args.size}^2 "
-              f"pair ({', '.join(UNITS)}) on every worker; {steps} steps; pairs/s = workers / sum of mean unit "
-              f"walls ({per_pair:.1f} s per pair per worker)")
+    what = ("the unmodified reference (baseline/_ref rift2: compute_fields, detect_keypoints, pipeline.describe, "
+            "match_nn)" if pool.kind == "reference" else "the oracle port (reference not installed)")
+    sample = (f"{n} worker processes x 1 thread running {what}; each step runs one of {len(UNITS)} stages of a "
+              f"{args.size}^2 pair ({', '.join(UNITS)}) on every worker; {steps} steps; pairs/s = workers / sum "
+              f"of mean stage walls ({per_pair:.1f} s per pair per worker)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
             "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload(args, world),
-            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": n, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": n, "kind": pool.kind, "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -297,6 +360,26 @@ def traffic():
         return None, None
 
 
+def dataclass_api_latency(cfg, size, seeds):
+    """Wall time of paper_2303_00319_b200.match_pair (the reference's
+    dataclass API: host float64 images in, Keypoint / Descriptor / MatchSet
+    objects out) per pair; the first call warms the workspaces."""
+    from paper_2303_00319_b200 import match_pair, synth
+    pairs = [synth.make_pair(size, s)[:2] for s in seeds]
+    match_pair(*pairs[0], cfg)
+    walls = []
+    for a, b in pairs:
+        t0 = time.perf_counter()
+        res = match_pair(a, b, cfg)
+        walls.append(time.perf_counter() - t0)
+        assert len(res.matches.pairs) > 0
+    walls.sort()
+    return {"what": f"match_pair on one {size}^2 pair (dataclass API incl. host<->device copies and "
+                    f"Keypoint/Descriptor/MatchSet construction), seeds {seeds[0]}-{seeds[-1]}",
+            "ms_median": 1e3 * statistics.median(walls), "ms_min": 1e3 * walls[0], "ms_max": 1e3 * walls[-1],
+            "pairs_per_s": len(walls) / sum(walls)}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -360,12 +443,13 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e: public API with host buffers -- every step uploads its images from
     # pinned host memory (copy stream, double-buffered against the previous
-    # step's compute) and reads the match arrays back
+    # step's compute) and reads back the match arrays and the keypoint
+    # coordinates they index (a usable result: matched point pairs)
     host_in = torch.from_numpy(imgs).pin_memory()
-    out_keys = ("ref", "tgt", "dist", "count")
-    host_out = {k: torch.empty(pipe.m[k].shape, dtype=pipe.m[k].dtype).pin_memory() for k in out_keys}
+    out_keys = ("ref", "tgt", "dist", "count", "kp_x", "kp_y", "kp_count")
+    host_out = {k: torch.empty(shp, dtype=dt).pin_memory() for k, (shp, dt) in pipe.result_shapes(out_keys).items()}
     h2d = host_in.numel() * 4
-    d2h = sum(pipe.m[k].numel() * pipe.m[k].element_size() for k in out_keys)
+    d2h = sum(t.numel() * t.element_size() for t in host_out.values())
     pipe.run_from_host_pipelined(host_in, 2, host_out)
     torch.cuda.synchronize()
     if world > 1:
@@ -378,6 +462,17 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     clocks = clk.stop()
+    # the matched coordinates of the last batch, resolved on the host from the copied arrays
+    n0 = int(host_out["count"][0])
+    r0, t0_ = host_out["ref"][0, :n0].long(), host_out["tgt"][0, :n0].long()
+    matched_xy = torch.stack([host_out["kp_x"][0][r0], host_out["kp_y"][0][r0],
+                              host_out["kp_x"][1][t0_], host_out["kp_y"][1][t0_]], 1)
+
+    # dataclass drop-in API (ref pipeline.py:82-99): one pair per call,
+    # north_star's configs[1] single-pair latency over seeds 0-15 on 1 GPU
+    api = None
+    if world == 1 and args.size <= 1024:
+        api = dataclass_api_latency(cfg, args.size, seeds=range(16))
 
     total_ms, e2e_ms, fields_ms = max_over_ranks([total_ms, e2e_ms, fields_ms], world, "cuda")
     if rank != 0:
@@ -409,13 +504,17 @@ def run_ours(args, rank, world, local_rank):
                                "frac": match_flops / (match_ms / 1e3) / 1e12 / tpk,
                                "flops_per_launch": match_flops, "launch_ms": match_ms, "peak_source": tpk_src},
             "clocks": clocks,
+            "single_pair_api": api,
+            "e2e_matched_points_pair0": int(matched_xy.shape[0]),
             "matches_per_pair": float(np.mean(counts))}
     if world == 1 and not args.no_cpu_baseline:
         n = cpu_workers()
-        rate, wall, per = cpu_sample(args.size, n)
-        line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": n, "kind": "port",
-                                "sample": f"{n} pairs ({n} processes x 1 pair, {args.size}^2, oracle pipeline, "
-                                          f"{wall:.1f} s wall, {statistics.mean(per):.1f} s/pair/core)"}
+        rate, wall, per, kind = cpu_sample(args.size, n, args.max_kp)
+        what = "rift2.compute_fields/detect_keypoints/describe/match_nn of baseline/_ref" if kind == "reference" \
+            else "oracle port"
+        line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": n, "kind": kind, "host": host_info(),
+                                "sample": f"{n} pairs ({n} single-threaded processes x 1 pair, {args.size}^2, "
+                                          f"{what}, {wall:.1f} s wall, {statistics.mean(per):.1f} s/pair/core)"}
     print(json.dumps(line), flush=True)
 
 

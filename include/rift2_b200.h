@@ -239,6 +239,67 @@ int32_t rift2_synth_targets(const double* src, int64_t src_image_stride, int32_t
                             int32_t first_image, float* dst, int64_t dst_image_stride, float* dst_src_copy,
                             int64_t copy_image_stride, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- unfused reference entry points ----------------------------------------
+ * The reference's step-by-step API for callers that use the stages one at a
+ * time (the fused rift2_fields / rift2_describe are the pipeline path).
+ *
+ * rift2_filter_bank: ref loggabor.py:131-159 (build_filter_bank): transfer
+ *   [n_scales][n_orient][height][width] float64 (device), same formulas in
+ *   float64; height, width >= 16.
+ * rift2_apply_bank: ref loggabor.py:162-185 (apply_bank) of a GIVEN bank:
+ *   image [height][width] float32, transfer [S][O][height][width] float32
+ *   (device) -> even, odd, amplitude [S][O][height][width] float32 (fp32
+ *   FFTs; FFT lengths with factors 2, 3, 5).
+ * rift2_pc_moments: ref loggabor.py:188-251 (orientation_amplitudes,
+ *   phase_congruency_moments) from a response stack (float32 device planes
+ *   as rift2_apply_bank writes them): a_o, pc [O][height][width], moment_max,
+ *   moment_min [height][width] float32; pc / moment maps may all be NULL
+ *   (then only a_o, and no workspace is used).  The noise floor uses the
+ *   exact median of each scale-0 amplitude plane.
+ * rift2_orientation_amplitudes: ref loggabor.py:188-190: amplitude
+ *   [S][O][height][width] float64 -> a_o [O][height][width] float64 (sum
+ *   over scales in scale order).
+ * rift2_build_mim: ref mim.py:43-55 (build_mim): a_o [O][height][width]
+ *   float64 -> indices int32 (1-based first argmax), max_amplitude float64
+ *   (nullable).
+ * rift2_patch_counts: ref mim.py:58-66 (patch_histogram) and
+ *   descriptor.py:145-164 (encode, before normalisation), for n patches:
+ *   indices [n][height][width] int32 (values 1..n_orient count, 0 is
+ *   ignored), amplitude (same shape, float64, NULL = unweighted counts) ->
+ *   hist [n][n_orient] and/or cells [n][grid*grid*n_orient] float64 (cells
+ *   need square patches divisible into grid x grid cells).
+ * rift2_remap_indices: ref mim.py:117-136, in place on count int32 values:
+ *   kind 0 recode (pivot = dominant index), kind 1 cyclic_shift (pivot =
+ *   initial layer).
+ * rift2_extract_patch: ref descriptor.py:85-125 for a non-zero angle:
+ *   indices [height][width] int32 (+ optional float64 amplitudes) ->
+ *   out_indices [size][size] (+ out_amplitude, NULL to skip); cos_a / sin_a
+ *   are the snapped cosine and sine; *out_of_bounds (device int32) is set
+ *   when any sample leaves the map (the reference returns None). */
+int32_t rift2_filter_bank(int32_t height, int32_t width, const rift2_bank_params* params, double* transfer,
+                          void* stream);
+int32_t rift2_apply_bank_workspace_size(int32_t height, int32_t width, int32_t n_scales, int32_t n_orient,
+                                        size_t* bytes);
+int32_t rift2_apply_bank(const float* image, int32_t height, int32_t width, int32_t n_scales, int32_t n_orient,
+                         const float* transfer, float* even, float* odd, float* amplitude, void* workspace,
+                         size_t workspace_bytes, void* stream);
+int32_t rift2_pc_moments_workspace_size(int32_t height, int32_t width, const rift2_bank_params* params,
+                                        size_t* bytes);
+int32_t rift2_pc_moments(const float* even, const float* odd, const float* amplitude, int32_t height,
+                         int32_t width, const rift2_bank_params* params, float* a_o, float* pc, float* moment_max,
+                         float* moment_min, void* workspace, size_t workspace_bytes, void* stream);
+int32_t rift2_orientation_amplitudes(const double* amplitude, int32_t n_scales, int32_t n_orient, int32_t height,
+                                     int32_t width, double* a_o, void* stream);
+int32_t rift2_build_mim(const double* a_o, int32_t n_orient, int32_t height, int32_t width, int32_t* indices,
+                        double* max_amplitude, void* stream);
+int32_t rift2_patch_counts(const int32_t* indices, const double* amplitude, int32_t n_patches, int32_t height,
+                           int32_t width, int32_t n_orient, int32_t grid, double* hist, double* cells, void* stream);
+int32_t rift2_remap_indices(int32_t* indices, int64_t count, int32_t n_orient, int32_t pivot, int32_t kind,
+                            void* stream);
+int32_t rift2_extract_patch(const int32_t* indices, const double* amplitude, int32_t height, int32_t width,
+                            double x, double y, int32_t size, double cos_a, double sin_a, int32_t* out_indices,
+                            double* out_amplitude, int32_t* out_of_bounds, void* stream);
+
 /* ---- diagnostics ----------------------------------------------------------
  * The filter bank's exact-median stage (the Rayleigh noise estimate, ref:
  * loggabor.py:222, np.median) on caller-given complex64 planes

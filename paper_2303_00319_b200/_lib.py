@@ -6,6 +6,7 @@ every entry point raises instead of computing anything on the host.
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 import threading
@@ -61,6 +62,18 @@ _SIGNATURES = {
     "rift2_synth_workspace_size": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
     "rift2_synth_targets": (_c_int, [_c_p, ctypes.c_int64, _c_int, _c_int, _c_int, _c_p, _c_p, ctypes.c_uint64,
                                      _c_int, _c_p, ctypes.c_int64, _c_p, ctypes.c_int64, _c_p, _c_sz, _c_p]),
+    "rift2_filter_bank": (_c_int, [_c_int, _c_int, ctypes.POINTER(BankParamsC), _c_p, _c_p]),
+    "rift2_apply_bank_workspace_size": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
+    "rift2_apply_bank": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "rift2_pc_moments_workspace_size": (_c_int, [_c_int, _c_int, ctypes.POINTER(BankParamsC), ctypes.POINTER(_c_sz)]),
+    "rift2_pc_moments": (_c_int, [_c_p, _c_p, _c_p, _c_int, _c_int, ctypes.POINTER(BankParamsC), _c_p, _c_p, _c_p,
+                                  _c_p, _c_p, _c_sz, _c_p]),
+    "rift2_orientation_amplitudes": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p]),
+    "rift2_build_mim": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p]),
+    "rift2_patch_counts": (_c_int, [_c_p, _c_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p]),
+    "rift2_remap_indices": (_c_int, [_c_p, ctypes.c_int64, _c_int, _c_int, _c_int, _c_p]),
+    "rift2_extract_patch": (_c_int, [_c_p, _c_p, _c_int, _c_int, _c_d, _c_d, _c_int, _c_d, _c_d, _c_p, _c_p, _c_p,
+                                     _c_p]),
     "rift2_debug_median_workspace_size": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_sz)]),
     "rift2_debug_median": (_c_int, [_c_p, _c_int, _c_int, _c_p, _c_p, _c_p, _c_sz, _c_p]),
 }
@@ -96,8 +109,14 @@ def load(require_gpu: bool = False):
     return _lib
 
 
+# completed C-ABI calls by name (every entry point reports through check()):
+# lets tests prove a caller's stages all reached the library
+CALLS: collections.Counter = collections.Counter()
+
+
 def check(rc: int, what: str) -> None:
     """Map a C status onto the reference's exception types (ref: errors.py)."""
+    CALLS[what] += 1
     if rc == 0:
         return
     msg = _lib.rift2_last_error().decode(errors="replace") if _lib else ""

@@ -135,9 +135,10 @@ class BatchPipeline:
         """End-to-end steps from host memory: step i uploads host_images[i %
         len] (pinned (B, H, W) float32 tensors) on a copy stream into one of
         two device buffers while the previous step computes, runs the whole
-        pipeline on the current stream, and copies the match arrays back into
-        `host_out` (pinned tensors shaped like `self.m`).  Enqueues only; the
-        caller synchronises."""
+        pipeline on the current stream, and copies results back into
+        `host_out` (pinned tensors keyed like `_result`: match arrays and the
+        keypoint coordinates they index).  Enqueues only; the caller
+        synchronises."""
         if self.graphs is None:
             self.capture()
         if not isinstance(host_images, (list, tuple)):
@@ -165,7 +166,7 @@ class BatchPipeline:
             self.replay_features()
             if host_out is not None:
                 for k, t in host_out.items():
-                    t.copy_(self.m[k], non_blocking=True)
+                    t.copy_(self._result(k), non_blocking=True)
         cs.wait_stream(xs)
 
     # ---- cross-step pipeline --------------------------------------------------
@@ -253,10 +254,21 @@ class BatchPipeline:
             done[b].record(cs)
             if i >= 1 and host_out is not None:            # batch i-1 is complete
                 for k, t in host_out.items():
-                    t.copy_(self.m[k], non_blocking=True)
+                    t.copy_(self._result(k), non_blocking=True)
         cs.wait_stream(xs)
 
     # ---- results -----------------------------------------------------------
+    def _result(self, key: str) -> torch.Tensor:
+        """A result array by name: match arrays (ref, tgt, dist, count) or the
+        keypoints they index (kp_x, kp_y, kp_count: (2 * n_pairs, K), the
+        reference image of pair p at row 2p, its target at 2p + 1)."""
+        if key.startswith("kp_"):
+            return self.k[key[3:]]
+        return self.m[key]
+
+    def result_shapes(self, keys) -> dict:
+        return {k: (tuple(self._result(k).shape), self._result(k).dtype) for k in keys}
+
     def matches_host(self):
         """Per pair (ref ids, tgt ids, dist) numpy arrays."""
         cnt = self.m["count"].cpu().numpy()

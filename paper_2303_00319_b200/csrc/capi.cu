@@ -20,6 +20,7 @@
 #include "synth.h"
 #include "fields.h"
 #include "match.h"
+#include "patch.h"
 
 namespace {
 
@@ -386,4 +387,112 @@ int32_t rift2_debug_median(const void* planes_c64, int32_t planes, int32_t n, fl
                       "rift2_debug_median");
 }
 
+
+// ------------------------------------------------- unfused reference entry points
+int32_t rift2_filter_bank(int32_t height, int32_t width, const rift2_bank_params* params, double* transfer,
+                          void* stream) {
+  r2::BankConsts k;
+  int32_t rc = bank_consts(params, k);
+  if (rc) return rc;
+  if (height < 16 || width < 16) return fail(RIFT2_BAD_ARGUMENT, "filter bank needs width and height >= 16");
+  if (!transfer) return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  const double st = params->orientation_spread > 0 ? params->orientation_spread : M_PI / params->n_orient;
+  rc = r2::filter_bank_run(height, width, params->n_scales, params->n_orient, params->min_wavelength,
+                           params->scale_mult, params->sigma_on_f, st, transfer, static_cast<cudaStream_t>(stream));
+  return map_internal(rc, "rift2_filter_bank");
+}
+
+int32_t rift2_apply_bank_workspace_size(int32_t height, int32_t width, int32_t n_scales, int32_t n_orient,
+                                        size_t* bytes) {
+  if (!bytes || n_scales < 1 || n_orient < 1) return fail(RIFT2_BAD_ARGUMENT, "bad apply_bank arguments");
+  int32_t rc = check_fields_dims(1, height, width);
+  if (rc) return rc;
+  *bytes = r2::apply_bank_workspace_bytes(height, width, n_scales, n_orient);
+  return RIFT2_OK;
+}
+
+int32_t rift2_apply_bank(const float* image, int32_t height, int32_t width, int32_t n_scales, int32_t n_orient,
+                         const float* transfer, float* even, float* odd, float* amplitude, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  if (n_scales < 1 || n_orient < 1) return fail(RIFT2_BAD_ARGUMENT, "bad bank shape");
+  int32_t rc = check_fields_dims(1, height, width);
+  if (rc) return rc;
+  if (!image || !transfer || !even || !odd || !amplitude || !workspace) return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  rc = r2::apply_bank_run(image, height, width, n_scales, n_orient, transfer, even, odd, amplitude, workspace,
+                          workspace_bytes, static_cast<cudaStream_t>(stream));
+  return map_internal(rc, "rift2_apply_bank");
+}
+
+int32_t rift2_pc_moments_workspace_size(int32_t height, int32_t width, const rift2_bank_params* params,
+                                        size_t* bytes) {
+  r2::BankConsts k;
+  int32_t rc = bank_consts(params, k);
+  if (rc) return rc;
+  if (!bytes || height < 1 || width < 1) return fail(RIFT2_BAD_ARGUMENT, "bad pc_moments arguments");
+  *bytes = r2::pc_stack_workspace_bytes(height, width, k.n_scales, k.n_orient);
+  return RIFT2_OK;
+}
+
+int32_t rift2_pc_moments(const float* even, const float* odd, const float* amplitude, int32_t height,
+                         int32_t width, const rift2_bank_params* params, float* a_o, float* pc, float* moment_max,
+                         float* moment_min, void* workspace, size_t workspace_bytes, void* stream) {
+  r2::BankConsts k;
+  int32_t rc = bank_consts(params, k);
+  if (rc) return rc;
+  if (height < 1 || width < 1 || (long long)height * width > 0x7fffffffLL)
+    return fail(RIFT2_BAD_ARGUMENT, "bad dimensions");
+  const bool full = pc || moment_max || moment_min;
+  if (!amplitude || (full && (!even || !odd || !pc || !moment_max || !moment_min || !workspace)))
+    return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  rc = r2::pc_stack_run(even, odd, amplitude, height, width, k, a_o, pc, moment_max, moment_min, workspace,
+                        workspace_bytes, static_cast<cudaStream_t>(stream));
+  return map_internal(rc, "rift2_pc_moments");
+}
+
+int32_t rift2_orientation_amplitudes(const double* amplitude, int32_t n_scales, int32_t n_orient, int32_t height,
+                                     int32_t width, double* a_o, void* stream) {
+  if (!amplitude || !a_o || n_scales < 1 || n_orient < 1 || height < 0 || width < 0)
+    return fail(RIFT2_BAD_ARGUMENT, "bad orientation_amplitudes arguments");
+  return map_internal(r2::sum_scales_run(amplitude, n_scales, n_orient, height, width, a_o,
+                                         static_cast<cudaStream_t>(stream)), "rift2_orientation_amplitudes");
+}
+
+int32_t rift2_build_mim(const double* a_o, int32_t n_orient, int32_t height, int32_t width, int32_t* indices,
+                        double* max_amplitude, void* stream) {
+  if (n_orient < 2) return fail(RIFT2_BAD_ARGUMENT, "need >= 2 stacked channels");
+  if (height < 1 || width < 1 || !a_o || !indices) return fail(RIFT2_BAD_ARGUMENT, "bad build_mim arguments");
+  return map_internal(r2::build_mim_run(a_o, n_orient, height, width, indices, max_amplitude,
+                                        static_cast<cudaStream_t>(stream)), "rift2_build_mim");
+}
+
+int32_t rift2_patch_counts(const int32_t* indices, const double* amplitude, int32_t n_patches, int32_t height,
+                           int32_t width, int32_t n_orient, int32_t grid, double* hist, double* cells, void* stream) {
+  if (n_patches < 0 || height < 1 || width < 1 || n_orient < 1 || !indices)
+    return fail(RIFT2_BAD_ARGUMENT, "bad patch arguments");
+  if (cells && (grid < 1 || height != width || width % grid != 0))
+    return fail(RIFT2_BAD_ARGUMENT, "patch %dx%d does not divide into %dx%d cells", height, width, grid, grid);
+  return map_internal(r2::patch_counts_run(indices, amplitude, n_patches, height, width, n_orient, grid, hist, cells,
+                                           static_cast<cudaStream_t>(stream)), "rift2_patch_counts");
+}
+
+int32_t rift2_remap_indices(int32_t* indices, int64_t count, int32_t n_orient, int32_t pivot, int32_t kind,
+                            void* stream) {
+  if (count < 0 || (count > 0 && !indices) || n_orient < 1 || (kind != 0 && kind != 1))
+    return fail(RIFT2_BAD_ARGUMENT, "bad remap arguments");
+  if (pivot < 1 || pivot > n_orient) return fail(RIFT2_BAD_ARGUMENT, "index %d outside [1, %d]", pivot, n_orient);
+  return map_internal(r2::remap_run(indices, count, n_orient, pivot, kind, static_cast<cudaStream_t>(stream)),
+                      "rift2_remap_indices");
+}
+
+int32_t rift2_extract_patch(const int32_t* indices, const double* amplitude, int32_t height, int32_t width,
+                            double x, double y, int32_t size, double cos_a, double sin_a, int32_t* out_indices,
+                            double* out_amplitude, int32_t* out_of_bounds, void* stream) {
+  if (!indices || !out_indices || !out_of_bounds || height < 1 || width < 1 || size < 1)
+    return fail(RIFT2_BAD_ARGUMENT, "bad extract_patch arguments");
+  if (!std::isfinite(x) || !std::isfinite(y)) return fail(RIFT2_BAD_ARGUMENT, "keypoint is not finite");
+  const int integer_kp = (x == std::floor(x) && y == std::floor(y)) ? 1 : 0;
+  return map_internal(r2::gather_run(indices, amplitude, height, width, x, y, integer_kp, size, cos_a, sin_a,
+                                     out_indices, out_amplitude, out_of_bounds, static_cast<cudaStream_t>(stream)),
+                      "rift2_extract_patch");
+}
 }  // extern "C"

@@ -62,6 +62,8 @@ struct FieldsConst {
   float lp_lncut;              // ln(0.45)
   float log2_inv_hw;           // log2(1 / (H*W)): the inverse-FFT scale folded into the exponent
   double thr_factor;           // T = median * thr_factor
+  const float* xfer;           // explicit transfer [S*O][H][W] (apply_bank of a given bank) or nullptr
+  float inv_hw;                // 1 / (H*W) for the explicit transfer
   const float2* tw_w;          // W_W^j
   const float2* tw_h;          // W_H^j
   GenericPlan plan_w, plan_h;
@@ -233,8 +235,10 @@ R2_DEV void cols_filters(const FieldsConst& c, const float2* Sc, const float2* G
       fence_proxy_async();
       sync();
       if (t == 0) {
+#ifndef R2_EXP_NOSTORE
         for (int k = 0; k < N / 1024; ++k)
           tma_store_3d(qst, 0, xo, (b * c.S * c.O + f) * (c.Hp >> 2) + 256 * k, buf + 1024 * k);
+#endif
         bulk_commit();
       }
       continue;
@@ -381,7 +385,8 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
             sv = S[cc * PL + pad32(ky)];
             sv.y = -sv.y;
           }
-          const float gv = transfer(lnr, L2, th, c.log_lambda[s], c.ang[o], c.a2, c.b2);
+          const float gv = c.xfer ? c.xfer[((size_t)f * H + ky) * W + (mir ? W - kx : kx)] * c.inv_hw
+                                  : transfer(lnr, L2, th, c.log_lambda[s], c.ang[o], c.a2, c.b2);
           buf[pad32(ky)] = make_float2(sv.x * gv, sv.y * gv);
         }
         __syncthreads();
@@ -554,8 +559,14 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constan
         const float2 zz = cconj(v[m]);
         const float a = sqrt_approx(fmaf(zz.x, zz.x, zz.y * zz.y));   // as k_rows_amp0
         if (write_r0) Rp[(size_t)y * W + t + G * m] = zz;   // not needed when K3b recomputes scale 0
+#ifndef R2_EXP_NOAMP
         A[(size_t)y * W + t + G * m] = a;
+#endif
+#ifndef R2_EXP_NOHIST
         atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
+#else
+        if (a < 0.f) sh[0] = 1;                          // keep the amplitude live
+#endif
       }
     }
     __syncthreads();                               // the next group's TMA rewrites the buffers
@@ -1139,31 +1150,58 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
 // One CTA per row pair (y0, y0+1): each orientation stage's inputs arrive in
 // shared memory by the tensor-memory accelerator -- the two rows of every
 // scale as 3-D boxes {2 rows of a 4-row column tile, 256 columns} (the rows
-// the CTA needs, 16 of every 32 bytes of the tile's sectors, gathered without
-// load instructions), one mbarrier per scale -- and all eight warps run one
-// row FFT each: scale 0 is transformed here again rather than read back from
-// K3a, so K3a writes no R0 plane (1.6 GB per 32 images) and no warp idles in
-// the FFT phase.  Buffers: scale s, row r at s*2 + r (a scale's pair is
-// contiguous: the staging of its boxes as [x][row]).  Same arithmetic as
-// k_rows_pc, and bit-identical scale-0 responses (same FFT, same input).
+// the CTA needs, gathered without load instructions), one mbarrier per
+// scale -- and all eight warps run one row FFT each: scale 0 is transformed
+// here again rather than read back from K3a, so K3a writes no R0 plane (1.6
+// GB per 32 images) and no warp idles in the FFT phase.  Buffers: scale s,
+// row r at s*2 + r (a scale's pair is contiguous: the staging of its boxes
+// as [x][row]).  The first kPcExtra scales are staged one whole stage ahead
+// in extra slots (the shared memory two CTAs per SM leave free): their TMA
+// for stage o+1 is issued as soon as stage o's FFT warps have read the slot,
+// so half of the warps start each stage without waiting for memory; the
+// other scales land in the buffers once the pixel phase has released them.
+// Same arithmetic as k_rows_pc, and bit-identical scale-0 responses (same
+// FFT, same input).
+#ifndef R2_PC_EXTRA
+#define R2_PC_EXTRA 0
+#endif
+constexpr int kPcExtra = R2_PC_EXTRA;
+#ifndef R2_PC_DIST
+#define R2_PC_DIST 1
+#endif
+constexpr int kPcDist = R2_PC_DIST;   // L2 prefetch distance in stages (0: none)
 __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_constant__ CUtensorMap qmap,
                                                              const float2* __restrict__ Q,
                                                              const float* __restrict__ thr, PcOut out,
                                                              const __grid_constant__ FieldsConst c, int ahead) {
   // buffer pitch rounded to 128 bytes: TMA destinations must be 128-byte aligned
-  constexpr int G = 32, S = 4, W = 1024, PL = (padded_len(W) + 15) & ~15, PIX = 8;
+  constexpr int G = 32, S = 4, W = 1024, PL = (padded_len(W) + 15) & ~15, PIX = 8, NE = kPcExtra;
   extern __shared__ float2 sm_raw[];
   __shared__ uint64_t s_bar[4];                   // one per scale: its FFT warps start on their own rows
+  __shared__ uint64_t e_bar[NE > 0 ? NE : 1];     // one per extra staging slot
   float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
+  float2* ext = sm + 8 * PL;                      // [NE][2 W] staging slots, [x][row]
   const int H = c.H, O = c.O, F = S * O;
   const int b = blockIdx.y, y0 = 2 * blockIdx.x;
   const float* thr_b = thr + (size_t)b * O;
   const float inv_sm1 = c.inv_sm1, gain = c.spread_gain, cut = c.spread_cutoff;
   const int g = threadIdx.x / G, t = threadIdx.x % G;
+  // the two rows of scale s, orientation o as W / 256 boxes into dst
+  auto issue = [&](int s, int o, float2* dst, uint64_t* bar) {
+#ifdef R2_EXP_NOLOAD
+    return;                                        // timing experiment: compute on stale shared memory
+#endif
+    const int z = (b * F + s * O + o) * (c.Hp >> 2) + (y0 >> 2);
+    mbar_expect_tx(bar, (uint32_t)(2 * W * sizeof(float2)));
+    for (int k = 0; k < W / kPcTmaBox; ++k)
+      tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, bar);
+  };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(&qmap) : "memory");
     for (int q = 0; q < 4; ++q) mbar_init(&s_bar[q], 1);
+    for (int q = 0; q < NE; ++q) mbar_init(&e_bar[q], 1);
     mbar_fence_init();
+    for (int s = 0; s < NE; ++s) issue(s, 0, ext + s * 2 * W, &e_bar[s]);
   }
   __syncthreads();
   float acc_a[PIX], acc_b[PIX], acc_c[PIX], best[PIX];
@@ -1172,39 +1210,41 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
   for (int i = 0; i < PIX; ++i) { acc_a[i] = acc_b[i] = acc_c[i] = 0.f; best[i] = -1.f; bidx[i] = 1; }
   for (int o = 0; o < O; ++o) {
     if (threadIdx.x == 0) {
-      // this stage's inputs (the previous stage's pixel phase is done with
-      // the buffers: the barrier at the end of the loop, then the proxy fence)
+      // this stage's buffer-landed inputs (the previous stage's pixel phase
+      // is done with the buffers: the barrier at the end of the loop, then
+      // the proxy fence)
       fence_proxy_async();
-      const int tile = y0 >> 2;
-      for (int s = 0; s < S; ++s) {
-        const int z = (b * F + s * O + o) * (c.Hp >> 2) + tile;
-        float2* dst = sm + s * 2 * PL;
-        mbar_expect_tx(&s_bar[s], (uint32_t)(2 * W * sizeof(float2)));
-        for (int k = 0; k < W / kPcTmaBox; ++k)
-          tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, &s_bar[s]);
-      }
-      // and the next stage's (or the CTA one resident wave later's first stage) into L2
-      int pb = b, py = y0, o1 = o + 1;
+      for (int s = NE; s < S; ++s) issue(s, o, sm + s * 2 * PL, &s_bar[s]);
+      // and stage o + kPcDist (or, past the last stage, that stage of the CTA
+      // one resident wave later) into L2
+      int pb = b, py = y0, o1 = o + kPcDist;
       bool go = o1 < O;
       if (!go && ahead > 0) {
         const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + ahead;
-        if (lin < (long long)gridDim.x * gridDim.y) { pb = (int)(lin / gridDim.x); py = 2 * (int)(lin % gridDim.x); o1 = 0; go = true; }
+        if (lin < (long long)gridDim.x * gridDim.y) { pb = (int)(lin / gridDim.x); py = 2 * (int)(lin % gridDim.x); o1 -= O; go = true; }
       }
-      if (go) {
+      if (go && kPcDist > 0) {
         const float2* pQ = Q + (size_t)pb * F * c.Hp * W;
-        for (int s = 0; s < S; ++s)
+        for (int s = (o1 == 0 ? 0 : NE); s < S; ++s)
           l2_prefetch(pQ + ((size_t)(s * O + o1) * c.Hp + (py & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
       }
     }
     {                                              // eight FFT warps: scale g / 2 (0 included), row g % 2
       const int s = g >> 1, r = g & 1;
-      mbar_wait(&s_bar[s], (uint32_t)(o & 1));
-      const float2* st = sm + s * 2 * PL;          // [x][row]
+      const bool staged = s < NE;
+#ifndef R2_EXP_NOLOAD
+      mbar_wait(staged ? &e_bar[s] : &s_bar[s], (uint32_t)(o & 1));
+#endif
+      const float2* st = staged ? ext + s * 2 * W : sm + s * 2 * PL;   // [x][row]
       float2 v[32];
 #pragma unroll
       for (int m = 0; m < 32; ++m) v[m] = cconj(st[2 * (t + 32 * m) + r]);
-      SyncNamed pair{8 + s, 2 * G};                // both rows read before the FFT reuses the staging
+      SyncNamed pair{8 + s, 2 * G};                // both rows read before the slot / buffers are reused
       pair();
+      if (staged && r == 0 && t == 0 && o + 1 < O) {
+        fence_proxy_async();                       // the slot's generic reads precede the async refill
+        issue(s, o + 1, ext + s * 2 * W, &e_bar[s]);
+      }
       float2* buf = sm + (s * 2 + r) * PL;
       SyncWarp sw{0xffffffffu};
       fft_fast<G>(v, buf, c.tw_w, t, sw);
@@ -1472,7 +1512,7 @@ static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, c
                           const FieldsConst& c, cudaStream_t st, cudaError_t& e) {
   CUtensorMap map{};
   if (c.S != 4 || (c.H & 1) || !make_qmap(Q, c, map)) return false;
-  const size_t smem = (size_t)8 * ((padded_len(1024) + 15) & ~15) * sizeof(float2) + 128;
+  const size_t smem = ((size_t)8 * ((padded_len(1024) + 15) & ~15) + (size_t)kPcExtra * 2 * 1024) * sizeof(float2) + 128;
   if ((e = set_smem(k_rows_pc_tma, smem)) != cudaSuccess) return true;
   k_rows_pc_tma<<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, thr, out, c,
                                                             resident_ctas((const void*)k_rows_pc_tma, kThreads, smem));
@@ -1592,6 +1632,247 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   return 0;
 }
 
+
+// ================================================= unfused reference entry points
+// The reference's step-by-step API (ref: loggabor.py:131-251, mim.py:43-55)
+// for callers that use the stages separately; the fused path above is what
+// the pipeline runs.
+
+// ref: loggabor.py:122-159 (_frequency_grids, build_filter_bank), in float64
+// with the reference's own formulas: radial log-Gaussian x Butterworth
+// low-pass (cutoff 0.45, order 15), angular Gaussian of the wrapped angle
+// difference taken through atan2 of sin/cos differences, DC zeroed.
+__global__ void __launch_bounds__(256) k_filter_bank(double* __restrict__ T, int H, int W, int S, int O,
+                                                     double min_wl, double mult, double sigma_on_f,
+                                                     double sigma_theta) {
+  const size_t n = (size_t)H * W;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int ky = (int)(i / W), kx = (int)(i % W);
+    const double fy = (double)(ky < (H + 1) / 2 ? ky : ky - H) / (double)H;
+    const double fx = (double)(kx < (W + 1) / 2 ? kx : kx - W) / (double)W;
+    const bool dc = ky == 0 && kx == 0;
+    const double radius = dc ? 1.0 : hypot(fx, fy);
+    const double theta = atan2(fy, fx);
+    const double lowpass = 1.0 / (1.0 + pow(radius / 0.45, 30.0));
+    const double lsig2 = 2.0 * log(sigma_on_f) * log(sigma_on_f);
+    const double st = sin(theta), ct = cos(theta);
+    for (int o = 0; o < O; ++o) {
+      const double a = (double)o * M_PI / (double)O;
+      const double ds = st * cos(a) - ct * sin(a);
+      const double dcos = ct * cos(a) + st * sin(a);
+      const double dth = fabs(atan2(ds, dcos));
+      const double ang = exp(-(dth * dth) / (2.0 * sigma_theta * sigma_theta));
+      double wl = min_wl;
+      for (int s = 0; s < S; ++s) {
+        if (s) wl = min_wl * pow(mult, (double)s);
+        const double l = log(radius / (1.0 / wl));
+        const double rad = dc ? 0.0 : exp(-(l * l) / lsig2) * lowpass;
+        T[((size_t)s * O + o) * n + i] = dc ? 0.0 : rad * ang;
+      }
+    }
+  }
+}
+
+int filter_bank_run(int H, int W, int S, int O, double min_wl, double mult, double sigma_on_f, double sigma_theta,
+                    double* transfer, cudaStream_t st) {
+  const size_t n = (size_t)H * W;
+  const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
+  k_filter_bank<<<blocks, 256, 0, st>>>(transfer, H, W, S, O, min_wl, mult, sigma_on_f, sigma_theta);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
+
+// Inverse row FFT of every Q plane -> even / odd / amplitude planes
+// [F][H][W] (ref: loggabor.py:178-184).
+__global__ void __launch_bounds__(kThreads) k_rows_resp(const float2* __restrict__ Q, float* __restrict__ even,
+                                                        float* __restrict__ odd, float* __restrict__ amp,
+                                                        const __grid_constant__ FieldsConst c) {
+  extern __shared__ float2 sm[];
+  const int y = blockIdx.x, f = blockIdx.y, W = c.W, H = c.H;
+  const float2* Qp = Q + (size_t)f * c.Hp * W;
+  float2* buf = sm;
+  float2* scr = sm + padded_len(W);
+  for (int x = threadIdx.x; x < W; x += blockDim.x) buf[pad32(x)] = cconj(Qp[tq(y, x, W)]);
+  __syncthreads();
+  fft_generic(buf, scr, W, c.plan_w, c.tw_w, threadIdx.x, blockDim.x);
+  for (int x = threadIdx.x; x < W; x += blockDim.x) {
+    const float2 z = cconj(buf[pad32(x)]);
+    const size_t o = ((size_t)f * H + y) * W + x;
+    even[o] = z.x;
+    odd[o] = z.y;
+    amp[o] = hypotf(z.x, z.y);
+  }
+}
+
+size_t apply_bank_workspace_bytes(int H, int W, int S, int O) {
+  const FieldsPlan p = plan_fields(1, H, W, S, O);
+  return p.off_Q + align_up((size_t)p.F * p.Hp * W * sizeof(float2));
+}
+
+// ref: loggabor.py:162-185 (apply_bank) for an explicit transfer array
+// [S][O][H][W] (the bank as given): the generic mixed-radix passes, the
+// transfer read from memory instead of generated
+int apply_bank_run(const float* image, int H, int W, int S, int O, const float* transfer, float* even, float* odd,
+                   float* amp, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const FieldsPlan p = plan_fields(1, H, W, S, O);
+  if (ws_bytes < apply_bank_workspace_bytes(H, W, S, O)) return 1;
+  FieldsConst c{};
+  c.B = 1; c.H = H; c.W = W; c.Wh = p.Wh; c.Hp = p.Hp; c.S = S; c.O = O;
+  c.tw_w = twiddle_table(W);
+  c.tw_h = twiddle_table(H);
+  if (!c.tw_w || !c.tw_h) return 3;
+  if (!make_plan(W, c.plan_w) || !make_plan(H, c.plan_h)) return 2;
+  c.xfer = transfer;
+  c.inv_hw = (float)(1.0 / ((double)H * (double)W));
+  char* w = static_cast<char*>(ws);
+  float2* P = reinterpret_cast<float2*>(w + p.off_P);
+  float2* Q = reinterpret_cast<float2*>(w + p.off_Q);
+  cudaError_t e = launch_rows_fwd<0>(image, P, c, st);
+  if (e == cudaSuccess) e = launch_cols<0>(P, Q, c, st);
+  if (e != cudaSuccess) return 3;
+  const size_t smem = (size_t)2 * padded_len(W) * sizeof(float2);
+  if (set_smem(k_rows_resp, smem) != cudaSuccess) return 3;
+  k_rows_resp<<<dim3(H, S * O), kThreads, smem, st>>>(Q, even, odd, amp, c);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
+
+// level-1 radix histogram of given amplitude planes (the exact-median input)
+__global__ void __launch_bounds__(256) k_hist_planes(const float* __restrict__ a, unsigned* __restrict__ hist, unsigned n) {
+  __shared__ unsigned sh[kHistBins];
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const float* ap = a + (size_t)blockIdx.y * n;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&sh[__float_as_uint(fmaxf(ap[i], 0.f)) >> 19], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[(size_t)blockIdx.y * kHistBins + i], sh[i]);
+}
+
+// Per-pixel phase congruency and moments from a response stack (ref:
+// loggabor.py:188-251), float32; T[o] from the exact median of the scale-0
+// amplitude plane.  pc == nullptr: orientation amplitude sums only.
+struct Trig16 { float c[16], s[16]; };
+__global__ void __launch_bounds__(256) k_pc_stack(const float* __restrict__ even, const float* __restrict__ odd,
+                                                  const float* __restrict__ amp, int S, int O, size_t n,
+                                                  const float* __restrict__ thr, float inv_sm1, float gain,
+                                                  float cut, const Trig16 trig, float* __restrict__ a_o,
+                                                  float* __restrict__ pc, float* __restrict__ mmax,
+                                                  float* __restrict__ mmin) {
+  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n; p += (size_t)gridDim.x * blockDim.x) {
+    float A = 0.f, B = 0.f, C = 0.f;
+    for (int o = 0; o < O; ++o) {
+      float se = 0.f, so = 0.f, sa = 0.f, mx = 0.f;
+      for (int s = 0; s < S; ++s) {
+        const size_t q = ((size_t)s * O + o) * n + p;
+        se += even[q];
+        so += odd[q];
+        sa += amp[q];
+        mx = fmaxf(mx, amp[q]);
+      }
+      if (a_o) a_o[(size_t)o * n + p] = sa;
+      if (!pc) continue;
+      const float xe = sqrtf(se * se + so * so) + 1e-4f;
+      const float me = se / xe, mo = so / xe;
+      float en = 0.f;
+      for (int s = 0; s < S; ++s) {
+        const size_t q = ((size_t)s * O + o) * n + p;
+        const float e = even[q], d = odd[q];
+        en += e * me + d * mo - fabsf(e * mo - d * me);
+      }
+      en = fmaxf(en - thr[o], 0.f);
+      const float spread = (sa / (mx + 1e-4f) - 1.f) * inv_sm1;
+      const float w = 1.f / (1.f + expf(gain * (cut - spread)));
+      const float v = w * en / (sa + 1e-4f);
+      pc[(size_t)o * n + p] = v;
+      const float pcc = v * trig.c[o], pcs = v * trig.s[o];
+      A += pcc * pcc;
+      B += pcc * pcs;
+      C += pcs * pcs;
+    }
+    if (!pc) continue;
+    const float b2 = 2.f * B;
+    const float root = sqrtf(b2 * b2 + (A - C) * (A - C));
+    mmax[p] = 0.5f * (C + A + root);
+    mmin[p] = fmaxf(0.5f * (C + A - root), 0.f);
+  }
+}
+
+size_t pc_stack_workspace_bytes(int H, int W, int S, int O) {
+  const size_t n = (size_t)H * W;
+  return debug_median_workspace_bytes(O, (int)n) + align_up((size_t)O * sizeof(float));
+}
+
+int pc_stack_run(const float* even, const float* odd, const float* amp, int H, int W, const BankConsts& bk,
+                 float* a_o, float* pc, float* mmax, float* mmin, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int S = bk.n_scales, O = bk.n_orient;
+  const size_t n = (size_t)H * W;
+  if (ws_bytes < pc_stack_workspace_bytes(H, W, S, O)) return 1;
+  char* w = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) { char* q = w; w += align_up(bytes); return q; };
+  auto* hist = reinterpret_cast<unsigned*>(take((size_t)O * kHistBins * sizeof(unsigned)));
+  auto* info = reinterpret_cast<MedInfo*>(take((size_t)O * sizeof(MedInfo)));
+  auto* cand = reinterpret_cast<unsigned*>(take((size_t)O * n * sizeof(unsigned)));
+  auto* cnt = reinterpret_cast<unsigned*>(take((size_t)O * sizeof(unsigned)));
+  auto* mh = reinterpret_cast<unsigned*>(take((size_t)O * 2 * kMedH * sizeof(unsigned)));
+  auto* thr = reinterpret_cast<float*>(take((size_t)O * sizeof(float)));
+  Trig16 trig{};
+  for (int o = 0; o < O; ++o) { trig.c[o] = (float)bk.cos_a[o]; trig.s[o] = (float)bk.sin_a[o]; }
+  if (pc) {
+    // exact median of each scale-0 amplitude plane (amp[0][o] = planes o of amp)
+    cudaMemsetAsync(hist, 0, (size_t)O * kHistBins * sizeof(unsigned), st);
+    cudaMemsetAsync(cnt, 0, (size_t)O * sizeof(unsigned), st);
+    k_hist_planes<<<dim3(64, O), 256, 0, st>>>(amp, hist, (unsigned)n);
+    k_med_bins<<<O, 1024, 0, st>>>(hist, info, (unsigned)n);
+    k_med_collect<<<dim3(64, O), 256, 0, st>>>(amp, info, cand, cnt, (unsigned)n);
+    launch_med_select(cand, cnt, info, mh, thr, O, (unsigned)n, bk.thr_factor, st);
+  }
+  const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 8192);
+  k_pc_stack<<<blocks, 256, 0, st>>>(even, odd, amp, S, O, n, thr, (float)(1.0 / (S > 1 ? S - 1 : 1)),
+                                     (float)bk.spread_gain, (float)bk.spread_cutoff, trig, a_o, pc, mmax, mmin);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
+
+// ref: loggabor.py:188-190 (orientation_amplitudes): sum over scales in
+// float64, in scale order (as numpy's axis-0 reduction)
+__global__ void __launch_bounds__(256) k_sum_scales(const double* __restrict__ amp, int S, int O, size_t n,
+                                                    double* __restrict__ a_o) {
+  const size_t total = (size_t)O * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    double acc = amp[i];
+    for (int s = 1; s < S; ++s) acc += amp[(size_t)s * total + i];
+    a_o[i] = acc;
+  }
+}
+
+int sum_scales_run(const double* amp, int S, int O, int H, int W, double* a_o, cudaStream_t st) {
+  const size_t total = (size_t)O * H * W;
+  const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 8192);
+  if (total) k_sum_scales<<<blocks, 256, 0, st>>>(amp, S, O, (size_t)H * W, a_o);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
+
+// ref: mim.py:43-55 (build_mim): first argmax over channels, 1-based, in float64
+__global__ void __launch_bounds__(256) k_build_mim(const double* __restrict__ a, int O, size_t n,
+                                                   int* __restrict__ idx, double* __restrict__ amax) {
+  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n; p += (size_t)gridDim.x * blockDim.x) {
+    double best = a[p];
+    int bi = 0;
+    for (int o = 1; o < O; ++o) {
+      const double v = a[(size_t)o * n + p];
+      if (v > best || (v != v && best == best)) { best = v; bi = o; }   // NaN wins first, as np.argmax
+      if (best != best) break;
+    }
+    idx[p] = bi + 1;
+    if (amax) amax[p] = best;
+  }
+}
+
+int build_mim_run(const double* a_o, int O, int H, int W, int* idx, double* amax, cudaStream_t st) {
+  const size_t n = (size_t)H * W;
+  const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 8192);
+  k_build_mim<<<blocks, 256, 0, st>>>(a_o, O, n, idx, amax);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
 
 // ---------------------------------------------------------- diagnostics ---
 // The exact-median stage on arbitrary complex planes: |z| of each element

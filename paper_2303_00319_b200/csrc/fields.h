@@ -33,6 +33,18 @@ size_t fields_workspace_bytes(int B, int H, int W, int S, int O);
 int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, const FieldsOutputs& out,
                void* ws, size_t ws_bytes, cudaStream_t st);
 
+// unfused reference entry points (ref: loggabor.py:131-251, mim.py:43-55)
+int filter_bank_run(int H, int W, int S, int O, double min_wl, double mult, double sigma_on_f, double sigma_theta,
+                    double* transfer, cudaStream_t st);
+size_t apply_bank_workspace_bytes(int H, int W, int S, int O);
+int apply_bank_run(const float* image, int H, int W, int S, int O, const float* transfer, float* even, float* odd,
+                   float* amp, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t pc_stack_workspace_bytes(int H, int W, int S, int O);
+int pc_stack_run(const float* even, const float* odd, const float* amp, int H, int W, const BankConsts& bk,
+                 float* a_o, float* pc, float* mmax, float* mmin, void* ws, size_t ws_bytes, cudaStream_t st);
+int sum_scales_run(const double* amp, int S, int O, int H, int W, double* a_o, cudaStream_t st);
+int build_mim_run(const double* a_o, int O, int H, int W, int* idx, double* amax, cudaStream_t st);
+
 // diagnostics: exact median of |z| per plane through the filter bank's median kernels
 size_t debug_median_workspace_bytes(int planes, int n);
 int debug_median_run(const float2* z, int planes, int n, float* amps, float* med, void* ws, size_t ws_bytes,

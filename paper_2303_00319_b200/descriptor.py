@@ -180,3 +180,62 @@ def read_descriptors(path) -> list:
     vec = rec["vec"].astype(np.float64)
     return [Descriptor(vec[i], int(rec["kp"][i]), int(rec["variant"][i]), _MODE_NAMES[int(rec["mode"][i])])
             for i in range(count)]
+
+
+def _snap(v: float) -> float:
+    """cos / sin snapping of ref: descriptor.py:59-60 (quarter turns exact)."""
+    if abs(v) < 1e-12:
+        return 0.0
+    if abs(abs(v) - 1.0) < 1e-12:
+        return float(np.copysign(1.0, v))
+    return float(v)
+
+
+def extract_patch(mim, keypoint, size: int, angle: float = 0.0, with_amplitude: bool = True):
+    """ref: descriptor.py:85-125 -- size x size index patch on a grid rotated
+    by `angle` about the keypoint, None when any sample leaves the map.  The
+    axis-aligned crop is a view (as the reference returns); rotated grids are
+    gathered by rift2_extract_patch with the reference's float64 offsets and
+    rounding."""
+    import torch
+    from . import engine
+    from .mim import IndexMap
+    h, w = mim.shape
+    if angle == 0.0:
+        x0 = int(np.floor(keypoint.x + 1.0 - size / 2.0))
+        y0 = int(np.floor(keypoint.y + 1.0 - size / 2.0))
+        if x0 < 0 or y0 < 0 or x0 + size > w or y0 + size > h:
+            return None
+        return mim.region(y0, y0 + size, x0, x0 + size)
+    idx = torch.from_numpy(np.ascontiguousarray(mim.indices, dtype=np.int32)).cuda()
+    amp = torch.from_numpy(np.ascontiguousarray(mim.max_amplitude, dtype=np.float64)).cuda() if with_amplitude else None
+    c, s = _snap(np.cos(angle)), _snap(np.sin(angle))
+    oi, oa, oob = engine.extract_patch(idx, amp, float(keypoint.x), float(keypoint.y), int(size), c, s, with_amplitude)
+    if oob:
+        return None
+    amplitude = oa.cpu().numpy() if with_amplitude else np.broadcast_to(0.0, (size, size))
+    return IndexMap(oi.cpu().numpy().astype(np.asarray(mim.indices).dtype, copy=False), amplitude, mim.n_orient)
+
+
+def encode(patch, grid: int = 6, weighted: bool = False):
+    """ref: descriptor.py:145-164 -- concatenated per-cell index histograms,
+    L2-normalised; None for the all-zero vector (weighted mode only).  The
+    cell counts come from rift2_patch_counts; the float64 normalisation is the
+    reference's own (v / ||v||), as describe_* rebuilds its vectors."""
+    import torch
+    from . import engine
+    from .mim import _check_values
+    idx = np.asarray(patch.indices)
+    h, w = idx.shape
+    if h != w or h % grid != 0:
+        raise ParameterError(f"patch {h}x{w} does not divide into {grid}x{grid} cells")
+    _check_values(idx, patch.n_orient)
+    d_idx = torch.from_numpy(np.ascontiguousarray(idx[None], dtype=np.int32)).cuda()
+    amp = torch.from_numpy(np.ascontiguousarray(np.asarray(patch.max_amplitude, dtype=np.float64)[None])).cuda() \
+        if weighted else None
+    _, cells = engine.patch_counts(d_idx, amp, patch.n_orient, grid, hist=False, cells=True)
+    vector = cells[0].cpu().numpy()
+    norm = np.linalg.norm(vector)
+    if norm == 0:
+        return None
+    return vector / norm

@@ -321,3 +321,112 @@ def synth_targets(src: torch.Tensor, params: torch.Tensor, looks: torch.Tensor, 
                                  src_copy.stride(0) if src_copy is not None else 0, _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "rift2_synth_targets")
     return dst
+
+
+# ---------------------------------------------------- unfused reference entry points
+def filter_bank(height: int, width: int, bank) -> torch.Tensor:
+    """rift2_filter_bank -> (S, O, H, W) float64 CUDA transfer functions."""
+    lib = _lib.load(require_gpu=True)
+    p = bank_c(bank)
+    out = torch.empty((int(bank.n_scales), int(bank.n_orient), int(height), int(width)), dtype=torch.float64,
+                      device="cuda")
+    _lib.check(lib.rift2_filter_bank(int(height), int(width), ctypes.byref(p), _ptr(out), _stream()),
+               "rift2_filter_bank")
+    return out
+
+
+def apply_bank(image: torch.Tensor, transfer: torch.Tensor, ws_key: str = "apply_bank"):
+    """rift2_apply_bank: image (H, W) float32 CUDA, transfer (S, O, H, W)
+    float32 CUDA -> (even, odd, amplitude) each (S, O, H, W) float32."""
+    lib = _lib.load(require_gpu=True)
+    H, W = image.shape
+    S, O = transfer.shape[:2]
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.rift2_apply_bank_workspace_size(H, W, S, O, ctypes.byref(nbytes)), "apply_bank")
+    ws = WORKSPACES.get(ws_key, nbytes.value)
+    outs = [torch.empty((S, O, H, W), dtype=torch.float32, device=image.device) for _ in range(3)]
+    _lib.check(lib.rift2_apply_bank(_ptr(image.contiguous()), H, W, S, O, _ptr(transfer.contiguous()),
+                                    *(_ptr(t) for t in outs), _ptr(ws), ws.numel(), _stream()), "rift2_apply_bank")
+    return tuple(outs)
+
+
+def pc_moments(even, odd, amplitude: torch.Tensor, bank, full: bool = True, ws_key: str = "pc_moments"):
+    """rift2_pc_moments on (S, O, H, W) float32 CUDA planes -> dict(a_o[,
+    pc, mmax, mmin]) float32."""
+    lib = _lib.load(require_gpu=True)
+    S, O, H, W = amplitude.shape
+    p = bank_c(bank)
+    dev = amplitude.device
+    out = {"a_o": torch.empty((O, H, W), dtype=torch.float32, device=dev)}
+    ws = None
+    if full:
+        out.update(pc=torch.empty((O, H, W), dtype=torch.float32, device=dev),
+                   mmax=torch.empty((H, W), dtype=torch.float32, device=dev),
+                   mmin=torch.empty((H, W), dtype=torch.float32, device=dev))
+        nbytes = ctypes.c_size_t()
+        _lib.check(lib.rift2_pc_moments_workspace_size(H, W, ctypes.byref(p), ctypes.byref(nbytes)), "pc_moments")
+        ws = WORKSPACES.get(ws_key, nbytes.value)
+    _lib.check(lib.rift2_pc_moments(_ptr(even.contiguous() if full else None), _ptr(odd.contiguous() if full else None),
+                                    _ptr(amplitude.contiguous()), H, W, ctypes.byref(p), _ptr(out["a_o"]),
+                                    _ptr(out.get("pc")), _ptr(out.get("mmax")), _ptr(out.get("mmin")), _ptr(ws),
+                                    0 if ws is None else ws.numel(), _stream()), "rift2_pc_moments")
+    return out
+
+
+def build_mim(a_o: torch.Tensor):
+    """rift2_build_mim: (O, H, W) float64 CUDA -> (indices int32, max_amplitude float64)."""
+    lib = _lib.load(require_gpu=True)
+    O, H, W = a_o.shape
+    idx = torch.empty((H, W), dtype=torch.int32, device=a_o.device)
+    amax = torch.empty((H, W), dtype=torch.float64, device=a_o.device)
+    _lib.check(lib.rift2_build_mim(_ptr(a_o.contiguous()), O, H, W, _ptr(idx), _ptr(amax), _stream()),
+               "rift2_build_mim")
+    return idx, amax
+
+
+def patch_counts(indices: torch.Tensor, amplitude: torch.Tensor | None, n_orient: int, grid: int = 0,
+                 hist: bool = True, cells: bool = False):
+    """rift2_patch_counts: indices (n, h, w) int32 CUDA, amplitude same shape
+    float64 or None -> (hist (n, n_orient) | None, cells (n, grid^2 n_orient) | None) float64."""
+    lib = _lib.load(require_gpu=True)
+    n, h, w = indices.shape
+    dev = indices.device
+    hh = torch.empty((n, n_orient), dtype=torch.float64, device=dev) if hist else None
+    c = torch.empty((n, grid * grid * n_orient), dtype=torch.float64, device=dev) if cells else None
+    _lib.check(lib.rift2_patch_counts(_ptr(indices.contiguous()), _ptr(None if amplitude is None else amplitude.contiguous()),
+                                      n, h, w, int(n_orient), int(grid), _ptr(hh), _ptr(c), _stream()),
+               "rift2_patch_counts")
+    return hh, c
+
+
+def remap_indices(indices: torch.Tensor, n_orient: int, pivot: int, kind: int) -> torch.Tensor:
+    """rift2_remap_indices in place on an int32 CUDA tensor (kind 0 recode, 1 cyclic shift)."""
+    lib = _lib.load(require_gpu=True)
+    _lib.check(lib.rift2_remap_indices(_ptr(indices), indices.numel(), int(n_orient), int(pivot), int(kind),
+                                       _stream()), "rift2_remap_indices")
+    return indices
+
+
+def extract_patch(indices: torch.Tensor, amplitude: torch.Tensor | None, x: float, y: float, size: int,
+                  cos_a: float, sin_a: float, with_amplitude: bool):
+    """rift2_extract_patch -> (indices (size, size) int32, amplitude float64 | None, out_of_bounds bool)."""
+    lib = _lib.load(require_gpu=True)
+    H, W = indices.shape
+    dev = indices.device
+    oi = torch.empty((size, size), dtype=torch.int32, device=dev)
+    oa = torch.empty((size, size), dtype=torch.float64, device=dev) if with_amplitude else None
+    oob = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(lib.rift2_extract_patch(_ptr(indices.contiguous()), _ptr(None if amplitude is None else amplitude.contiguous()),
+                                       H, W, float(x), float(y), int(size), float(cos_a), float(sin_a), _ptr(oi), _ptr(oa),
+                                       _ptr(oob), _stream()), "rift2_extract_patch")
+    return oi, oa, bool(oob.item())
+
+
+def orientation_amplitudes(amplitude: torch.Tensor) -> torch.Tensor:
+    """rift2_orientation_amplitudes: (S, O, H, W) float64 CUDA -> (O, H, W) float64."""
+    lib = _lib.load(require_gpu=True)
+    S, O, H, W = amplitude.shape
+    out = torch.empty((O, H, W), dtype=torch.float64, device=amplitude.device)
+    _lib.check(lib.rift2_orientation_amplitudes(_ptr(amplitude.contiguous()), S, O, H, W, _ptr(out), _stream()),
+               "rift2_orientation_amplitudes")
+    return out

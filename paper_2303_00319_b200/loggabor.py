@@ -1,10 +1,14 @@
-"""Phase-congruency data types and parameters, name-compatible with
-ref: pkg/src/rift2/loggabor.py:35-119.  The computation itself is the CUDA
-filter bank (csrc/fields.cu) reached through pipeline.compute_fields; this
-module holds the parameter/result types the callers exchange."""
+"""Log-Gabor filter bank and phase congruency, drop-in for
+ref: pkg/src/rift2/loggabor.py.  The pipeline path is the fused CUDA filter
+bank (csrc/fields.cu, rift2_fields) reached through pipeline.compute_fields;
+the reference's step-by-step entry points (build_filter_bank, apply_bank,
+orientation_amplitudes, phase_congruency_moments) run on their own CUDA
+kernels of the same library (rift2_filter_bank, rift2_apply_bank,
+rift2_orientation_amplitudes, rift2_pc_moments)."""
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -67,3 +71,89 @@ class PCField:
     @property
     def shape(self):
         return self.moment_max.shape
+
+
+def fft_workers(threads: int = 0) -> int:
+    """ref: loggabor.py:28-32 (worker count of the reference's CPU FFTs; kept
+    for API compatibility -- the transforms here run on the GPU)."""
+    if threads and threads > 0:
+        return threads
+    return os.cpu_count() or 1
+
+
+@dataclass(frozen=True)
+class FilterBank:
+    """Transfer functions (n_scales, n_orient, height, width) float64
+    (ref: loggabor.py:83-92)."""
+
+    transfer: np.ndarray
+    params: BankParams
+
+    @property
+    def shape(self):
+        return self.transfer.shape[2], self.transfer.shape[3]
+
+
+@dataclass(frozen=True)
+class ConvolutionStack:
+    """Even / odd quadrature responses and their amplitude per scale and
+    orientation, (n_scales, n_orient, height, width) (ref: loggabor.py:95-103)."""
+
+    even: np.ndarray
+    odd: np.ndarray
+    amplitude: np.ndarray
+    params: BankParams
+
+
+def build_filter_bank(width: int, height: int, params: BankParams | None = None) -> FilterBank:
+    """ref: loggabor.py:131-159 -- computed by the rift2_filter_bank kernel in
+    float64 with the reference's formulas."""
+    from . import engine
+    params = params or BankParams()
+    if width < 16 or height < 16:
+        raise ParameterError("filter bank needs width and height >= 16")
+    t = engine.filter_bank(int(height), int(width), params)
+    return FilterBank(transfer=t.cpu().numpy(), params=params)
+
+
+def apply_bank(img, bank: FilterBank, threads: int = 0) -> ConvolutionStack:
+    """ref: loggabor.py:162-185 -- the given bank applied by the CUDA FFT
+    passes (rift2_apply_bank, float32 arithmetic; float64 results)."""
+    import torch
+    from . import engine
+    from .pipeline import check_image
+    arr = check_image(img)
+    if arr.shape != bank.shape:
+        raise ParameterError(f"image shape {arr.shape} does not match bank shape {bank.shape}")
+    image = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).cuda()
+    transfer = torch.from_numpy(np.ascontiguousarray(bank.transfer, dtype=np.float32)).cuda()
+    even, odd, amp = engine.apply_bank(image, transfer)
+    return ConvolutionStack(even=even.double().cpu().numpy(), odd=odd.double().cpu().numpy(),
+                            amplitude=amp.double().cpu().numpy(), params=bank.params)
+
+
+def orientation_amplitudes(stack: ConvolutionStack) -> np.ndarray:
+    """ref: loggabor.py:188-190 -- sum over scales (rift2_orientation_amplitudes, float64)."""
+    import torch
+    from . import engine
+    amp = np.asarray(stack.amplitude, dtype=np.float64)
+    if amp.ndim != 4:
+        raise ParameterError(f"expected a (scales, orientations, h, w) stack, got shape {amp.shape}")
+    out = engine.orientation_amplitudes(torch.from_numpy(np.ascontiguousarray(amp)).cuda())
+    return out.cpu().numpy()
+
+
+def phase_congruency_moments(stack: ConvolutionStack, params: BankParams | None = None) -> PCField:
+    """ref: loggabor.py:193-251 -- per-orientation phase congruency and the
+    moment maps from a response stack (rift2_pc_moments, float32 arithmetic,
+    exact median noise floor)."""
+    import torch
+    from . import engine
+    params = params or stack.params
+    amp = np.asarray(stack.amplitude)
+    if amp.ndim != 4 or amp.shape[0] != params.n_scales or amp.shape[1] != params.n_orient:
+        raise ParameterError(f"stack shape {amp.shape} does not match the bank parameters")
+    planes = [torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda() for a in (stack.even, stack.odd, amp)]
+    out = engine.pc_moments(*planes, params)
+    return PCField(a_o=orientation_amplitudes(stack), pc_per_orientation=out["pc"].double().cpu().numpy(),
+                   moment_max=out["mmax"].double().cpu().numpy(), moment_min=out["mmin"].double().cpu().numpy())

@@ -20,6 +20,11 @@ import numpy as np
 from .errors import ParameterError
 
 TENSOR_K = 224   # descriptor length the tensor-core tiles cover
+# ref: matcher.py:25 -- the reference's target block size.  The GPU kernels
+# tile the distance matrix on their own; the name is kept so callers that
+# tune it (e.g. ref tests/test_matcher.py:105-111) keep working, and results
+# do not depend on it.
+_TARGET_BLOCK = 1024
 
 
 @dataclass
