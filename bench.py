@@ -360,6 +360,41 @@ def traffic():
         return None, None
 
 
+def ring_vs_rift2(pipe, reps: int = 5):
+    """CUDA-event time of describe + match per mode on the pipeline's current
+    keypoints (the reference benchmark's protocol: shared detection, ref
+    evalbench.py:282-325), plus descriptor counts and distance evaluations."""
+    import torch
+    from paper_2303_00319_b200 import engine
+    c = pipe.cfg
+    out = {}
+    for mode, desc_mode, per in (("rift2", "rift2", 2), ("ring", "ring_pipeline", c.n_orient)):
+        def run():
+            d = engine.describe(pipe.f["mim"], pipe.k["x"], pipe.k["y"], pipe.k["count"], c.n_orient, c.patch_size,
+                                c.grid, c.dominant_ratio, c.rotate_patch, desc_mode, capacity=per * pipe.K,
+                                ws_key=f"rvr_{mode}_d")
+            m = engine.match(d, pipe.dim, pipe.rb, pipe.tb, pipe.K, ws_key=f"rvr_{mode}_m")
+            return d, m
+        d, m = run()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a, b in ev:
+            a.record()
+            run()
+            b.record()
+        torch.cuda.synchronize()
+        cnt = d["count"].cpu().numpy().astype(np.int64)
+        out[mode] = {"ms": statistics.median(a.elapsed_time(b) for a, b in ev),
+                     "ref_descriptors": int(cnt[0::2].sum()), "tgt_descriptors": int(cnt[1::2].sum()),
+                     "distance_evals": int((cnt[0::2] * cnt[1::2]).sum())}
+    kps = int(pipe.k["count"].cpu().numpy()[0::2].sum())
+    return {"what": "describe + match of the whole batch per mode on shared keypoints (GPU, CUDA events)",
+            "rift2": out["rift2"], "ring": out["ring"], "ref_keypoints": kps,
+            "speedup": out["ring"]["ms"] / out["rift2"]["ms"],
+            "descriptor_reduction": out["ring"]["ref_descriptors"] / max(out["rift2"]["ref_descriptors"], 1),
+            "distance_eval_reduction": out["ring"]["distance_evals"] / max(out["rift2"]["distance_evals"], 1)}
+
+
 def dataclass_api_latency(cfg, size, seeds):
     """Wall time of paper_2303_00319_b200.match_pair (the reference's
     dataclass API: host float64 images in, Keypoint / Descriptor / MatchSet
@@ -468,6 +503,10 @@ def run_ours(args, rank, world, local_rank):
     matched_xy = torch.stack([host_out["kp_x"][0][r0], host_out["kp_y"][0][r0],
                               host_out["kp_x"][1][t0_], host_out["kp_y"][1][t0_]], 1)
 
+    # ring vs RIFT2 (ref evalbench.py:282-325, acceptance criteria 5-6): the
+    # description + matching stage of both modes on this batch's keypoints
+    ring = ring_vs_rift2(pipe) if world == 1 else None
+
     # dataclass drop-in API (ref pipeline.py:82-99): one pair per call,
     # north_star's configs[1] single-pair latency over seeds 0-15 on 1 GPU
     api = None
@@ -505,6 +544,7 @@ def run_ours(args, rank, world, local_rank):
                                "flops_per_launch": match_flops, "launch_ms": match_ms, "peak_source": tpk_src},
             "clocks": clocks,
             "single_pair_api": api,
+            "ring_vs_rift2": ring,
             "e2e_matched_points_pair0": int(matched_xy.shape[0]),
             "matches_per_pair": float(np.mean(counts))}
     if world == 1 and not args.no_cpu_baseline:

@@ -113,9 +113,11 @@ int32_t rift2_detect_f64(const double* min_maps, const double* max_maps, int32_t
  *   desc_variant [batch][desc_capacity] uint8 out: dominant index / layer
  *   desc_count   [batch] int32 out, desc_skipped [batch] int32 out
  * Descriptors are ordered by keypoint, then [peak, runner-up] (rift2) or
- * layer 1..n (ring).  mode: 0 plain, 1 ring, 2 rift2.
- * desc_capacity must be >= rows-per-keypoint (1 plain, n_orient ring,
- * 2 rift2) x kp_stride, else RIFT2_CAPACITY; kp_count values above
+ * layer 1..n (ring).  mode: 0 plain, 1 ring, 2 rift2, 3 the pipeline's ring
+ * mode (ref: pipeline.py:53-64): even blocks (reference side) ring, odd
+ * blocks (target side) plain.
+ * desc_capacity must be >= rows-per-keypoint (1 plain, n_orient ring and
+ * mode 3, 2 rift2) x kp_stride, else RIFT2_CAPACITY; kp_count values above
  * kp_stride are clamped to it. */
 int32_t rift2_describe_workspace_size(int32_t batch, int32_t kp_stride, int32_t grid, int32_t n_orient,
                                       size_t* bytes);

@@ -31,8 +31,13 @@ _INSTANCE_IDS = itertools.count()
 class BatchPipeline:
     def __init__(self, n_pairs: int, height: int, width: int, cfg: RiftConfig | None = None, device=None):
         self.cfg = cfg or RiftConfig()
-        if self.cfg.mode != "rift2":
-            raise ParameterError("the batched pipeline runs the rift2 mode")
+        # descriptor mode and rows per keypoint (ref: pipeline.py:53-64): rift2
+        # one or two per keypoint on both sides; ring n_orient cyclic layers on
+        # the reference side against plain targets; plain one per keypoint
+        modes = {"rift2": ("rift2", 2), "ring": ("ring_pipeline", self.cfg.n_orient), "plain": ("plain", 1)}
+        if self.cfg.mode not in modes:
+            raise ParameterError(f"unknown mode {self.cfg.mode!r}")
+        self.desc_mode, per = modes[self.cfg.mode]
         self.bank = self.cfg.bank_params()
         self.P, self.H, self.W = int(n_pairs), int(height), int(width)
         self.B = 2 * self.P
@@ -49,7 +54,8 @@ class BatchPipeline:
                       response=torch.zeros((B, K), dtype=torch.float64, device=d),
                       kind=torch.zeros((B, K), dtype=torch.uint8, device=d),
                       count=torch.zeros((B,), dtype=torch.int32, device=d))
-        cap = 2 * K
+        cap = per * K
+        self.cap = cap
         self.d = dict(counts=torch.zeros((B, cap, engine.DESC_STRIDE), dtype=torch.float16, device=d),
                       sqnorm=torch.zeros((B, cap), dtype=torch.int32, device=d),
                       kp=torch.zeros((B, cap), dtype=torch.int32, device=d),
@@ -83,7 +89,7 @@ class BatchPipeline:
         engine.detect(f["mmin"], f["mmax"], c.fast_threshold, self.K, c.patch_size // 2, ws_key=ws + "detect",
                       out=self.k)
         engine.describe(f["mim"], self.k["x"], self.k["y"], self.k["count"], c.n_orient, c.patch_size, c.grid,
-                        c.dominant_ratio, c.rotate_patch, "rift2", capacity=2 * self.K, ws_key=ws + "describe",
+                        c.dominant_ratio, c.rotate_patch, self.desc_mode, capacity=self.cap, ws_key=ws + "describe",
                         out=self.d)
         engine.match(self.d, self.dim, self.rb, self.tb, self.K, ws_key=ws + "match", out=self.m)
 

@@ -228,9 +228,10 @@ int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_
   if (patch_size > 256 || grid > 16 || grid * grid * n_orient > desc_stride)
     return fail(RIFT2_UNSUPPORTED, "patch_size <= 256, grid <= 16 and grid^2*n_orient <= desc_stride required");
   if (!(dominant_ratio > 0 && dominant_ratio <= 1)) return fail(RIFT2_BAD_ARGUMENT, "dominant_ratio in (0, 1]");
-  if (mode < 0 || mode > 2) return fail(RIFT2_BAD_ARGUMENT, "mode must be 0 plain, 1 ring, 2 rift2");
+  if (mode < 0 || mode > 3)
+    return fail(RIFT2_BAD_ARGUMENT, "mode must be 0 plain, 1 ring, 2 rift2, 3 ring reference / plain target");
   // every keypoint yields at most `per` rows, so this capacity can never overflow
-  const int64_t per = mode == 0 ? 1 : (mode == 1 ? n_orient : 2);
+  const int64_t per = mode == 0 ? 1 : ((mode == 1 || mode == 3) ? n_orient : 2);
   if ((int64_t)desc_capacity < per * kp_stride)
     return fail(RIFT2_CAPACITY, "desc_capacity %d < %lld rows per keypoint x kp_stride %d", desc_capacity,
                 (long long)per, kp_stride);

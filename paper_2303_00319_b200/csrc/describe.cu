@@ -275,6 +275,9 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   __shared__ int s_k;
   __shared__ unsigned s_excl;
   const int b = blockIdx.y;
+  // mode 3 is the reference pipeline's ring mode (ref: pipeline.py:53-64):
+  // the reference side (even blocks) ring, the target side (odd blocks) plain
+  const int mode = c.mode == 3 ? ((b & 1) ? 0 : 1) : c.mode;
   // keypoints are taken in CTA start order (a per-image ticket), so every
   // keypoint before this one belongs to a CTA that has already started: the
   // look-back below only waits on running CTAs
@@ -373,8 +376,8 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
 #pragma unroll
     for (int v = 0; v < 8; ++v) hs[v] = v < O ? s_hist[v] : 0u;
     int skip = 0;
-    if (c.mode == 0) { pick[np++] = 1; }
-    else if (c.mode == 1) {
+    if (mode == 0) { pick[np++] = 1; }
+    else if (mode == 1) {
 #pragma unroll
       for (int v = 1; v <= kMaxPick; ++v) if (v <= O) pick[np++] = v;
     } else {
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
     }
   }
   // count the rotated picks (at most two) into their own buffers
-  const bool rot_mode = c.mode == 2 && c.rotate;
+  const bool rot_mode = mode == 2 && c.rotate;
   const int dom90 = (O % 2 == 0 && c.P % 2 == 0) ? O / 2 + 1 : -1;
   int nrot = 0;
 #pragma unroll
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
     if (dst < (unsigned)a.cap) {
       const size_t o = (size_t)b * a.cap + dst;
       __half* row = a.counts + o * a.stride;
-      const int var = c.mode == 0 ? 1 : dom;
+      const int var = mode == 0 ? 1 : dom;
       if (rot_mode && dom == dom90) emit_row_rot90<OT, GT>(a, c, cnt, dom, row);
       else emit_row<OT, GT>(a, c, rotated ? cnt_rot[r] : cnt, var, row);
       if (threadIdx.x == 0) {
@@ -484,7 +487,7 @@ struct DescWs {
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-int per_kp(int mode, int O) { return mode == 1 ? O : (mode == 2 ? 2 : 1); }
+int per_kp(int mode, int O) { return (mode == 1 || mode == 3) ? O : (mode == 2 ? 2 : 1); }
 
 DescWs plan_ws(int B, int S) {
   DescWs p{};

@@ -121,7 +121,7 @@ def detect(mins: torch.Tensor, maxs: torch.Tensor | None, threshold: float, max_
     return out
 
 
-MODE_CODE = {"plain": 0, "ring": 1, "rift2": 2}
+MODE_CODE = {"plain": 0, "ring": 1, "rift2": 2, "ring_pipeline": 3}
 
 
 def describe(mim: torch.Tensor, kp_x: torch.Tensor, kp_y: torch.Tensor, kp_count: torch.Tensor,
@@ -132,7 +132,7 @@ def describe(mim: torch.Tensor, kp_x: torch.Tensor, kp_y: torch.Tensor, kp_count
     lib = _lib.load(require_gpu=True)
     B, H, W = mim.shape
     S = kp_x.shape[1]
-    per = {"plain": 1, "ring": n_orient, "rift2": 2}[mode]
+    per = {"plain": 1, "ring": n_orient, "rift2": 2, "ring_pipeline": n_orient}[mode]
     cap = capacity if capacity is not None else max(S * per, 1)
     dim = grid * grid * n_orient
     stride = DESC_STRIDE if dim <= DESC_STRIDE else int(math.ceil(dim / 32) * 32)

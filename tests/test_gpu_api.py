@@ -273,3 +273,29 @@ def test_run_from_host_pipelined_results(r2):
         for p, n in enumerate(w["count"].tolist()):            # rows past count are stale workspace
             for k in ("ref", "tgt", "dist"):
                 assert torch.equal(w[k][p, :n], out[k][p, :n]), (steps, p, k)
+
+
+@pytest.mark.parametrize("mode", ["ring", "plain"])
+def test_batch_pipeline_ring_and_plain_modes(r2, mode):
+    """BatchPipeline in the reference's other modes (ref: pipeline.py:53-64:
+    ring = n_orient cyclic layers on the reference side against plain
+    targets): the same matches as the dataclass API, and the ring reference
+    side carries exactly n_orient rows per described keypoint."""
+    from paper_2303_00319_b200 import synth
+    cfg = r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=700, mode=mode)
+    imgs, _ = synth.make_batch(2, 256, seed0=7, looks=None)
+    pipe = r2.BatchPipeline(2, 256, 256, cfg)
+    pipe.load(imgs)
+    pipe.capture()
+    pipe.step()
+    torch.cuda.synchronize()
+    res = pipe.matches_host()
+    dcount = pipe.d["count"].cpu().numpy()
+    for p in range(2):
+        api = r2.match_pair(imgs[2 * p].astype(np.float64), imgs[2 * p + 1].astype(np.float64), cfg)
+        assert list(zip(res[p][0].tolist(), res[p][1].tolist())) == [(a, b) for a, b, _ in api.matches.pairs]
+        np.testing.assert_allclose(res[p][2], [d for _, _, d in api.matches.pairs], rtol=0, atol=0)
+        assert dcount[2 * p] == len(api.ref.descriptors) and dcount[2 * p + 1] == len(api.tgt.descriptors)
+        if mode == "ring":
+            assert dcount[2 * p] == 6 * len({d.keypoint_id for d in api.ref.descriptors})
+            assert dcount[2 * p + 1] == len({d.keypoint_id for d in api.tgt.descriptors})
