@@ -180,8 +180,6 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 6 : 1) k_fast_nms(const 
                                                   unsigned* __restrict__ cnt, size_t cap) {
   __shared__ __align__(16) T sv[kInY][kIn + 1];
   __shared__ double ss[kScY][kSc + 1];
-  __shared__ unsigned short s_list[kScY * kSc];   // score positions that need the full arc test
-  __shared__ unsigned s_n;
   const int plane = blockIdx.z;
   const int kind = nm == 2 ? (plane & 1) : 0;
   const T* p = plane_ptr(mins, maxs, plane, nm, (size_t)H * W);
@@ -215,60 +213,20 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 6 : 1) k_fast_nms(const 
       }
     }
   }
-  if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  // Pre-screen (exact): a pixel can score above thr only if some 9-arc of
-  // its ring beats the centre by more than thr * span on the raw map, and
-  // every 9-arc contains two compass pixels 4 apart (ring positions 0, 4,
-  // 8, 12).  Pixels failing it score <= thr: they are never candidates and
-  // never beat a candidate in the 3x3 NMS, so they keep score 0 (the slack
-  // 1e-6 * thr dwarfs the float64 rounding of the normalisation).  The full
-  // arc scores run only on the compacted list of survivors.
-  const double t_raw = thr * span * (1.0 - 1e-6);
-  auto screen = [&](int sy, int sx, int y, int x, bool in) {
-    double base;
-    bool full = in;
-    if (!in) {
-      if (y < 0 || y >= H || x < 0 || x >= W) { base = -DBL_MAX; full = false; }
-      else if (y < 3 || y >= H - 3 || x < 3 || x >= W - 3) { base = 0.0; full = false; }
-      else { base = 0.0; full = true; }
-    } else {
-      base = 0.0;
-    }
-    if (full) {
-      const int cy = sy + kHalo - 1, cx = sx + kHalo - 1;
-      const double c = (double)sv[cy][cx];
-      const double n0 = (double)sv[cy - 3][cx], n4 = (double)sv[cy][cx + 3];
-      const double n8 = (double)sv[cy + 3][cx], n12 = (double)sv[cy][cx - 3];
-      const bool b0 = n0 - c > t_raw, b4 = n4 - c > t_raw, b8 = n8 - c > t_raw, b12 = n12 - c > t_raw;
-      const bool d0 = c - n0 > t_raw, d4 = c - n4 > t_raw, d8 = c - n8 > t_raw, d12 = c - n12 > t_raw;
-      full = (b0 && b4) || (b4 && b8) || (b8 && b12) || (b12 && b0) ||
-             (d0 && d4) || (d4 && d8) || (d8 && d12) || (d12 && d0);
-    }
-    ss[sy][sx] = base;
-    const unsigned slot = agg_inc(&s_n, full);
-    if (full) s_list[slot] = (unsigned short)(sy * kSc + sx);
-  };
-  // interior 32 x 64: warp = row group, lane = column
+  // interior 32 x 32 scores: warp = row group, lane = column
 #pragma unroll 1
-  for (int r = warp; r < kTileY; r += 8) screen(r + 1, lane + 1, ty0 + r, tx0 + lane, inner);
+  for (int r = warp; r < kTileY; r += 8)
+    ss[r + 1][lane + 1] = tile_score(sv, r + 1, lane + 1, ty0 + r, tx0 + lane, H, W, inner, lo, span, rspan);
   // the one-pixel border ring of the score tile (196 positions)
-  {
-    int sy = 0, sx = 0;
+  if (threadIdx.x < 2 * kSc + 2 * kTileY) {
+    int sy, sx;
     const int i = threadIdx.x;
-    const bool on = i < 2 * kSc + 2 * kTileY;
     if (i < kSc) { sy = 0; sx = i; }
     else if (i < 2 * kSc) { sy = kScY - 1; sx = i - kSc; }
     else if (i < 2 * kSc + kTileY) { sy = 1 + i - 2 * kSc; sx = 0; }
-    else if (on) { sy = 1 + i - 2 * kSc - kTileY; sx = kSc - 1; }
-    if (on) screen(sy, sx, ty0 - 1 + sy, tx0 - 1 + sx, false);
-    else agg_inc(&s_n, false);                    // every lane joins the warp-wide ballot
-  }
-  __syncthreads();
-  const int n_full = (int)s_n;
-  for (int i = threadIdx.x; i < n_full; i += blockDim.x) {
-    const int q = s_list[i], sy = q / kSc, sx = q - sy * kSc;
-    ss[sy][sx] = fast_score(sv, sy + kHalo - 1, sx + kHalo - 1, lo, span, rspan);
+    else { sy = 1 + i - 2 * kSc - kTileY; sx = kSc - 1; }
+    ss[sy][sx] = tile_score(sv, sy, sx, ty0 - 1 + sy, tx0 - 1 + sx, H, W, false, lo, span, rspan);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kTileY * kTile; i += blockDim.x) {

@@ -530,18 +530,18 @@ __global__ void __launch_bounds__(256) k_match_combine(MatchArgs a, IdxWs w, con
     const int r0 = w.rstart[(size_t)pair * a.cap + best.kp], r1 = w.rend[(size_t)pair * a.cap + best.kp];
     dmin = r1 > r0 ? 1e300 : INFINITY;
     for (int r = r0; r < r1; ++r) {
-      const double nr = sqrt((double)a.sqnorm[(size_t)rb * a.cap + r]);
+      const double ir = 1.0 / sqrt((double)a.sqnorm[(size_t)rb * a.cap + r]);
       const __half* cr = a.counts + ((size_t)rb * a.cap + r) * a.stride;
       for (int t = t0; t < t1; ++t) {
-        const double nt = sqrt((double)a.sqnorm[(size_t)tb * a.cap + t]);
+        const double it = 1.0 / sqrt((double)a.sqnorm[(size_t)tb * a.cap + t]);
         const __half* ct = a.counts + ((size_t)tb * a.cap + t) * a.stride;
         double acc = 0.0;
         for (int i = lane; i < a.dim; i += 32) {
-          // reference vectors are c / ||c|| in float64 (ref: descriptor.py:161-164),
-          // each component rounded on its own (no FMA contraction): equal
+          // reference vectors are c / ||c|| in float64 (ref: descriptor.py:161-164);
+          // both products rounded on their own (no FMA contraction), so equal
           // descriptors are at distance exactly 0, as in the reference
-          const double dv = __dsub_rn(__ddiv_rn((double)__half2float(cr[i]), nr),
-                                      __ddiv_rn((double)__half2float(ct[i]), nt));
+          const double dv = __dsub_rn(__dmul_rn((double)__half2float(cr[i]), ir),
+                                      __dmul_rn((double)__half2float(ct[i]), it));
           acc = fma(dv, dv, acc);
         }
 #pragma unroll

@@ -94,10 +94,12 @@ def _run(mim, keypoints, patch_size, grid, ratio, rotate, weighted, mode) -> Des
     counts = out["counts"][0, :n, :dim].to(torch.int64).cpu().numpy()
     kps = out["kp"][0, :n].cpu().numpy()
     var = out["variant"][0, :n].cpu().numpy()
-    descs = []
-    for c, k, v in zip(counts, kps, var):
-        vec = c.astype(np.float64)
-        descs.append(Descriptor(vec / np.linalg.norm(vec), int(k), int(v), mode, c))
+    # the reference's vector is counts / ||counts|| (ref: descriptor.py:161-164);
+    # the counts are integers, so c.c is exact in any summation order and the
+    # row-wise norm and division below are bit-identical to the per-vector ones
+    vecs = counts.astype(np.float64)
+    vecs /= np.sqrt(np.einsum("ij,ij->i", vecs, vecs))[:, None]
+    descs = [Descriptor(vec, int(k), int(v), mode, c) for vec, c, k, v in zip(vecs, counts, kps.tolist(), var.tolist())]
     return DescriptorSet(descs, int(out["skipped"][0]))
 
 
