@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--max-kp", type=int, default=5000, help="max keypoints per image (configs[3]: 20000)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the configs[3] / [4] side measurements")
     return ap.parse_args()
 
 
@@ -395,6 +396,56 @@ def ring_vs_rift2(pipe, reps: int = 5):
             "distance_eval_reduction": out["ring"]["distance_evals"] / max(out["rift2"]["distance_evals"], 1)}
 
 
+def other_configs(reps: int = 10) -> dict:
+    """BASELINE.json configs[3] and [4] on this GPU, pipelined steps with
+    inputs resident, CUDA events (the headline line is configs[1]/[2]):
+    configs[3] one 4096^2 pair (blob sigma x4, <= 20,000 keypoints);
+    configs[4] 64 pairs of 512^2 per step from the rotation sweep (theta in
+    15-degree steps, scale jitter 0.1, speckle looks 1 / 4 / 16)."""
+    import torch
+    from paper_2303_00319_b200 import BatchPipeline, RiftConfig, synth
+    out = {}
+    for name, size, n, kp in (("configs[3]", 4096, 1, 20000), ("configs[4]", 512, 64, 5000)):
+        if name == "configs[3]":
+            imgs, _ = synth.make_batch(1, 4096, seed0=0)
+        else:
+            imgs = np.empty((2 * n, size, size), np.float32)
+            for i in range(n):
+                th = 15 * (i % 24)
+                a, b, _ = synth.make_pair(size, seed=5000 + i, theta_deg=float(th), scale_jitter=0.1,
+                                          looks=(1, 4, 16)[(i // 24 + i) % 3])
+                imgs[2 * i], imgs[2 * i + 1] = a, b
+        pipe = BatchPipeline(n, size, size, RiftConfig(max_keypoints=kp, **BASE_PARAMS))
+        pipe.load(imgs)
+        pipe.capture_pipelined()
+        pipe._alt.copy_(pipe.images)
+        for i in range(3):
+            pipe.pipelined_step(i)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(reps):
+            pipe.pipelined_step(i + 1)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(reps):
+            pipe.replay_fields()
+        f1.record()
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1) / reps
+        byts = BYTES_PER_PX * size * size * 2 * n
+        out[name] = {"pairs_per_step": n, "size": size, "max_keypoints": kp, "ms_per_step": ms,
+                     "pairs_per_s": n / (ms / 1e3), "filter_bank_ms": fms,
+                     "filter_bank_frac_hbm": byts / (fms / 1e3) / 1e9 / peaks()[0],
+                     "matches_pair0": int(pipe.m["count"][0])}
+        del pipe
+        torch.cuda.empty_cache()
+    return out
+
+
 def dataclass_api_latency(cfg, size, seeds):
     """Wall time of paper_2303_00319_b200.match_pair (the reference's
     dataclass API: host float64 images in, Keypoint / Descriptor / MatchSet
@@ -466,13 +517,27 @@ def run_ours(args, rank, world, local_rank):
     from paper_2303_00319_b200 import engine
     engine.match(pipe.d, pipe.dim, pipe.rb, pipe.tb, pipe.K, ws_key="bench_match")   # allocates its workspace
     torch.cuda.synchronize()
-    em = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    for i in range(K):
-        em[i][0].record()
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    m0.record()
+    for _ in range(K):                      # back to back (see the GEMM timing below)
         engine.match(pipe.d, pipe.dim, pipe.rb, pipe.tb, pipe.K, ws_key="bench_match")
-        em[i][1].record()
+    m1.record()
     torch.cuda.synchronize()
-    match_ms = sum(a.elapsed_time(b) for a, b in em) / K
+    match_ms = m0.elapsed_time(m1) / K
+    # the tensor-core GEMM kernel alone (rift2_match_partial launches exactly
+    # k_match_gemm, with the same single column split the batch uses)
+    parts = engine.match_partial(pipe.d, pipe.dim, pipe.rb, pipe.tb)
+    torch.cuda.synchronize()
+    # back to back between two events: the host-side launch preparation
+    # (tensor-map encoding) overlaps the previous launch instead of leaving
+    # the device idle inside the timed interval
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    for _ in range(K):
+        engine.match_partial(pipe.d, pipe.dim, pipe.rb, pipe.tb, out=parts)
+    g1.record()
+    torch.cuda.synchronize()
+    gemm_ms = g0.elapsed_time(g1) / K
     dcnt = pipe.d["count"].cpu().numpy().astype(np.int64)
     match_flops = float(sum(2 * dcnt[2 * q] * dcnt[2 * q + 1] * pipe.dim for q in range(args.pairs)))
 
@@ -509,9 +574,11 @@ def run_ours(args, rank, world, local_rank):
 
     # dataclass drop-in API (ref pipeline.py:82-99): one pair per call,
     # north_star's configs[1] single-pair latency over seeds 0-15 on 1 GPU
-    api = None
+    api = others = None
     if world == 1 and args.size <= 1024:
         api = dataclass_api_latency(cfg, args.size, seeds=range(16))
+        if not args.no_other_configs:
+            others = other_configs()
 
     total_ms, e2e_ms, fields_ms = max_over_ranks([total_ms, e2e_ms, fields_ms], world, "cuda")
     if rank != 0:
@@ -542,8 +609,15 @@ def run_ours(args, rank, world, local_rank):
                                "achieved": match_flops / (match_ms / 1e3) / 1e12, "peak": tpk, "unit": "TFLOP/s",
                                "frac": match_flops / (match_ms / 1e3) / 1e12 / tpk,
                                "flops_per_launch": match_flops, "launch_ms": match_ms, "peak_source": tpk_src},
+            "roofline_gemm": {"bound": "tensor", "kernel": "k_match_gemm (tcgen05 kind::f16, TMEM accumulators, "
+                                                            "TMA operands, fused exact argmax epilogue)",
+                              "achieved": match_flops / (gemm_ms / 1e3) / 1e12, "peak": tpk, "unit": "TFLOP/s",
+                              "frac": match_flops / (gemm_ms / 1e3) / 1e12 / tpk, "flops_per_launch": match_flops,
+                              "launch_ms": gemm_ms, "peak_source": tpk_src,
+                              "note": "algorithmic 2*N_ref*N_tgt*216 flops; the kernel multiplies K=224 (zero padded)"},
             "clocks": clocks,
             "single_pair_api": api,
+            "other_configs": others,
             "ring_vs_rift2": ring,
             "e2e_matched_points_pair0": int(matched_xy.shape[0]),
             "matches_per_pair": float(np.mean(counts))}

@@ -44,7 +44,8 @@ def test_our_arm_json():
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    d = _run(["--size", "256", "--pairs", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"], 900)
+    d = _run(["--size", "256", "--pairs", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+              "--no-other-configs"], 900)
     _common(d)
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3
     r = d["roofline"]
