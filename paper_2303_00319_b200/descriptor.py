@@ -39,6 +39,10 @@ class Descriptor:
     variant: int
     mode: str
     counts: np.ndarray | None = field(default=None, compare=False, repr=False)
+    # the describe call's (n, dim) count matrix and this row in it: lets
+    # match_nn gather whole descriptor lists without restacking them
+    _src: np.ndarray | None = field(default=None, compare=False, repr=False)
+    _row: int = field(default=-1, compare=False, repr=False)
 
 
 @dataclass
@@ -99,7 +103,8 @@ def _run(mim, keypoints, patch_size, grid, ratio, rotate, weighted, mode) -> Des
     # row-wise norm and division below are bit-identical to the per-vector ones
     vecs = counts.astype(np.float64)
     vecs /= np.sqrt(np.einsum("ij,ij->i", vecs, vecs))[:, None]
-    descs = [Descriptor(vec, int(k), int(v), mode, c) for vec, c, k, v in zip(vecs, counts, kps.tolist(), var.tolist())]
+    descs = [Descriptor(vec, k, v, mode, c, counts, i)
+             for i, (vec, c, k, v) in enumerate(zip(vecs, counts, kps.tolist(), var.tolist()))]
     return DescriptorSet(descs, int(out["skipped"][0]))
 
 

@@ -80,7 +80,13 @@ def _match_counts(ref_descs, tgt_descs):
     sq = np.zeros((2, cap), np.int32)
     kp = np.zeros((2, cap), np.int32)
     for side, (descs, order, dense) in enumerate(((ref_descs, r_ord, r_dense), (tgt_descs, t_ord, t_dense))):
-        c = np.stack([descs[i].counts for i in order]).astype(np.int64)
+        src = getattr(descs[0], "_src", None)
+        if src is not None and all(getattr(d, "_src", None) is src for d in descs):
+            # rows of one describe call's count matrix: one fancy-index gather
+            rows = np.fromiter((d._row for d in descs), dtype=np.int64, count=len(descs))
+            c = src[rows[order]]
+        else:
+            c = np.stack([descs[i].counts for i in order]).astype(np.int64)
         counts[side, :len(order), :dim] = c
         sq[side, :len(order)] = (c * c).sum(1)
         kp[side, :len(order)] = dense
