@@ -236,6 +236,19 @@ int32_t rift2_evaluate(const int32_t* kp_x, const int32_t* kp_y, const int32_t* 
  *   dst_src_copy + i*copy_image_stride : optional float32 copy of the source
  *     (NULL = none), e.g. the reference slot of a [ref, tgt, ...] batch. */
 int32_t rift2_synth_workspace_size(int32_t n_images, int32_t height, int32_t width, size_t* bytes);
+/* Image 1 of the generator on the device:
+ * rift2_synth_blobs: out [n_images][height][width] float64 = the sum of
+ *   n_blobs anisotropic Gaussian blobs per image, blobs [n_images][n_blobs]
+ *   [11] = cx, cy, sx, sy, cos phi, sin phi, amp, x0, x1, y0, y1 (the
+ *   blob's window [x0, x1) x [y0, y1)), added in order in float64;
+ * rift2_synth_normals: out [n_images][n] float32 standard normals
+ *   (Philox4x32-10, counter (pixel pair, first_image + i, 0x5eed), key
+ *   seed; Box-Muller) -- the white noise of the band-limited component,
+ *   which rift2_apply_bank with a 0/1 radial mask then filters. */
+int32_t rift2_synth_blobs(const double* blobs, int32_t n_images, int32_t n_blobs, int32_t height, int32_t width,
+                          double* out, void* stream);
+int32_t rift2_synth_normals(uint64_t seed, int32_t first_image, int32_t n_images, int64_t n, float* out,
+                            void* stream);
 int32_t rift2_synth_targets(const double* src, int64_t src_image_stride, int32_t n_images, int32_t height,
                             int32_t width, const double* params, const int32_t* looks, uint64_t seed,
                             int32_t first_image, float* dst, int64_t dst_image_stride, float* dst_src_copy,

@@ -60,6 +60,8 @@ _SIGNATURES = {
     "rift2_evaluate": (_c_int, [_c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_int, _c_int, _c_p, _c_d,
                                 _c_d, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "rift2_synth_workspace_size": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
+    "rift2_synth_blobs": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p]),
+    "rift2_synth_normals": (_c_int, [ctypes.c_uint64, _c_int, _c_int, ctypes.c_int64, _c_p, _c_p]),
     "rift2_synth_targets": (_c_int, [_c_p, ctypes.c_int64, _c_int, _c_int, _c_int, _c_p, _c_p, ctypes.c_uint64,
                                      _c_int, _c_p, ctypes.c_int64, _c_p, ctypes.c_int64, _c_p, _c_sz, _c_p]),
     "rift2_filter_bank": (_c_int, [_c_int, _c_int, ctypes.POINTER(BankParamsC), _c_p, _c_p]),

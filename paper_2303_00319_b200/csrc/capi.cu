@@ -350,6 +350,21 @@ int32_t rift2_evaluate(const int32_t* kp_x, const int32_t* kp_y, const int32_t* 
   return map_internal(r2::evaluate_run(a, static_cast<cudaStream_t>(stream)), "rift2_evaluate");
 }
 
+int32_t rift2_synth_blobs(const double* blobs, int32_t n_images, int32_t n_blobs, int32_t height, int32_t width,
+                          double* out, void* stream) {
+  if (n_images < 0 || n_blobs < 0 || height < 1 || width < 1 || !out || (n_blobs > 0 && !blobs))
+    return fail(RIFT2_BAD_ARGUMENT, "bad blob arguments");
+  return map_internal(r2::blobs_run(blobs, n_images, n_blobs, height, width, out, static_cast<cudaStream_t>(stream)),
+                      "rift2_synth_blobs");
+}
+
+int32_t rift2_synth_normals(uint64_t seed, int32_t first_image, int32_t n_images, int64_t n, float* out,
+                            void* stream) {
+  if (n_images < 0 || n < 0 || (n > 0 && !out)) return fail(RIFT2_BAD_ARGUMENT, "bad normals arguments");
+  return map_internal(r2::normals_run(seed, first_image, n_images, (size_t)n, out, static_cast<cudaStream_t>(stream)),
+                      "rift2_synth_normals");
+}
+
 int32_t rift2_synth_workspace_size(int32_t n_images, int32_t height, int32_t width, size_t* bytes) {
   if (n_images < 0 || height < 2 || width < 2 || !bytes) return fail(RIFT2_BAD_ARGUMENT, "bad synthesis sizes");
   *bytes = r2::synth_workspace_bytes(n_images, height, width);

@@ -158,7 +158,68 @@ __global__ void __launch_bounds__(kSynthThreads) k_synth_norm(SynthArgs a, const
   }
 }
 
+// Image 1 of the generator (synth.blob_field): the sum of anisotropic
+// Gaussian blobs, one thread per pixel adding the blobs in draw order (the
+// host adds them blob by blob in the same order), in numpy's operation
+// order without FMA contraction; blob b of image i is blobs[(i * n + b) * 11]
+// = cx, cy, sx, sy, cos phi, sin phi, amp, x0, x1, y0, y1 (window [x0, x1) x
+// [y0, y1), empty windows skipped).
+__global__ void __launch_bounds__(256) k_blobs(const double* __restrict__ blobs, int n_blobs, int H, int W,
+                                               double* __restrict__ out) {
+  const int img = blockIdx.y;
+  const size_t n = (size_t)H * W;
+  const double* bl = blobs + (size_t)img * n_blobs * 11;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / W), x = (int)(i % W);
+    double acc = 0.0;
+    for (int b = 0; b < n_blobs; ++b) {
+      const double* q = bl + (size_t)b * 11;
+      if (x < (int)q[7] || x >= (int)q[8] || y < (int)q[9] || y >= (int)q[10]) continue;
+      const double dx = __dsub_rn((double)x, q[0]), dy = __dsub_rn((double)y, q[1]);
+      const double u = __dadd_rn(__dmul_rn(q[4], dx), __dmul_rn(q[5], dy));
+      const double v = __dadd_rn(__dmul_rn(-q[5], dx), __dmul_rn(q[4], dy));
+      const double a = __ddiv_rn(u, q[2]), c = __ddiv_rn(v, q[3]);
+      const double e = exp(__dmul_rn(-0.5, __dadd_rn(__dmul_rn(a, a), __dmul_rn(c, c))));
+      acc = __dadd_rn(acc, __dmul_rn(q[6], e));
+    }
+    out[(size_t)img * n + i] = acc;
+  }
+}
+
+// Standard normals from Philox4x32-10 (Box-Muller on two 53-bit uniforms),
+// counter (pixel pair, image, 0x5eed) and key seed: the device draw of the
+// white noise behind the band-limited component.
+__global__ void __launch_bounds__(256) k_normals(unsigned long long seed, int first_image, size_t n,
+                                                 float* __restrict__ out) {
+  const int img = blockIdx.y;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 r = philox(make_uint4((unsigned)i, (unsigned)(i >> 32), (unsigned)(first_image + img), 0x5eedu),
+                           (unsigned)seed, (unsigned)(seed >> 32));
+    const double u1 = u53(r.x, r.y), u2 = u53(r.z, r.w);
+    const double rad = sqrt(-2.0 * log(u1));
+    const double t = 6.283185307179586 * u2;
+    float* o = out + (size_t)img * n;
+    o[2 * i] = (float)(rad * cos(t));
+    if (2 * i + 1 < n) o[2 * i + 1] = (float)(rad * sin(t));
+  }
+}
+
 }  // namespace
+
+int blobs_run(const double* blobs, int n_images, int n_blobs, int H, int W, double* out, cudaStream_t st) {
+  if (n_images <= 0) return 0;
+  const size_t n = (size_t)H * W;
+  const unsigned gx = (unsigned)((n + 255) / 256 < 2048 ? (n + 255) / 256 : 2048);
+  k_blobs<<<dim3(gx, n_images), 256, 0, st>>>(blobs, n_blobs, H, W, out);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
+
+int normals_run(unsigned long long seed, int first_image, int n_images, size_t n, float* out, cudaStream_t st) {
+  if (n_images <= 0) return 0;
+  const unsigned gx = (unsigned)((n / 2 + 255) / 256 < 2048 ? (n / 2 + 255) / 256 : 2048);
+  k_normals<<<dim3(gx, n_images), 256, 0, st>>>(seed, first_image, n, out);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+}
 
 size_t synth_workspace_bytes(int n_images, int H, int W) {
   return (((size_t)n_images * H * W * sizeof(double) + 255) & ~(size_t)255) + (size_t)n_images * 16;

@@ -25,6 +25,8 @@ struct SynthArgs {
 };
 
 size_t synth_workspace_bytes(int n_images, int H, int W);
+int blobs_run(const double* blobs, int n_images, int n_blobs, int H, int W, double* out, cudaStream_t st);
+int normals_run(unsigned long long seed, int first_image, int n_images, size_t n, float* out, cudaStream_t st);
 int synth_run(const SynthArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace r2

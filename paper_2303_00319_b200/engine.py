@@ -430,3 +430,22 @@ def orientation_amplitudes(amplitude: torch.Tensor) -> torch.Tensor:
     _lib.check(lib.rift2_orientation_amplitudes(_ptr(amplitude.contiguous()), S, O, H, W, _ptr(out), _stream()),
                "rift2_orientation_amplitudes")
     return out
+
+
+def synth_blobs(blobs: torch.Tensor, height: int, width: int) -> torch.Tensor:
+    """rift2_synth_blobs: blobs (n, n_blobs, 11) float64 CUDA -> (n, H, W) float64."""
+    lib = _lib.load(require_gpu=True)
+    n, nb = blobs.shape[:2]
+    out = torch.empty((n, height, width), dtype=torch.float64, device=blobs.device)
+    _lib.check(lib.rift2_synth_blobs(_ptr(blobs.contiguous()), n, nb, height, width, _ptr(out), _stream()),
+               "rift2_synth_blobs")
+    return out
+
+
+def synth_normals(seed: int, first_image: int, n_images: int, n: int, device="cuda") -> torch.Tensor:
+    """rift2_synth_normals -> (n_images, n) float32 standard normals."""
+    lib = _lib.load(require_gpu=True)
+    out = torch.empty((n_images, n), dtype=torch.float32, device=device)
+    _lib.check(lib.rift2_synth_normals(int(seed) & (2**64 - 1), int(first_image), n_images, n, _ptr(out), _stream()),
+               "rift2_synth_normals")
+    return out

@@ -73,6 +73,63 @@ def blob_field(size: int, seed: int, n_blobs: int = 200, sigma_scale: float = 1.
     return (img - img.min()) / (img.max() - img.min())
 
 
+def blob_params(size: int, seed: int, n_blobs: int = 200, sigma_scale: float = 1.0):
+    """The blob draws of blob_field, in its order, as rift2_synth_blobs rows
+    (cx, cy, sx, sy, cos phi, sin phi, amp, x0, x1, y0, y1); returns the rows
+    and the generator positioned at the white-noise draw."""
+    rng = np.random.default_rng(seed)
+    rows = np.zeros((n_blobs, 11))
+    for i in range(n_blobs):
+        cx, cy = rng.uniform(0, size, 2)
+        sx, sy = rng.uniform(2.0, 20.0, 2) * sigma_scale
+        phi = rng.uniform(0, math.pi)
+        amp = rng.uniform(-1.0, 1.0)
+        ext = int(math.ceil(4.0 * max(sx, sy)))
+        x0, x1 = max(int(cx) - ext, 0), min(int(cx) + ext + 1, size)
+        y0, y1 = max(int(cy) - ext, 0), min(int(cy) + ext + 1, size)
+        rows[i] = (cx, cy, sx, sy, math.cos(phi), math.sin(phi), amp, x0, x1, y0, y1)
+    return rows, rng
+
+
+def image1_device(n_images: int, size: int, seed0: int = 0, noise: str = "device", sigma_scale: float | None = None,
+                  noise_weight: float = 0.5, f_cut: float = 0.2, noise_seed: int | None = None):
+    """Image 1 of the generator for seeds seed0.. on the GPU -> (n, size,
+    size) float64 CUDA tensor.  The blobs are rift2_synth_blobs on the host's
+    own draws (blob_params); the white noise is the host's standard_normal
+    draw ("host": the same image as blob_field up to float32 FFT rounding) or
+    Philox normals on the device ("device", key noise_seed, default seed0:
+    a different but equally distributed noise field, no host work); the
+    band-limit is rift2_apply_bank with a 0/1 mask of radial frequency <
+    f_cut; then blob_field's normalisation."""
+    import torch
+    from . import engine
+    if sigma_scale is None:
+        sigma_scale = 4.0 if size >= 4096 else 1.0
+    rows, hostnoise = [], []
+    for i in range(n_images):
+        r, rng = blob_params(size, seed0 + i, sigma_scale=sigma_scale)
+        rows.append(r)
+        if noise == "host":
+            hostnoise.append(rng.standard_normal((size, size)).astype(np.float32))
+    img = engine.synth_blobs(torch.from_numpy(np.stack(rows)).cuda(), size, size)
+    if noise == "host":
+        white = torch.from_numpy(np.stack(hostnoise)).cuda()
+    else:
+        white = engine.synth_normals(seed0 if noise_seed is None else noise_seed, 0, n_images, size * size)
+        white = white.view(n_images, size, size)
+    f = np.fft.fftfreq(size)
+    mask = torch.from_numpy((np.hypot(f[:, None], f[None, :]) < f_cut).astype(np.float32)[None, None]).cuda()
+    for i in range(n_images):
+        even, _, _ = engine.apply_bank(white[i].contiguous(), mask)
+        nz = even[0, 0].double()
+        nz = nz / torch.clamp(nz.std(unbiased=False), min=1e-12)
+        im = img[i]
+        im = im / torch.clamp(im.std(unbiased=False), min=1e-12)
+        im = im + noise_weight * nz
+        img[i] = (im - im.min()) / (im.max() - im.min())
+    return img
+
+
 def similarity(size: int, theta_deg: float, scale: float, t) -> np.ndarray:
     """2x3 matrix of p' = s R (p - c) + c + t, c the image centre."""
     c = (size - 1) / 2.0
@@ -161,10 +218,12 @@ def make_batch(n_pairs: int, size: int = 1024, seed0: int = 0, dtype=np.float32,
 
 def make_batch_device(n_pairs: int, size: int = 1024, seed0: int = 0, device="cuda", speckle_seed: int | None = None,
                       theta_deg: float | None = None, scale_jitter: float = 0.0, looks: int | None = 4,
-                      sigma_scale: float | None = None, radiometric: bool = True):
+                      sigma_scale: float | None = None, radiometric: bool = True, image1: str = "host"):
     """make_batch with the target side synthesised on the GPU
-    (rift2_synth_targets): image 1 and the per-pair draws (hence the truths)
-    are the host generator's; the warp, inversion, gamma and renormalisation
+    (rift2_synth_targets); image 1 from the host generator (image1="host"),
+    or on the GPU (image1="device": image1_device with Philox white noise;
+    "device_hostnoise": the host's noise draw); the per-pair draws (hence the
+    truths) are the host generator's; the warp, inversion, gamma and renormalisation
     match make_pair to float32 rounding (pow on the device is within 2 ulp);
     the speckle is drawn from Philox4x32-10 (key speckle_seed, default
     seed0; counter word 2 = pair index) instead of numpy's stream.
@@ -173,18 +232,22 @@ def make_batch_device(n_pairs: int, size: int = 1024, seed0: int = 0, device="cu
     from . import engine
     if sigma_scale is None:
         sigma_scale = 4.0 if size >= 4096 else 1.0
-    src = np.empty((n_pairs, size, size))
     params = np.zeros((n_pairs, 8))
     truths = []
+    if image1 == "host":
+        src = np.empty((n_pairs, size, size))
+        for i in range(n_pairs):
+            src[i] = blob_field(size, seed0 + i, sigma_scale=sigma_scale)
     for i in range(n_pairs):
-        src[i] = blob_field(size, seed0 + i, sigma_scale=sigma_scale)
         tr, _ = _pair_draws(size, seed0 + i, theta_deg, scale_jitter, looks)
         params[i, :6] = inverse_map(tr.matrix).ravel()
         params[i, 6] = tr.gamma
         params[i, 7] = (1 if tr.inverted else 0) | (2 if radiometric else 0)
         truths.append(tr)
     out = torch.empty((2 * n_pairs, size, size), dtype=torch.float32, device=device)
-    d_src = torch.from_numpy(src).to(device)
+    d_src = torch.from_numpy(src).to(device) if image1 == "host" else \
+        image1_device(n_pairs, size, seed0, noise="host" if image1 == "device_hostnoise" else "device",
+                      sigma_scale=sigma_scale)
     d_par = torch.from_numpy(params).to(device)
     d_looks = torch.full((n_pairs,), int(looks or 0), dtype=torch.int32, device=device)
     engine.synth_targets(d_src, d_par, d_looks, seed0 if speckle_seed is None else speckle_seed, out[1::2],

@@ -132,3 +132,57 @@ def test_argument_errors(eng):
         eng.synth_targets(src, torch.zeros((2, 7), dtype=torch.float64, device="cuda"), looks, 0, dst)
     with pytest.raises(ParameterError):
         eng.synth_targets(src.float(), torch.zeros((2, 8), dtype=torch.float64, device="cuda"), looks, 0, dst)
+
+
+# ---- image 1 on the device -------------------------------
+def test_blobs_kernel_vs_host_sum():
+    """rift2_synth_blobs adds the host's blob draws in the host's order."""
+    import math
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2303_00319_b200 import engine, synth
+    rows, _ = synth.blob_params(200, seed=7, n_blobs=40)
+    got = engine.synth_blobs(torch.from_numpy(rows[None]).cuda(), 200, 200)[0].cpu().numpy()
+    want = np.zeros((200, 200))
+    for cx, cy, sx, sy, c, s, amp, x0, x1, y0, y1 in rows:
+        x0, x1, y0, y1 = int(x0), int(x1), int(y0), int(y1)
+        if x0 >= x1 or y0 >= y1:
+            continue
+        ys, xs = np.mgrid[y0:y1, x0:x1].astype(np.float64)
+        dx, dy = xs - cx, ys - cy
+        u = c * dx + s * dy
+        v = -s * dx + c * dy
+        want[y0:y1, x0:x1] += amp * np.exp(-0.5 * ((u / sx) ** 2 + (v / sy) ** 2))
+    np.testing.assert_allclose(got, want, rtol=1e-13, atol=1e-15)
+    assert not math.isnan(got.sum())
+
+
+def test_image1_device_equals_host_generator():
+    """With the host's white-noise draw, the device image 1 equals
+    synth.blob_field up to the float32 FFT of the noise band-limit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2303_00319_b200 import synth
+    got = synth.image1_device(2, 256, seed0=3, noise="host").cpu().numpy()
+    for i in range(2):
+        want = synth.blob_field(256, 3 + i)
+        assert np.abs(got[i] - want).max() <= 2e-5
+
+
+def test_device_generated_batch_registers():
+    """A batch generated entirely on the device (image 1 with Philox noise,
+    target by rift2_synth_targets) runs through the pipeline and registers
+    against the generator's truths (no speckle: SURVEY D5)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2303_00319_b200 as r2
+    from paper_2303_00319_b200 import synth
+    imgs, truths = synth.make_batch_device(2, 512, seed0=21, looks=None, image1="device")
+    assert float(imgs.min()) >= 0.0 and float(imgs.max()) <= 1.0
+    pipe = r2.BatchPipeline(2, 512, 512, r2.RiftConfig(scale_mult=1.6, sigma_on_f=0.75, max_keypoints=2000))
+    pipe.images.copy_(imgs)
+    pipe.step()
+    torch.cuda.synchronize()
+    ev = r2.evaluate_batch(pipe, truths)
+    torch.cuda.synchronize()
+    assert int(ev["n_correct"].min()) > 50 and bool(ev["success"].all())
