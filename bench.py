@@ -320,12 +320,15 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def tensor_peak():
-    """Dense fp16/bf16 tensor peak (the matching GEMM runs kind::f16)."""
+def tensor_peak(sustained: bool = False):
+    """Dense fp16/bf16 tensor peak (the matching GEMM runs kind::f16): the
+    burst figure for a launch timed alone, the sustained one for back-to-back
+    launches."""
+    key = "bf16_tflops_sustained" if sustained else "bf16_tflops"
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+        return float(p[key]), f"measured (MEASURED_PEAKS.json {key})"
     except (OSError, KeyError, ValueError):
         return 2250.0, "nominal dense bf16 (fallback)"
 
@@ -359,6 +362,46 @@ def traffic():
         return float(p["filter_bank"]["dram_bytes_per_pass"]), os.path.relpath(files[-1], ROOT)
     except (OSError, KeyError, ValueError):
         return None, None
+
+
+def graph_ms(fn, reps: int, gap_s: float = 0.0) -> float:
+    """Device time per call of `fn` (a sequence of our launches), captured
+    once in a CUDA graph and replayed `reps` times between two CUDA events:
+    the host-side launch preparation (tensor-map encoding, ctypes) stays out
+    of the timed interval, as it does in the pipeline's own graphs.  With
+    gap_s > 0 every replay is timed on its own after an idle gap (a kernel
+    timed alone, at burst clocks; back to back, the tensor-core GEMM runs at
+    the sustained, power-capped clock); returns the median."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    if gap_s > 0:
+        ts = []
+        for _ in range(reps):
+            time.sleep(gap_s)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 
 def ring_vs_rift2(pipe, reps: int = 5):
@@ -517,27 +560,15 @@ def run_ours(args, rank, world, local_rank):
     from paper_2303_00319_b200 import engine
     engine.match(pipe.d, pipe.dim, pipe.rb, pipe.tb, pipe.K, ws_key="bench_match")   # allocates its workspace
     torch.cuda.synchronize()
-    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    m0.record()
-    for _ in range(K):                      # back to back (see the GEMM timing below)
-        engine.match(pipe.d, pipe.dim, pipe.rb, pipe.tb, pipe.K, ws_key="bench_match")
-    m1.record()
-    torch.cuda.synchronize()
-    match_ms = m0.elapsed_time(m1) / K
+    match_ms = graph_ms(lambda: engine.match(pipe.d, pipe.dim, pipe.rb, pipe.tb, pipe.K, ws_key="bench_match",
+                                             out=pipe.m), K)
     # the tensor-core GEMM kernel alone (rift2_match_partial launches exactly
     # k_match_gemm, with the same single column split the batch uses)
     parts = engine.match_partial(pipe.d, pipe.dim, pipe.rb, pipe.tb)
     torch.cuda.synchronize()
-    # back to back between two events: the host-side launch preparation
-    # (tensor-map encoding) overlaps the previous launch instead of leaving
-    # the device idle inside the timed interval
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    g0.record()
-    for _ in range(K):
-        engine.match_partial(pipe.d, pipe.dim, pipe.rb, pipe.tb, out=parts)
-    g1.record()
-    torch.cuda.synchronize()
-    gemm_ms = g0.elapsed_time(g1) / K
+    gemm_ms = graph_ms(lambda: engine.match_partial(pipe.d, pipe.dim, pipe.rb, pipe.tb, out=parts), K)
+    gemm_burst_ms = graph_ms(lambda: engine.match_partial(pipe.d, pipe.dim, pipe.rb, pipe.tb, out=parts), K,
+                             gap_s=0.02)
     dcnt = pipe.d["count"].cpu().numpy().astype(np.int64)
     match_flops = float(sum(2 * dcnt[2 * q] * dcnt[2 * q + 1] * pipe.dim for q in range(args.pairs)))
 
@@ -611,10 +642,17 @@ def run_ours(args, rank, world, local_rank):
                                "flops_per_launch": match_flops, "launch_ms": match_ms, "peak_source": tpk_src},
             "roofline_gemm": {"bound": "tensor", "kernel": "k_match_gemm (tcgen05 kind::f16, TMEM accumulators, "
                                                             "TMA operands, fused exact argmax epilogue)",
-                              "achieved": match_flops / (gemm_ms / 1e3) / 1e12, "peak": tpk, "unit": "TFLOP/s",
-                              "frac": match_flops / (gemm_ms / 1e3) / 1e12 / tpk, "flops_per_launch": match_flops,
-                              "launch_ms": gemm_ms, "peak_source": tpk_src,
-                              "note": "algorithmic 2*N_ref*N_tgt*216 flops; the kernel multiplies K=224 (zero padded)"},
+                              "achieved": match_flops / (gemm_burst_ms / 1e3) / 1e12, "peak": tpk, "unit": "TFLOP/s",
+                              "frac": match_flops / (gemm_burst_ms / 1e3) / 1e12 / tpk,
+                              "flops_per_launch": match_flops, "launch_ms": gemm_burst_ms, "peak_source": tpk_src,
+                              "sustained": {"launch_ms": gemm_ms,
+                                            "achieved": match_flops / (gemm_ms / 1e3) / 1e12,
+                                            "peak": tensor_peak(sustained=True)[0],
+                                            "frac": match_flops / (gemm_ms / 1e3) / 1e12 / tensor_peak(sustained=True)[0],
+                                            "note": "K launches back to back: power-capped clocks, against the "
+                                                    "sustained matmul peak"},
+                              "note": "one launch after an idle gap (burst clocks), median of K; algorithmic "
+                                      "2*N_ref*N_tgt*216 flops, the kernel multiplies K=224 (zero padded)"},
             "clocks": clocks,
             "single_pair_api": api,
             "other_configs": others,

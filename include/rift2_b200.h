@@ -67,14 +67,19 @@ const char* rift2_last_error(void);
  *   mim          [batch][height][width] uint8 out, 1-based (IndexMap.indices)
  *   a_o, pc_o    [batch][n_orient][height][width] float32 out, may be NULL
  *   a_max        [batch][height][width] float32 out, may be NULL
+ *   moment_range [batch][2][2] uint64 out, may be NULL: per image the (min,
+ *                max) of moment_min, then of moment_max, as order-preserving
+ *                keys of the float64 values (bit pattern | 2^63), reduced in
+ *                the PC pass; rift2_detect_* reads them instead of
+ *                re-reading the maps for the normalisation
  * height, width >= 16 with prime factors in {2, 3, 5}; n_scales <= 8,
  * n_orient <= 16. */
 int32_t rift2_fields_workspace_size(int32_t batch, int32_t height, int32_t width,
                                     const rift2_bank_params* params, size_t* bytes);
 int32_t rift2_fields(const float* images, int32_t batch, int32_t height, int32_t width,
                      const rift2_bank_params* params, float* moment_max, float* moment_min,
-                     uint8_t* mim, float* a_o, float* pc_o, float* a_max, void* workspace,
-                     size_t workspace_bytes, void* stream);
+                     uint8_t* mim, float* a_o, float* pc_o, float* a_max, uint64_t* moment_range,
+                     void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- stage 2: FAST keypoints on both moment maps -------------------------
  * Replaces ref: pkg/src/rift2/detector.py:140-155 (detect_keypoints) for a
@@ -88,6 +93,8 @@ int32_t rift2_fields(const float* images, int32_t batch, int32_t height, int32_t
  *   kp_x, kp_y   [batch][max_points] int32 out
  *   kp_response  [batch][max_points] float64 out
  *   kp_kind      [batch][max_points] uint8 out (0 corner, 1 edge)
+ *   moment_range rift2_fields' per-image map extrema, or NULL (then the
+ *                detector reduces the maps itself); two-map mode only
  *   kp_count     [batch] int32 out
  * Keypoints are ordered by (-response, y, x), corner before edge on ties. */
 int32_t rift2_detect_workspace_size(int32_t batch, int32_t height, int32_t width, int32_t max_points,
@@ -95,11 +102,13 @@ int32_t rift2_detect_workspace_size(int32_t batch, int32_t height, int32_t width
 int32_t rift2_detect_f32(const float* min_maps, const float* max_maps, int32_t batch, int32_t height,
                          int32_t width, double threshold, int32_t max_points, int32_t border_margin, int32_t single_map,
                          int32_t* kp_x, int32_t* kp_y, double* kp_response, uint8_t* kp_kind,
-                         int32_t* kp_count, void* workspace, size_t workspace_bytes, void* stream);
+                         int32_t* kp_count, const uint64_t* moment_range, void* workspace, size_t workspace_bytes,
+                         void* stream);
 int32_t rift2_detect_f64(const double* min_maps, const double* max_maps, int32_t batch, int32_t height,
                          int32_t width, double threshold, int32_t max_points, int32_t border_margin, int32_t single_map,
                          int32_t* kp_x, int32_t* kp_y, double* kp_response, uint8_t* kp_kind,
-                         int32_t* kp_count, void* workspace, size_t workspace_bytes, void* stream);
+                         int32_t* kp_count, const uint64_t* moment_range, void* workspace, size_t workspace_bytes,
+                         void* stream);
 
 /* ---- stage 3: RIFT2 dominant-index descriptors ---------------------------
  * Replaces ref: pkg/src/rift2/descriptor.py:179-216 (describe_rift2),

@@ -37,12 +37,12 @@ _SIGNATURES = {
     "rift2_fields_workspace_size": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(BankParamsC),
                                              ctypes.POINTER(_c_sz)]),
     "rift2_fields": (_c_int, [_c_p, _c_int, _c_int, _c_int, ctypes.POINTER(BankParamsC), _c_p, _c_p, _c_p,
-                              _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+                              _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "rift2_detect_workspace_size": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
     "rift2_detect_f32": (_c_int, [_c_p, _c_p, _c_int, _c_int, _c_int, _c_d, _c_int, _c_int, _c_int, _c_p,
-                                  _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+                                  _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "rift2_detect_f64": (_c_int, [_c_p, _c_p, _c_int, _c_int, _c_int, _c_d, _c_int, _c_int, _c_int, _c_p,
-                                  _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+                                  _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "rift2_describe_workspace_size": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
     "rift2_describe": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p, _c_int, _c_int, _c_int,
                                 _c_d, _c_int, _c_int, _c_p, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p,

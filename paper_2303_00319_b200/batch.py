@@ -48,7 +48,8 @@ class BatchPipeline:
         self.images = torch.zeros((B, H, W), dtype=torch.float32, device=d)
         self.f = dict(mmax=torch.empty((B, H, W), dtype=torch.float32, device=d),
                       mmin=torch.empty((B, H, W), dtype=torch.float32, device=d),
-                      mim=torch.empty((B, H, W), dtype=torch.uint8, device=d))
+                      mim=torch.empty((B, H, W), dtype=torch.uint8, device=d),
+                      range=torch.zeros((B, 2, 2), dtype=torch.int64, device=d))
         self.k = dict(x=torch.zeros((B, K), dtype=torch.int32, device=d),
                       y=torch.zeros((B, K), dtype=torch.int32, device=d),
                       response=torch.zeros((B, K), dtype=torch.float64, device=d),
@@ -87,7 +88,7 @@ class BatchPipeline:
         f = self.f if f is None else f
         c = self.cfg
         engine.detect(f["mmin"], f["mmax"], c.fast_threshold, self.K, c.patch_size // 2, ws_key=ws + "detect",
-                      out=self.k)
+                      out=self.k, moment_range=f["range"])
         engine.describe(f["mim"], self.k["x"], self.k["y"], self.k["count"], c.n_orient, c.patch_size, c.grid,
                         c.dominant_ratio, c.rotate_patch, self.desc_mode, capacity=self.cap, ws_key=ws + "describe",
                         out=self.d)
@@ -97,7 +98,8 @@ class BatchPipeline:
         self.run_fields()
         self.run_features()
 
-    # our kernels per step: fields 9 + detect 10 + describe 1 + match 7
+    # our kernels per step: fields 10 (with the moment-range init) + detect 9
+    # (no k_minmax: the PC pass reduced the maps) + describe 1 + match 7
     KERNELS_PER_STEP = 27
 
     # ---- graphs ------------------------------------------------------------

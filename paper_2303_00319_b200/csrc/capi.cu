@@ -122,14 +122,16 @@ template <class T>
 static int32_t detect_impl(const T* mins, const T* maxs, int32_t batch, int32_t height, int32_t width, double threshold,
                            int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
                            int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
-                           void* workspace, size_t workspace_bytes, void* stream) {
+                           const uint64_t* moment_range, void* workspace, size_t workspace_bytes, void* stream) {
   if (!(threshold > 0)) return fail(RIFT2_BAD_ARGUMENT, "FAST threshold must be positive");
   if (batch < 1 || height < 1 || width < 1 || max_points < 0 || border_margin < 0)
     return fail(RIFT2_BAD_ARGUMENT, "bad detect dimensions");
   if (!mins || (!single_map && !maxs) || !kp_count || !workspace || (max_points > 0 && (!kp_x || !kp_y || !kp_response || !kp_kind)))
     return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  if (moment_range && single_map) return fail(RIFT2_BAD_ARGUMENT, "moment_range applies to the two-map detector");
   r2::DetectArgs a{batch, height, width, threshold, max_points, border_margin, single_map != 0,
-                   kp_x, kp_y, kp_response, kp_kind, kp_count};
+                   kp_x, kp_y, kp_response, kp_kind, kp_count,
+                   reinterpret_cast<const unsigned long long*>(moment_range)};
   int32_t rc = r2::detect_run(mins, maxs, a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
   return map_internal(rc, "rift2_detect");
 }
@@ -165,15 +167,16 @@ int32_t rift2_fields_workspace_size(int32_t batch, int32_t height, int32_t width
 
 int32_t rift2_fields(const float* images, int32_t batch, int32_t height, int32_t width,
                      const rift2_bank_params* params, float* moment_max, float* moment_min, uint8_t* mim,
-                     float* a_o, float* pc_o, float* a_max, void* workspace, size_t workspace_bytes,
-                     void* stream) {
+                     float* a_o, float* pc_o, float* a_max, uint64_t* moment_range, void* workspace,
+                     size_t workspace_bytes, void* stream) {
   r2::BankConsts k;
   int32_t rc = bank_consts(params, k);
   if (rc) return rc;
   if ((rc = check_fields_dims(batch, height, width))) return rc;
   if (!images || !moment_max || !moment_min || !mim || !workspace)
     return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
-  r2::FieldsOutputs out{moment_max, moment_min, mim, a_o, pc_o, a_max};
+  r2::FieldsOutputs out{moment_max, moment_min, mim, a_o, pc_o, a_max,
+                        reinterpret_cast<unsigned long long*>(moment_range)};
   rc = r2::fields_run(images, batch, height, width, k, out, workspace, workspace_bytes,
                       static_cast<cudaStream_t>(stream));
   return map_internal(rc, "rift2_fields");
@@ -192,18 +195,18 @@ int32_t rift2_detect_f32(const float* min_maps, const float* max_maps, int32_t b
                          int32_t width, double threshold,
                          int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
                          int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
-                         void* workspace, size_t workspace_bytes, void* stream) {
+                         const uint64_t* moment_range, void* workspace, size_t workspace_bytes, void* stream) {
   return detect_impl(min_maps, max_maps, batch, height, width, threshold, max_points, border_margin, single_map, kp_x, kp_y,
-                     kp_response, kp_kind, kp_count, workspace, workspace_bytes, stream);
+                     kp_response, kp_kind, kp_count, moment_range, workspace, workspace_bytes, stream);
 }
 
 int32_t rift2_detect_f64(const double* min_maps, const double* max_maps, int32_t batch, int32_t height,
                          int32_t width, double threshold,
                          int32_t max_points, int32_t border_margin, int32_t single_map, int32_t* kp_x,
                          int32_t* kp_y, double* kp_response, uint8_t* kp_kind, int32_t* kp_count,
-                         void* workspace, size_t workspace_bytes, void* stream) {
+                         const uint64_t* moment_range, void* workspace, size_t workspace_bytes, void* stream) {
   return detect_impl(min_maps, max_maps, batch, height, width, threshold, max_points, border_margin, single_map, kp_x, kp_y,
-                     kp_response, kp_kind, kp_count, workspace, workspace_bytes, stream);
+                     kp_response, kp_kind, kp_count, moment_range, workspace, workspace_bytes, stream);
 }
 
 // ---------------------------------------------------------------- describe

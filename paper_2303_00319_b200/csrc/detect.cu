@@ -583,7 +583,10 @@ int detect_impl(const T* mins, const T* maxs, const DetectArgs& a, void* ws, siz
   }
   k_init<<<(planes + 255) / 256, 256, 0, st>>>(mm, cnt, planes);
   const size_t n = (size_t)a.H * a.W;
-  {
+  if (a.range) {
+    // the filter bank already reduced the maps (same key format, same plane order)
+    cudaMemcpyAsync(mm, a.range, (size_t)planes * 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st);
+  } else {
     dim3 grid((unsigned)min((size_t)64, (n + 1023) / 1024), planes);
     k_minmax<T><<<grid, 256, 0, st>>>(mins, maxs, nm, n, mm);
   }

@@ -16,6 +16,7 @@ struct DetectArgs {
   double* kp_resp;
   uint8_t* kp_kind;
   int32_t* kp_count;
+  const unsigned long long* range;   // nullable: per-image (min, max) keys of both maps from rift2_fields
 };
 
 size_t detect_workspace_bytes(int B, int H, int W, int max_points);

@@ -840,7 +840,57 @@ struct PcOut {
   float* a_o;    // nullable [B][O][H][W]
   float* pc;     // nullable [B][O][H][W]
   float* amax;   // nullable [B][H][W]
+  unsigned long long* range;   // nullable [B][2 maps: min, max][lo, hi] ordered float64 keys
 };
+
+// Per-image min / max of the two moment maps, folded into the PC pass so
+// the detector's normalisation (ref: detector.py:80-84) needs no re-read of
+// the maps: per-thread running extrema, a CTA reduction, four atomics per
+// CTA on order-preserving keys of the float64 value (the detector's own key
+// format; the maps are >= 0).
+R2_DEV unsigned long long range_key(float v) {
+  return (unsigned long long)__double_as_longlong((double)v) | 0x8000000000000000ull;
+}
+struct RangeAcc {
+  float lo0 = INFINITY, hi0 = -INFINITY, lo1 = INFINITY, hi1 = -INFINITY;   // map 0 = moment_min, 1 = moment_max
+  R2_DEV void add(float vmin, float vmax) {
+    lo0 = fminf(lo0, vmin); hi0 = fmaxf(hi0, vmin);
+    lo1 = fminf(lo1, vmax); hi1 = fmaxf(hi1, vmax);
+  }
+  // two pixels per call: three-input min / max (FMNMX3)
+  R2_DEV void add2(float vmin0, float vmax0, float vmin1, float vmax1) {
+    lo0 = fminf(fminf(lo0, vmin0), vmin1); hi0 = fmaxf(fmaxf(hi0, vmin0), vmin1);
+    lo1 = fminf(fminf(lo1, vmax0), vmax1); hi1 = fmaxf(fmaxf(hi1, vmax0), vmax1);
+  }
+  // all threads of the CTA; range = this image's four keys
+  R2_DEV void flush(unsigned long long* range) {
+    __shared__ float s_r[4][32];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      lo0 = fminf(lo0, __shfl_xor_sync(0xffffffffu, lo0, d));
+      hi0 = fmaxf(hi0, __shfl_xor_sync(0xffffffffu, hi0, d));
+      lo1 = fminf(lo1, __shfl_xor_sync(0xffffffffu, lo1, d));
+      hi1 = fmaxf(hi1, __shfl_xor_sync(0xffffffffu, hi1, d));
+    }
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) { s_r[0][w] = lo0; s_r[1][w] = hi0; s_r[2][w] = lo1; s_r[3][w] = hi1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < nw; ++q) {
+        lo0 = fminf(lo0, s_r[0][q]); hi0 = fmaxf(hi0, s_r[1][q]);
+        lo1 = fminf(lo1, s_r[2][q]); hi1 = fmaxf(hi1, s_r[3][q]);
+      }
+      if (lo0 <= hi0) { atomicMin(&range[0], range_key(lo0)); atomicMax(&range[1], range_key(hi0)); }
+      if (lo1 <= hi1) { atomicMin(&range[2], range_key(lo1)); atomicMax(&range[3], range_key(hi1)); }
+    }
+  }
+};
+
+__global__ void k_range_init(unsigned long long* range, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) range[i] = (i & 1) ? 0ull : ~0ull;
+}
 
 template <int G>
 struct PcShape {
@@ -956,6 +1006,7 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
   const float2* Rb = R0 + (size_t)b * O * H * W;
   const float inv_sm1 = c.inv_sm1, gain = c.spread_gain, cut = c.spread_cutoff;
 
+  RangeAcc racc;
   for (int rbase = 0; rbase < 2; rbase += rr) {
     const int npix = rr * W;
     float acc_a[PIX], acc_b[PIX], acc_c[PIX], best[PIX];
@@ -1137,12 +1188,15 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
       const float a = acc_a[i], bq = 2.f * acc_b[i], cq = acc_c[i];
       const float root = sqrtf(bq * bq + (a - cq) * (a - cq));
       const size_t po = ((size_t)b * H + y) * W + x;
-      out.mmax[po] = 0.5f * (cq + a + root);
-      out.mmin[po] = fmaxf(0.5f * (cq + a - root), 0.f);
+      const float vmax = 0.5f * (cq + a + root), vmin = fmaxf(0.5f * (cq + a - root), 0.f);
+      out.mmax[po] = vmax;
+      out.mmin[po] = vmin;
       out.mim[po] = (uint8_t)bidx[i];
       if (out.amax) out.amax[po] = best[i];
+      if (out.range) racc.add(vmin, vmax);
     }
   }
+  if (out.range) racc.flush(out.range + 4 * (size_t)b);
 }
 
 
@@ -1286,6 +1340,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
     }
     __syncthreads();                               // the next stage's TMA rewrites the buffers
   }
+  RangeAcc racc;
+  float vmin[PIX], vmax[PIX];
 #pragma unroll
   for (int i = 0; i < PIX; ++i) {
     const int p = threadIdx.x + kThreads * i;
@@ -1294,10 +1350,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
     const float a = acc_a[i], bq = 2.f * acc_b[i], cq = acc_c[i];
     const float root = sqrtf(bq * bq + (a - cq) * (a - cq));
     const size_t po = ((size_t)b * H + y) * W + x;
-    out.mmax[po] = 0.5f * (cq + a + root);
-    out.mmin[po] = fmaxf(0.5f * (cq + a - root), 0.f);
+    vmax[i] = 0.5f * (cq + a + root);
+    vmin[i] = fmaxf(0.5f * (cq + a - root), 0.f);
+    out.mmax[po] = vmax[i];
+    out.mmin[po] = vmin[i];
     out.mim[po] = (uint8_t)bidx[i];
     if (out.amax) out.amax[po] = best[i];
+  }
+  if (out.range) {                                 // CTA-uniform
+#pragma unroll
+    for (int i = 0; i < PIX; i += 2) racc.add2(vmin[i], vmax[i], vmin[i + 1], vmax[i + 1]);
+    racc.flush(out.range + 4 * (size_t)b);
   }
 }
 
@@ -1626,7 +1689,8 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   }
   launch_med_select(cand, cnt, info, reinterpret_cast<unsigned*>(w + p.off_mh), thr, B * c.O, n, c.thr_factor, st);
   if (cudaPeekAtLastError() != cudaSuccess) return 3;
-  PcOut po{o.mmax, o.mmin, o.mim, o.a_o, o.pc, o.amax};
+  PcOut po{o.mmax, o.mmin, o.mim, o.a_o, o.pc, o.amax, o.range};
+  if (o.range) k_range_init<<<(4 * B + 127) / 128, 128, 0, st>>>(o.range, 4 * B);
   R2_DISPATCH_G(p.gw, launch_pc, Q, R0, thr, po, c, st);
   if (e != cudaSuccess) return 3;
   return 0;

@@ -24,6 +24,7 @@ struct FieldsOutputs {
   float* a_o;   // nullable
   float* pc;    // nullable
   float* amax;  // nullable
+  unsigned long long* range;   // nullable [B][2][2]: per-image (lo, hi) keys of moment_min, moment_max
 };
 
 // W_n^j = exp(-2 pi i j / n), j < n, cached per (device, n); nullptr on failure.

@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "match.h"
@@ -816,6 +817,10 @@ int gemm_launch(const MatchArgs& a, Part* part, int splits, cudaStream_t st) {
   if (cr != CUDA_SUCCESS) return -3;
 
   const int m_tiles = (a.cap + BM - 1) / BM;
+  if (splits <= 0) {
+    static const int forced = [] { const char* e = std::getenv("R2_GEMM_SPLITS"); return e ? std::atoi(e) : 0; }();
+    if (forced > 0) splits = forced > kMaxSplits ? kMaxSplits : forced;   // experiment switch
+  }
   if (splits <= 0) {
     // split the reference range only as far as needed to put one CTA on every SM:
     // a CTA that sees few column tiles keeps a weak running best and pays the

@@ -61,7 +61,9 @@ def bank_c(bank) -> _lib.BankParamsC:
 
 
 def fields(images: torch.Tensor, bank, extras: bool = False, ws_key: str = "fields", out=None):
-    """images (B, H, W) float32 CUDA -> dict(mmax, mmin, mim[, a_o, pc, amax])."""
+    """images (B, H, W) float32 CUDA -> dict(mmax, mmin, mim[, a_o, pc, amax]);
+    an `out` dict may also carry "range" ((B, 2, 2) int64: the moment maps'
+    per-image extrema keys for detect())."""
     lib = _lib.load(require_gpu=True)
     if images.dim() != 3 or images.dtype != torch.float32 or not images.is_cuda:
         raise ParameterError("images must be a (B, H, W) float32 CUDA tensor")
@@ -83,15 +85,17 @@ def fields(images: torch.Tensor, bank, extras: bool = False, ws_key: str = "fiel
             out["amax"] = torch.empty((B, H, W), dtype=torch.float32, device=dev)
     rc = lib.rift2_fields(_ptr(images), B, H, W, ctypes.byref(p), _ptr(out["mmax"]), _ptr(out["mmin"]),
                           _ptr(out["mim"]), _ptr(out.get("a_o")), _ptr(out.get("pc")), _ptr(out.get("amax")),
-                          _ptr(ws), ws.numel(), _stream())
+                          _ptr(out.get("range")), _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "rift2_fields")
     return out
 
 
 def detect(mins: torch.Tensor, maxs: torch.Tensor | None, threshold: float, max_points: int, margin: int,
-           single_map: bool = False, ws_key: str = "detect", out=None):
+           single_map: bool = False, ws_key: str = "detect", out=None, moment_range: torch.Tensor | None = None):
     """mins / maxs (B, H, W) moment_min / moment_max (maxs unused with
-    single_map), float32 or float64 CUDA -> dict(x, y, response, kind, count)."""
+    single_map), float32 or float64 CUDA -> dict(x, y, response, kind, count).
+    moment_range: the (B, 2, 2) int64 extrema keys fields() wrote (its
+    "range" output), so the maps are not re-read for the normalisation."""
     lib = _lib.load(require_gpu=True)
     mins = mins.contiguous()
     maxs = mins if (single_map or maxs is None) else maxs.contiguous()
@@ -116,7 +120,7 @@ def detect(mins: torch.Tensor, maxs: torch.Tensor | None, threshold: float, max_
         raise ParameterError("maps must be float32 or float64")
     rc = fn(_ptr(mins), _ptr(maxs), B, H, W, float(threshold), K, int(margin), 1 if single_map else 0,
             _ptr(out["x"]), _ptr(out["y"]), _ptr(out["response"]), _ptr(out["kind"]), _ptr(out["count"]),
-            _ptr(ws), ws.numel(), _stream())
+            _ptr(moment_range), _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "rift2_detect")
     return out
 
