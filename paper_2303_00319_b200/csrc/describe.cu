@@ -41,8 +41,15 @@ namespace {
 
 constexpr int kT = 160;   // 5 warps: 144 counting threads for the 6x6 grid of 16-px cells
 
+// offsets are stored as uint16 dy*stride + dx + kOffBias: 8 bytes per four
+// samples, so the four rotated angles' tables (72 KB at 96^2) mostly stay in L1
+constexpr int kOffBias = 32768;
+#ifndef R2_DESC_CARVE
+#define R2_DESC_CARVE 100
+#endif
+
 struct GatherTables {
-  const int* soff;       // [O][P*P] dy*stride + dx into the staged region; angle 0 unused
+  const uint16_t* soff;  // [O][P*P] dy*stride + dx + kOffBias into the staged region; angle 0 unused
   const int4* bbox;      // [O] (dx_min, dx_max, dy_min, dy_max)
   int radius;            // max |offset| over all angles (and the axis crop)
   int stride;            // staged row length in bytes (multiple of 16)
@@ -95,14 +102,18 @@ GatherTables gather_tables(int P, int O) {
   const int stride = ((2 * radius + 1 + 15 + 4 + 15) / 16) * 16;
   GatherTables t{nullptr, nullptr, radius, stride, {}};
   for (int a = 0; a < O && a < 8; ++a) t.hbbox[a] = bbox[a];
-  // int32 offsets: a thread's four samples of a row are one 16-byte load
-  std::vector<int> soff(off.size());
-  for (size_t i = 0; i < off.size(); ++i) soff[i] = off[i].y * stride + off[i].x;
-  int* d_off = nullptr;
+  // biased 16-bit offsets: a thread's four samples of a row are one 8-byte load
+  std::vector<uint16_t> soff(off.size());
+  for (size_t i = 0; i < off.size(); ++i) {
+    const int v = off[i].y * stride + off[i].x + kOffBias;
+    if (v < 0 || v > 65535) return t;            // (a patch far beyond the supported sizes)
+    soff[i] = (uint16_t)v;
+  }
+  uint16_t* d_off = nullptr;
   int4* d_bb = nullptr;
-  if (cudaMalloc(&d_off, soff.size() * sizeof(int)) != cudaSuccess) return t;
+  if (cudaMalloc(&d_off, soff.size() * sizeof(uint16_t)) != cudaSuccess) return t;
   if (cudaMalloc(&d_bb, bbox.size() * sizeof(int4)) != cudaSuccess) return t;
-  cudaMemcpy(d_off, soff.data(), soff.size() * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_off, soff.data(), soff.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
   cudaMemcpy(d_bb, bbox.data(), bbox.size() * sizeof(int4), cudaMemcpyHostToDevice);
   t.soff = d_off;
   t.bbox = d_bb;
@@ -128,6 +139,10 @@ R2_DEV void widen(uint32_t acc, uint32_t& e, uint32_t& o) {
 
 // reduce the 4 threads of a cell, write its O counts and add their squares
 // to the descriptor's squared norm (recode only permutes bins)
+// The patch histogram and the squared norm are reduced per warp (the
+// histogram as three words of two 16-bit counts: <= 9,216 per value) and
+// added to shared memory by one lane, instead of per-cell atomics on the same
+// few addresses.  Every lane of the warp calls this.
 template <int OT>
 R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int O_rt, int* sq,
                         unsigned* hist = nullptr) {
@@ -136,17 +151,34 @@ R2_DEV void reduce_cell(uint32_t e, uint32_t o, bool writer, unsigned* out, int 
   o += __shfl_xor_sync(0xffffffffu, o, 1);
   e += __shfl_xor_sync(0xffffffffu, e, 2);
   o += __shfl_xor_sync(0xffffffffu, o, 2);
+  int q = 0;
+  uint32_t h01 = 0, h23 = 0, h45 = 0;
   if (writer) {
-    int q = 0;
 #pragma unroll
     for (int v = 0; v < (OT ? OT : 8); ++v) {
       if (!OT && v >= O) break;
       const unsigned n = (((v & 1) ? o : e) >> (10 * (v >> 1))) & 1023u;
       out[v] = n;
       q += (int)(n * n);
-      if (hist && n) atomicAdd(&hist[v], n);      // the patch histogram (axis patch only)
     }
-    atomicAdd(sq, q);
+    // 16-bit packed histogram words: value v in word v / 2, half v % 2
+    h01 = (e & 1023u) | (o & 1023u) << 16;
+    h23 = ((e >> 10) & 1023u) | ((o >> 10) & 1023u) << 16;
+    h45 = ((e >> 20) & 1023u) | ((o >> 20) & 1023u) << 16;
+  }
+  q = __reduce_add_sync(0xffffffffu, q);
+  if (hist) {
+    h01 = __reduce_add_sync(0xffffffffu, h01);
+    h23 = __reduce_add_sync(0xffffffffu, h23);
+    h45 = __reduce_add_sync(0xffffffffu, h45);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (q) atomicAdd(sq, q);
+    if (hist) {
+      if (h01) atomicAdd(&hist[0], h01);
+      if (h23) atomicAdd(&hist[1], h23);
+      if (h45) atomicAdd(&hist[2], h45);
+    }
   }
 }
 
@@ -188,7 +220,7 @@ R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsign
 
 // rotated patch of angle table t: sample (i, j) at ctr + t[i*P + j]
 template <int CS, int OT, int GT>
-R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const int* __restrict__ t, unsigned* cnt,
+R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const uint16_t* __restrict__ t, unsigned* cnt,
                           int* sq) {
   const int tpc = CS / 4;
   const int g = GT ? GT : c.g, O = OT ? OT : c.O, P = GT ? GT * CS : c.P;
@@ -198,12 +230,13 @@ R2_DEV void count_rotated(const DescConst& c, const uint8_t* ctr, const int* __r
   const int cr = cell / g, cc = cell % g;
   uint32_t e = 0, o = 0;
   if (on) {
-    const int4* tr = reinterpret_cast<const int4*>(t + (cr * CS) * P + cc * CS + 4 * sub);
+    const uint2* tr = reinterpret_cast<const uint2*>(t + (cr * CS) * P + cc * CS + 4 * sub);
+    const uint8_t* cb = ctr - kOffBias;
     uint32_t acc = 0;
 #pragma unroll
     for (int r = 0; r < CS; ++r) {
-      const int4 a = __ldg(tr + r * (P / 4));
-      acc += one_hot(ctr[a.x]) + one_hot(ctr[a.y]) + one_hot(ctr[a.z]) + one_hot(ctr[a.w]);
+      const uint2 a = __ldg(tr + r * (P / 4));
+      acc += one_hot(cb[a.x & 0xffffu]) + one_hot(cb[a.x >> 16]) + one_hot(cb[a.y & 0xffffu]) + one_hot(cb[a.y >> 16]);
       if (r % 7 == 6 || r == CS - 1) { widen(acc, e, o); acc = 0; }
     }
   }
@@ -374,7 +407,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   {
     unsigned hs[8];
 #pragma unroll
-    for (int v = 0; v < 8; ++v) hs[v] = v < O ? s_hist[v] : 0u;
+    for (int v = 0; v < 8; ++v) hs[v] = v < O ? (s_hist[v >> 1] >> (16 * (v & 1))) & 0xffffu : 0u;
     int skip = 0;
     if (mode == 0) { pick[np++] = 1; }
     else if (mode == 1) {
@@ -555,6 +588,8 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
   // the BASELINE grid (6 orientations, 6 x 6 cells) with constant indexing
   auto kern = (c.O == 6 && c.g == 6) ? k_desc_main<16, 6, 6> : k_desc_main<16, 0, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // shared-memory carveout (percent): what is not carved out stays L1 for the offset tables
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, R2_DESC_CARVE);
   kern<<<grid, kT, smem, st>>>(tmap, mim, a, c, tab, chain, ticket);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
 }

@@ -47,7 +47,9 @@ constexpr int A_BYTES = KBOX * A_BOX;          // 64 KB, resident
 constexpr int NSTAGE = 4;                      // B ring: K boxes in flight
 constexpr int NACC = 2;                        // TMEM accumulator buffers
 constexpr int TMEM_COLS = NACC * BN;           // 512: all of TMEM
-constexpr int NEPI = 16;                       // epilogue warps: 4 lane quarters x 4 column groups
+// 8 epilogue warps (4 lane quarters x 2 column groups): 320 threads leave
+// room for two chunks in flight per warp (~130 registers)
+constexpr int NEPI = 8;
 constexpr int CPW = BN / 32 / (NEPI / 4);      // 32-column chunks per epilogue warp per tile
 constexpr int GEMM_THREADS = 64 + NEPI * 32;  // producer, MMA, epilogue warps
 constexpr int BAR_OFF = A_BYTES + NSTAGE * B_BOX;
@@ -107,6 +109,30 @@ R2_DEV void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumula
 R2_DEV void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                :: "r"(smem_u32(bar)) : "memory");
+}
+
+// TMEM load issue / completion, split so a chunk's load overlaps the
+// previous chunk's processing: the wait names the destination registers as
+// read-write, so nothing reads them before it
+R2_DEV void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+R2_DEV void tmem_ld_wait(uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+        "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+        "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+        "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :: "memory");
 }
 
 R2_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -282,10 +308,12 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
           if (kb == 0) R2_TR(3, i);
           tc_fence_after();
           const uint32_t b_base = smem_u32(sB + s * B_BOX);
+#ifndef R2_EXP_NOMMA   // timing experiment (DESIGN 4): operand loads only
 #pragma unroll
           for (int kk = 0; kk < (kb == KBOX - 1 ? 2 : 4); ++kk)
             mma_f16(d, smem_desc(a_base + kb * A_BOX + kk * 32), smem_desc(b_base + kk * 32),
                     (kb | kk) ? 1u : 0u);
+#endif
           mma_commit(&empty[s]);
         }
         mma_commit(&t_full[acc]);
@@ -329,68 +357,84 @@ k_match_gemm(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ 
       const int c = chunk_c0(0) + lane;
       q_nxt = c < n_r ? __ldg(&sq[c]) : 0;          // first chunk's squared norms
     }
-    // iteration j == nch is virtual: it only resolves the pending chunk
-    // (one call site for the exact path keeps the code and register use small)
-    for (int j = 0;; ++j) {
-      const bool last = j == nch;
-      const int i = j / CPW, k = j % CPW;
-      const int acc = i % NACC;
+    // Two chunks in flight: chunk j + 1's TMEM load is issued before chunk j
+    // is processed and waited for after it; a tile's accumulator goes back to
+    // the MMA warp as soon as its last chunk is in registers.
+    auto issue = [&](uint32_t (&dst)[32], int j) {
+      const int i = j / CPW, k = j % CPW, acc = i % NACC;
+      if (k == 0) {
+        mbar_wait(&t_full[acc], (i / NACC) & 1);
+        tc_fence_after();
+      }
+      tmem_ld32_issue(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + (h + NB * k) * 32, dst);
+    };
+    auto landed = [&](uint32_t (&dst)[32], int j) {
+      tmem_ld_wait(dst);
+      if (j % CPW == CPW - 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[(j / CPW) % NACC]);
+      }
+    };
+    // the screening and candidate bookkeeping of chunk j (raw dots in r)
+    auto process = [&](const uint32_t (&r)[32], int j) {
+#ifdef R2_EXP_NOEPI   // timing experiment (DESIGN 4): accumulators drained, not screened
+      return;
+#endif
       const int c0 = chunk_c0(j);
-      float v[32];
+      float* ic = inv_buf + (j & 1) * 32;
+      ic[lane] = inv_norm(q_nxt);
+      {
+        const int c = chunk_c0(j + 1) + lane;
+        q_nxt = (j + 1 < nch && c < n_r) ? __ldg(&sq[c]) : 0;   // next chunk, in flight
+      }
+      __syncwarp();
+      if (c0 >= n_r) return;                          // warp-uniform: past the reference rows
+      // screening maximum; invalid tail columns carry inv = 0 (score 0)
+      float cm = 0.f;
+      const float4* iv = reinterpret_cast<const float4*>(ic);
+#pragma unroll
+      for (int q4 = 0; q4 < 8; ++q4) {
+        const float4 f = iv[q4];
+        const float2 a = __fmul2_rn(make_float2(__uint_as_float(r[4 * q4 + 0]), __uint_as_float(r[4 * q4 + 1])),
+                                    make_float2(f.x, f.y));
+        const float2 b = __fmul2_rn(make_float2(__uint_as_float(r[4 * q4 + 2]), __uint_as_float(r[4 * q4 + 3])),
+                                    make_float2(f.z, f.w));
+        cm = fmaxf(fmaxf(cm, a.x), a.y);
+        cm = fmaxf(fmaxf(cm, b.x), b.y);
+      }
       // rows past the target count (the last M-tile's padding) never take the
       // exact path: their zero / stale rows would tie on every chunk
-      bool rec = false, near = last && row_ok;
-      float cm = 0.f;
-      if (!last) {
-        float* ic = inv_buf + (j & 1) * 32;
-        ic[lane] = inv_norm(q_nxt);
-        {
-          const int c = chunk_c0(j + 1) + lane;
-          q_nxt = (j + 1 < nch && c < n_r) ? __ldg(&sq[c]) : 0;   // next chunk, in flight
-        }
-        __syncwarp();
-        if (k == 0) {
-          if (e == 0 && lane == 0) R2_TR(6, i);
-          mbar_wait(&t_full[acc], (i / NACC) & 1);
-          if (e == 0 && lane == 0) R2_TR(7, i);
-          tc_fence_after();
-        }
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + (h + NB * k) * 32, v);
-        if (k == CPW - 1) {
-          // the tile's chunks are in registers: hand the accumulator back
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&t_empty[acc]);
-        }
-        if (c0 < n_r) {                               // warp-uniform
-          // screening maximum; invalid tail columns carry inv = 0 (score 0)
-          const float4* iv = reinterpret_cast<const float4*>(ic);
-#pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4) {
-            const float4 f = iv[q4];
-            const float2 a = __fmul2_rn(make_float2(v[4 * q4 + 0], v[4 * q4 + 1]), make_float2(f.x, f.y));
-            const float2 b = __fmul2_rn(make_float2(v[4 * q4 + 2], v[4 * q4 + 3]), make_float2(f.z, f.w));
-            cm = fmaxf(fmaxf(cm, a.x), a.y);
-            cm = fmaxf(fmaxf(cm, b.x), b.y);
-          }
-          const float T = fmaxf(r_cm, best);
-          rec = row_ok && cm > T * (1.f + 1e-5f);     // for T < 0 (nothing yet) always true
-          near = row_ok && !rec && cm >= T * (1.f - 1e-5f);
-        }
-      }
+      const float T = fmaxf(r_cm, best);
+      const bool rec = row_ok && cm > T * (1.f + 1e-5f);     // for T < 0 (nothing yet) always true
+      const bool near = row_ok && !rec && cm >= T * (1.f - 1e-5f);
       if (__any_sync(0xffffffffu, rec || near)) {
         if (near && r_c0 >= 0)
           resolve_chunk(rv, r_c0, r_cm, n_r, sq, best, bestD, bestq, bestcol);
-        if (last) break;
         if (rec) { best = -1.f; bestD = 0.f; bestq = 1; bestcol = -1; }
         const bool take = rec || near;
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) rv[jj] = take ? v[jj] : rv[jj];
+        for (int jj = 0; jj < 32; ++jj) rv[jj] = take ? __uint_as_float(r[jj]) : rv[jj];
         r_cm = take ? cm : r_cm;
         r_c0 = take ? c0 : r_c0;
       }
-      if (last) break;                                // also for warps of padding rows only
+    };
+    uint32_t va[32], vb[32];
+    if (nch > 0) {
+      issue(va, 0);
+      landed(va, 0);
     }
+    for (int j = 0; j < nch; j += 2) {
+      if (j + 1 < nch) issue(vb, j + 1);
+      process(va, j);
+      if (j + 1 >= nch) break;
+      landed(vb, j + 1);
+      if (j + 2 < nch) issue(va, j + 2);
+      process(vb, j + 1);
+      if (j + 2 < nch) landed(va, j + 2);
+    }
+    // the pending chunk, resolved once at the end
+    if (row_ok && r_c0 >= 0) resolve_chunk(rv, r_c0, r_cm, n_r, sq, best, bestD, bestq, bestcol);
     // merge the NB column blocks of each row (exact; ties -> smaller column = smaller kp id)
     if (h > 0) {
       const int sidx = (h - 1) * BM + row_loc;
