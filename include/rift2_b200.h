@@ -136,6 +136,21 @@ int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_
                        int32_t mode, void* desc_counts, int32_t desc_stride, int32_t desc_capacity,
                        int32_t* desc_sqnorm, int32_t* desc_kp, uint8_t* desc_variant, int32_t* desc_count,
                        int32_t* desc_skipped, void* workspace, size_t workspace_bytes, void* stream);
+/* As rift2_describe with float64 keypoint coordinates: keypoints need not
+ * be integral (ref: descriptor.py:105-125 -- axis crop at
+ * floor(x + 1 - patch/2), rotated samples at floor(x + ux + 0.5) from the
+ * reference's continuous float64 offsets; integral coordinates take the
+ * reference's integer-table path and give rift2_describe's result).  Any
+ * n_orient <= 16 and any cell size (patch_size divisible by grid) are
+ * accepted by both entry points; the BASELINE shape (6 orientations,
+ * 16-pixel cells, integer keypoints) runs on the staged fast kernel, the
+ * rest on a generic kernel with the same outputs. */
+int32_t rift2_describe_f64(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
+                           const double* kp_x, const double* kp_y, const int32_t* kp_count, int32_t kp_stride,
+                           int32_t patch_size, int32_t grid, double dominant_ratio, int32_t rotate_patch,
+                           int32_t mode, void* desc_counts, int32_t desc_stride, int32_t desc_capacity,
+                           int32_t* desc_sqnorm, int32_t* desc_kp, uint8_t* desc_variant, int32_t* desc_count,
+                           int32_t* desc_skipped, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- stage 4: brute-force nearest-neighbour matching ---------------------
  * Replaces ref: pkg/src/rift2/matcher.py:102-148 (match_nn) for `n_pairs`

@@ -51,12 +51,9 @@ int32_t map_internal(int32_t rc, const char* where) {
   return fail(RIFT2_UNSUPPORTED, "%s: unsupported size or parameter", where);
 }
 
-bool fft_len_ok(int n) {
-  if (n < 1) return false;
-  for (int p : {2, 3, 5})
-    while (n % p == 0) n /= p;
-  return n == 1;
-}
+// any length: radix-2/3/4/5/8 Stockham passes plus runtime-radix passes for
+// the other prime factors (fft.cuh generic_pass_any)
+bool fft_len_ok(int n) { return n >= 1; }
 
 int32_t bank_consts(const rift2_bank_params* p, r2::BankConsts& k) {
   if (!p) return fail(RIFT2_BAD_ARGUMENT, "params is NULL");
@@ -146,8 +143,7 @@ const char* rift2_last_error(void) { return g_err; }
 static int32_t check_fields_dims(int32_t batch, int32_t h, int32_t w) {
   if (batch < 1) return fail(RIFT2_BAD_ARGUMENT, "batch must be >= 1");
   if (h < 16 || w < 16) return fail(RIFT2_BAD_ARGUMENT, "filter bank needs width and height >= 16");
-  if (!fft_len_ok(h) || !fft_len_ok(w))
-    return fail(RIFT2_UNSUPPORTED, "image %dx%d: FFT lengths must factor into 2, 3 and 5", h, w);
+  if (!fft_len_ok(h) || !fft_len_ok(w)) return fail(RIFT2_UNSUPPORTED, "image %dx%d: bad FFT length", h, w);
   if ((w > 4096 || h > 4096) && !((w & (w - 1)) == 0 && (h & (h - 1)) == 0))
     return fail(RIFT2_UNSUPPORTED, "non power-of-two sizes above 4096 are not supported");
   if (w > 4096 || h > 4096) return fail(RIFT2_UNSUPPORTED, "sizes above 4096 are not supported");
@@ -218,12 +214,15 @@ int32_t rift2_describe_workspace_size(int32_t batch, int32_t kp_stride, int32_t 
   return RIFT2_OK;
 }
 
-int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
-                       const int32_t* kp_x, const int32_t* kp_y, const int32_t* kp_count, int32_t kp_stride,
-                       int32_t patch_size, int32_t grid, double dominant_ratio, int32_t rotate_patch,
-                       int32_t mode, void* desc_counts, int32_t desc_stride, int32_t desc_capacity,
-                       int32_t* desc_sqnorm, int32_t* desc_kp, uint8_t* desc_variant, int32_t* desc_count,
-                       int32_t* desc_skipped, void* workspace, size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+static int32_t describe_impl(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
+                             const int32_t* kp_x, const int32_t* kp_y, const double* kp_xd, const double* kp_yd,
+                             const int32_t* kp_count, int32_t kp_stride, int32_t patch_size, int32_t grid,
+                             double dominant_ratio, int32_t rotate_patch, int32_t mode, void* desc_counts,
+                             int32_t desc_stride, int32_t desc_capacity, int32_t* desc_sqnorm, int32_t* desc_kp,
+                             uint8_t* desc_variant, int32_t* desc_count, int32_t* desc_skipped, void* workspace,
+                             size_t workspace_bytes, void* stream) {
   if (batch < 1 || height < 1 || width < 1 || kp_stride < 0) return fail(RIFT2_BAD_ARGUMENT, "bad dimensions");
   if (n_orient < 2 || n_orient > 16) return fail(RIFT2_UNSUPPORTED, "n_orient must be in [2, 16]");
   if (grid < 1 || patch_size < grid || patch_size % grid != 0)
@@ -241,11 +240,38 @@ int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_
   if (!mim || !kp_count || !desc_counts || !desc_sqnorm || !desc_kp || !desc_variant || !desc_count ||
       !desc_skipped || !workspace)
     return fail(RIFT2_BAD_ARGUMENT, "NULL buffer");
+  if (kp_stride > 0 && !((kp_x && kp_y) || (kp_xd && kp_yd))) return fail(RIFT2_BAD_ARGUMENT, "NULL keypoints");
   r2::DescribeArgs a{batch, height, width, n_orient, kp_x, kp_y, kp_count, kp_stride, patch_size, grid,
                      dominant_ratio, rotate_patch != 0, mode, static_cast<__half*>(desc_counts), desc_stride,
-                     desc_capacity, desc_sqnorm, desc_kp, desc_variant, desc_count, desc_skipped};
+                     desc_capacity, desc_sqnorm, desc_kp, desc_variant, desc_count, desc_skipped, kp_xd, kp_yd};
   int32_t rc = r2::describe_run(mim, a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
   return map_internal(rc, "rift2_describe");
+}
+
+extern "C" {
+
+int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
+                       const int32_t* kp_x, const int32_t* kp_y, const int32_t* kp_count, int32_t kp_stride,
+                       int32_t patch_size, int32_t grid, double dominant_ratio, int32_t rotate_patch,
+                       int32_t mode, void* desc_counts, int32_t desc_stride, int32_t desc_capacity,
+                       int32_t* desc_sqnorm, int32_t* desc_kp, uint8_t* desc_variant, int32_t* desc_count,
+                       int32_t* desc_skipped, void* workspace, size_t workspace_bytes, void* stream) {
+  return describe_impl(mim, batch, height, width, n_orient, kp_x, kp_y, nullptr, nullptr, kp_count, kp_stride,
+                       patch_size, grid, dominant_ratio, rotate_patch, mode, desc_counts, desc_stride,
+                       desc_capacity, desc_sqnorm, desc_kp, desc_variant, desc_count, desc_skipped, workspace,
+                       workspace_bytes, stream);
+}
+
+int32_t rift2_describe_f64(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
+                           const double* kp_x, const double* kp_y, const int32_t* kp_count, int32_t kp_stride,
+                           int32_t patch_size, int32_t grid, double dominant_ratio, int32_t rotate_patch,
+                           int32_t mode, void* desc_counts, int32_t desc_stride, int32_t desc_capacity,
+                           int32_t* desc_sqnorm, int32_t* desc_kp, uint8_t* desc_variant, int32_t* desc_count,
+                           int32_t* desc_skipped, void* workspace, size_t workspace_bytes, void* stream) {
+  return describe_impl(mim, batch, height, width, n_orient, nullptr, nullptr, kp_x, kp_y, kp_count, kp_stride,
+                       patch_size, grid, dominant_ratio, rotate_patch, mode, desc_counts, desc_stride,
+                       desc_capacity, desc_sqnorm, desc_kp, desc_variant, desc_count, desc_skipped, workspace,
+                       workspace_bytes, stream);
 }
 
 // ------------------------------------------------------------------- match

@@ -48,12 +48,16 @@ constexpr int kOffBias = 32768;
 #define R2_DESC_CARVE 100
 #endif
 
+constexpr int kMaxOrientG = 16;   // the generic kernel's orientation limit (the C ABI's)
+
 struct GatherTables {
   const uint16_t* soff;  // [O][P*P] dy*stride + dx + kOffBias into the staged region; angle 0 unused
   const int4* bbox;      // [O] (dx_min, dx_max, dy_min, dy_max)
+  const double2* uv;     // [O][P*P] the reference's continuous offsets (ux, vy), float64
   int radius;            // max |offset| over all angles (and the axis crop)
   int stride;            // staged row length in bytes (multiple of 16)
   int4 hbbox[8];         // host copy of bbox
+  double4 hbbf[kMaxOrientG];   // (ux_min, ux_max, vy_min, vy_max) per angle
 };
 
 std::mutex g_mu;
@@ -75,6 +79,8 @@ GatherTables gather_tables(int P, int O) {
   auto it = g_tables.find(key);
   if (it != g_tables.end()) return it->second;
   std::vector<int2> off((size_t)O * P * P);
+  std::vector<double2> uv((size_t)O * P * P);
+  std::vector<double4> bbf(O);
   std::vector<int4> bbox(O);
   const double half = P / 2.0;
   int radius = (P + 1) / 2;   // axis crop spans [x + 1 - (P+1)/2, x + P - (P+1)/2]
@@ -82,33 +88,46 @@ GatherTables gather_tables(int P, int O) {
     const double ang = a * (M_PI / O);
     const double c = snap_h(std::cos(ang)), s = snap_h(std::sin(ang));
     int4 bb = make_int4(1 << 30, -(1 << 30), 1 << 30, -(1 << 30));
+    double4 bf = make_double4(1e300, -1e300, 1e300, -1e300);
     for (int i = 0; i < P; ++i) {
       const double v = i + 0.5 - half;
       for (int j = 0; j < P; ++j) {
         const double u = j + 0.5 - half;
-        const int dx = (int)std::floor(c * u - s * v + 0.5);
-        const int dy = (int)std::floor(s * u + c * v + 0.5);
+        const double ux = c * u - s * v, vy = s * u + c * v;   // ref: descriptor.py:61-62
+        uv[(size_t)a * P * P + i * P + j] = make_double2(ux, vy);
+        bf.x = std::min(bf.x, ux); bf.y = std::max(bf.y, ux);
+        bf.z = std::min(bf.z, vy); bf.w = std::max(bf.w, vy);
+        const int dx = (int)std::floor(ux + 0.5);
+        const int dy = (int)std::floor(vy + 0.5);
         off[(size_t)a * P * P + i * P + j] = make_int2(dx, dy);
         bb.x = std::min(bb.x, dx); bb.y = std::max(bb.y, dx);
         bb.z = std::min(bb.z, dy); bb.w = std::max(bb.w, dy);
       }
     }
     bbox[a] = bb;
+    bbf[a] = bf;
     radius = std::max({radius, -bb.x, bb.y, -bb.z, bb.w});
   }
   // staged row pitch: 2R+1 bytes from a 16-aligned start (+15; TMA box x
   // coordinates must be 16-byte aligned), one spare word for the funnel-shift
   // reads (+4), rounded to 16 bytes for the TMA box
   const int stride = ((2 * radius + 1 + 15 + 4 + 15) / 16) * 16;
-  GatherTables t{nullptr, nullptr, radius, stride, {}};
+  GatherTables t{nullptr, nullptr, nullptr, radius, stride, {}, {}};
   for (int a = 0; a < O && a < 8; ++a) t.hbbox[a] = bbox[a];
+  for (int a = 0; a < O && a < kMaxOrientG; ++a) t.hbbf[a] = bbf[a];
+  double2* d_uv = nullptr;
+  if (cudaMalloc(&d_uv, uv.size() * sizeof(double2)) != cudaSuccess) return t;
+  cudaMemcpy(d_uv, uv.data(), uv.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  t.uv = d_uv;                                   // the generic kernel's tables
   // biased 16-bit offsets: a thread's four samples of a row are one 8-byte load
   std::vector<uint16_t> soff(off.size());
+  bool fits = true;
   for (size_t i = 0; i < off.size(); ++i) {
     const int v = off[i].y * stride + off[i].x + kOffBias;
-    if (v < 0 || v > 65535) return t;            // (a patch far beyond the supported sizes)
+    if (v < 0 || v > 65535) { fits = false; break; }   // large patches: the generic kernel only
     soff[i] = (uint16_t)v;
   }
+  if (!fits) { g_tables[key] = t; return t; }
   uint16_t* d_off = nullptr;
   int4* d_bb = nullptr;
   if (cudaMalloc(&d_off, soff.size() * sizeof(uint16_t)) != cudaSuccess) return t;
@@ -514,6 +533,205 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   }
 }
 
+// ---------------------------------------------------------------------------
+// Generic descriptor kernel: any orientation count (<= 16), any cell size,
+// and keypoints with fractional coordinates (ref: descriptor.py:85-125: the
+// axis crop at floor(x + 1 - P/2), rotated samples at floor(x + ux + 0.5)
+// in float64 from the continuous offsets; integer keypoints take the
+// reference's integer table path floor(ux + 0.5) + x).  One CTA per
+// keypoint, straight from the global index map, counts by shared-memory
+// atomics: the BASELINE configuration (6 orientations, 16-px cells, integer
+// keypoints from the detector) runs on k_desc_main; this covers the rest of
+// the reference's parameter space exactly.
+struct DescConstG {
+  int H, W, O, P, g, cs, cells, dim;
+  double ratio;
+  bool rotate;
+  int mode;
+  double4 bbf[kMaxOrientG];   // continuous offset bounds per angle
+};
+
+constexpr int kTG = 256;
+
+R2_DEV void count_patch_g(const uint8_t* m, const DescConstG& c, const DescribeArgs& a, int y0, int x0,
+                          const double2* uv, double xd, double yd, bool integral, unsigned* cnt) {
+  const int P = c.P;
+  for (int idx = threadIdx.x; idx < P * P; idx += kTG) {
+    const int i = idx / P, j = idx - i * P;
+    int sy, sx;
+    if (!uv) {
+      sy = y0 + i;
+      sx = x0 + j;
+    } else {
+      const double2 o = __ldg(&uv[idx]);
+      if (integral) {
+        sx = (int)xd + (int)floor(o.x + 0.5);
+        sy = (int)yd + (int)floor(o.y + 0.5);
+      } else {
+        sx = (int)floor(__dadd_rn(__dadd_rn(xd, o.x), 0.5));
+        sy = (int)floor(__dadd_rn(__dadd_rn(yd, o.y), 0.5));
+      }
+    }
+    const int v = m[(size_t)sy * c.W + sx];   // 1..O; anything else counts nothing
+    const int cell = (i / c.cs) * c.g + j / c.cs;
+    if (v >= 1 && v <= c.O) atomicAdd(&cnt[cell * c.O + v - 1], 1u);
+  }
+}
+
+// bounds of a rotated patch (monotone in the offset: the extreme samples
+// come from the extreme offsets), ref: descriptor.py:118-125
+R2_DEV bool rotated_inside(const DescConstG& c, int ang, double xd, double yd, bool integral) {
+  const double4 b = c.bbf[ang];
+  int x_lo, x_hi, y_lo, y_hi;
+  if (integral) {
+    x_lo = (int)xd + (int)floor(b.x + 0.5); x_hi = (int)xd + (int)floor(b.y + 0.5);
+    y_lo = (int)yd + (int)floor(b.z + 0.5); y_hi = (int)yd + (int)floor(b.w + 0.5);
+  } else {
+    x_lo = (int)floor(__dadd_rn(__dadd_rn(xd, b.x), 0.5)); x_hi = (int)floor(__dadd_rn(__dadd_rn(xd, b.y), 0.5));
+    y_lo = (int)floor(__dadd_rn(__dadd_rn(yd, b.z), 0.5)); y_hi = (int)floor(__dadd_rn(__dadd_rn(yd, b.w), 0.5));
+  }
+  return x_lo >= 0 && x_hi < c.W && y_lo >= 0 && y_hi < c.H;
+}
+
+template <bool FKP>
+__global__ void __launch_bounds__(kTG) k_desc_generic(const uint8_t* __restrict__ mim, DescribeArgs a, DescConstG c,
+                                                      const double2* __restrict__ uv,
+                                                      unsigned long long* __restrict__ chain,
+                                                      unsigned* __restrict__ ticket) {
+  extern __shared__ unsigned s_cnt[];           // [3][cells * O]: axis patch, rotated picks 0 and 1
+  __shared__ unsigned s_hist[kMaxOrientG];
+  __shared__ int s_pick[kMaxOrientG];
+  __shared__ int s_np, s_k;
+  __shared__ unsigned s_excl;
+  const int b = blockIdx.y;
+  const int mode = c.mode == 3 ? ((b & 1) ? 0 : 1) : c.mode;   // see k_desc_main
+  if (threadIdx.x == 0) s_k = (int)atomicAdd(&ticket[b], 1u);
+  __syncthreads();
+  const int k = s_k;
+  if (k >= min(a.kp_count[b], a.kp_stride)) return;
+  unsigned long long* lb = chain + (size_t)b * a.kp_stride;
+  const size_t ki = (size_t)b * a.kp_stride + k;
+  const double xd = FKP ? a.kp_xd[ki] : (double)a.kp_x[ki];
+  const double yd = FKP ? a.kp_yd[ki] : (double)a.kp_y[ki];
+  const bool integral = !FKP || (xd == floor(xd) && yd == floor(yd));
+  const int x0 = (int)floor(xd + 1.0 - c.P / 2.0), y0 = (int)floor(yd + 1.0 - c.P / 2.0);
+  if (x0 < 0 || y0 < 0 || x0 + c.P > c.W || y0 + c.P > c.H) {
+    if (threadIdx.x == 0) {
+      chain_publish(&lb[k], kChainAgg, 0u);
+      atomicAdd(&a.skipped[b], 1);
+    }
+    return;
+  }
+  const int nb = c.cells * c.O;
+  const uint8_t* m = mim + (size_t)b * c.H * c.W;
+  for (int i = threadIdx.x; i < 3 * nb; i += kTG) s_cnt[i] = 0;
+  __syncthreads();
+  count_patch_g(m, c, a, y0, x0, nullptr, xd, yd, integral, s_cnt);
+  __syncthreads();
+  if (threadIdx.x < c.O) {                       // patch histogram (ref: mim.py:58-66)
+    unsigned h = 0;
+    for (int q = 0; q < c.cells; ++q) h += s_cnt[q * c.O + threadIdx.x];
+    s_hist[threadIdx.x] = h;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int np = 0, skip = 0;
+    if (mode == 0) s_pick[np++] = 1;
+    else if (mode == 1) { for (int v = 1; v <= c.O; ++v) s_pick[np++] = v; }
+    else {
+      // ref: mim.py:69-91 (first argmax; runner-up >= ratio * peak, cyclic tie rule)
+      int pk = 0;
+      for (int v = 1; v < c.O; ++v) if (s_hist[v] > s_hist[pk]) pk = v;
+      double rv = -1.0;
+      for (int v = 0; v < c.O; ++v) if (v != pk && (double)s_hist[v] > rv) rv = (double)s_hist[v];
+      int picks[2] = {pk + 1, 0}, cand = 1;
+      if (rv >= c.ratio * (double)s_hist[pk]) {
+        int best = -1, bestd = 1 << 30;
+        for (int v = 0; v < c.O; ++v) {
+          if (v == pk || (double)s_hist[v] != rv) continue;
+          const int d = v > pk ? v - pk : v - pk + c.O;
+          if (d < bestd) { bestd = d; best = v; }
+        }
+        picks[1] = best + 1;
+        cand = 2;
+      }
+      for (int q = 0; q < cand; ++q) {
+        const int dom = picks[q];
+        if (c.rotate && dom != 1 && !rotated_inside(c, dom - 1, xd, yd, integral)) { ++skip; continue; }
+        s_pick[np++] = dom;
+      }
+    }
+    s_np = np;
+    chain_publish(&lb[k], kChainAgg, (unsigned)np);
+    if (skip) atomicAdd(&a.skipped[b], skip);
+    if (np) atomicAdd(&a.count[b], np);
+  }
+  __syncthreads();
+  const int np = s_np;
+  const bool rot_mode = mode == 2 && c.rotate;
+  int nrot = 0;
+  for (int q = 0; q < np && q < 2; ++q) {
+    const int dom = s_pick[q];
+    if (rot_mode && dom != 1) {
+      count_patch_g(m, c, a, y0, x0, uv + (size_t)(dom - 1) * c.P * c.P, xd, yd, integral, s_cnt + (1 + nrot) * nb);
+      ++nrot;
+    }
+  }
+  // output offset: decoupled look-back over the earlier keypoints' counts (as k_desc_main)
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    unsigned excl = 0;
+    for (int base = k - 1; base >= 0; base -= 32) {
+      const int j = base - (int)lane;
+      unsigned long long f = 2ull << 62;
+      if (j >= 0) do { f = chain_read(&lb[j]); } while ((f >> 62) == 0);
+      const unsigned pre = __ballot_sync(0xffffffffu, (f >> 62) == kChainPrefix);
+      const int stop = pre ? __ffs(pre) - 1 : 32;
+      unsigned v = (int)lane <= stop ? (unsigned)f : 0u;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      excl += v;
+      if (pre) break;
+    }
+    if (lane == 0) {
+      chain_publish(&lb[k], kChainPrefix, excl + (unsigned)np);
+      s_excl = excl;
+    }
+  }
+  __syncthreads();
+  const unsigned excl = s_excl;
+  int r = 0;
+  for (int q = 0; q < np; ++q) {
+    const int dom = s_pick[q];
+    const bool rotated = rot_mode && dom != 1;
+    const unsigned* src = rotated ? s_cnt + (1 + r) * nb : s_cnt;
+    const int var = mode == 0 ? 1 : dom;
+    const unsigned dst = excl + q;
+    if (dst < (unsigned)a.cap) {
+      const size_t o = (size_t)b * a.cap + dst;
+      __half* row = a.counts + o * a.stride;
+      // recode (ref: mim.py:117-136): output bin (cell, w) <- value (w + var - 1) mod O
+      for (int i = threadIdx.x; i < a.stride; i += kTG) {
+        unsigned v = 0;
+        if (i < c.dim) {
+          const int cell = i / c.O, w = i % c.O;
+          const int u = w + var - 1;
+          v = src[cell * c.O + (u >= c.O ? u - c.O : u)];
+        }
+        row[i] = __uint2half_rn(v);
+      }
+      if (threadIdx.x == 0) {
+        int sq = 0;
+        for (int i = 0; i < nb; ++i) sq += (int)(src[i] * src[i]);
+        a.sqnorm[o] = sq;
+        a.kp[o] = k;
+        a.variant[o] = (uint8_t)var;
+      }
+    }
+    if (rotated) ++r;
+  }
+}
+
 struct DescWs {
   size_t off_chain, off_ticket, total;
 };
@@ -546,16 +764,38 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
   const int S = a.kp_stride > 0 ? a.kp_stride : 1;
   const DescWs p = plan_ws(a.B, S);
   if (ws_bytes < p.total) return 1;
-  if (a.stride % 8 != 0 || a.stride > kMaxStride) return 2;
+  if (a.stride % 8 != 0) return 2;
   const int cs = a.patch / a.grid;
-  // 5-bit one-hot fields (O <= 6, cs <= 31 rows per thread), 4 columns per thread
-  if (a.O > 6 || cs != 16 || a.grid * a.grid * (cs / 4) > kT) return 2;
+  if (a.O > kMaxOrientG || a.patch % a.grid != 0) return 2;
+  GatherTables tab = gather_tables(a.patch, a.O);
+  if (!tab.uv) return 3;
+  // k_desc_main: 5-bit one-hot fields (O <= 6, cs <= 31 rows per thread), 4
+  // columns per thread, integer keypoints; everything else: k_desc_generic
+  const bool fast = !a.kp_xd && a.O <= 6 && cs == 16 && a.grid * a.grid * (cs / 4) <= kT && tab.soff &&
+                    a.stride <= kMaxStride;
+  if (!fast) {
+    DescConstG g{};
+    g.H = a.H; g.W = a.W; g.O = a.O; g.P = a.patch; g.g = a.grid; g.cs = cs;
+    g.cells = a.grid * a.grid; g.dim = g.cells * a.O;
+    g.ratio = a.ratio; g.rotate = a.rotate; g.mode = a.mode;
+    for (int q = 0; q < a.O; ++q) g.bbf[q] = tab.hbbf[q];
+    char* w = static_cast<char*>(ws);
+    auto* chain = reinterpret_cast<unsigned long long*>(w + p.off_chain);
+    auto* ticket = reinterpret_cast<unsigned*>(w + p.off_ticket);
+    cudaMemsetAsync(a.count, 0, sizeof(int32_t) * a.B, st);
+    cudaMemsetAsync(a.skipped, 0, sizeof(int32_t) * a.B, st);
+    if (a.kp_stride == 0) return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+    cudaMemsetAsync(w, 0, p.total, st);
+    const size_t smem = 3 * (size_t)g.cells * g.O * sizeof(uint32_t);
+    auto kern = a.kp_xd ? k_desc_generic<true> : k_desc_generic<false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<dim3(a.kp_stride, a.B), kTG, smem, st>>>(mim, a, g, tab.uv, chain, ticket);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+  }
   DescConst c{};
   c.H = a.H; c.W = a.W; c.O = a.O; c.P = a.patch; c.g = a.grid; c.cs = cs;
   c.cells = a.grid * a.grid; c.dim = c.cells * a.O; c.per = per_kp(a.mode, a.O);
   c.ratio = a.ratio; c.rotate = a.rotate; c.mode = a.mode;
-  GatherTables tab = gather_tables(a.patch, a.O);
-  if (!tab.soff) return 2;
   c.R = tab.radius;
   for (int q = 0; q < 8; ++q) c.bbox[q] = tab.hbbox[q];
   c.stride = tab.stride;

@@ -24,6 +24,8 @@ struct DescribeArgs {
   uint8_t* variant;
   int32_t* count;
   int32_t* skipped;
+  const double* kp_xd = nullptr;   // float64 keypoints (rift2_describe_f64) instead of kp_x / kp_y
+  const double* kp_yd = nullptr;
 };
 
 size_t describe_workspace_bytes(int B, int kp_stride, int grid, int O);

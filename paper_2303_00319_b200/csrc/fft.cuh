@@ -295,6 +295,38 @@ R2_DEV void generic_pass(const float2* src, float2* dst, int N, int Ns, const fl
   }
 }
 
+// One Stockham pass of any radix R (the prime factors above 5 of a generic
+// length, ref: loggabor.py:162-185 takes any image size): thread per output,
+// an R-term DFT of the twiddled inputs with W_R^m = W_N^(m N / R) from the
+// same table.  O(N R) per pass, so lengths with large prime factors are
+// slow but exact in the same sense as the radix-2/3/5 passes.
+R2_DEV void generic_pass_any(const float2* src, float2* dst, int N, int Ns, int R, const float2* __restrict__ tw,
+                             int tid, int nth) {
+  const int NR = N / R;
+  const int step = N / (Ns * R);
+  const int wr = N / R;                 // W_R = W_N^wr
+  for (int idx = tid; idx < N; idx += nth) {
+    const int j = idx % NR, ro = idx / NR;
+    const int k = j % Ns;
+    float2 acc = make_float2(0.f, 0.f);
+    int e_in = 0, e_out = 0;            // exponents of W_N, kept reduced mod N
+    const int din = k * step, dout = (ro * wr) % N;
+    for (int r = 0; r < R; ++r) {
+      const float2 x = src[pad32(j + r * NR)];
+      const int e = e_in + e_out >= N ? e_in + e_out - N : e_in + e_out;   // twiddle r k step + DFT r ro N / R
+      const float2 w = __ldg(&tw[e]);
+      acc.x = fmaf(x.x, w.x, fmaf(-x.y, w.y, acc.x));
+      acc.y = fmaf(x.x, w.y, fmaf(x.y, w.x, acc.y));
+      e_in += din;
+      if (e_in >= N) e_in -= N;
+      e_out += dout;
+      if (e_out >= N) e_out -= N;
+    }
+    const int o = (j / Ns) * Ns * R + k;
+    dst[pad32(o + ro * Ns)] = acc;
+  }
+}
+
 // Block-cooperative forward FFT of buf (padded, natural order) in place.
 R2_DEV void fft_generic(float2* buf, float2* scr, int N, const GenericPlan& plan,
                         const float2* __restrict__ tw, int tid, int nth) {
@@ -308,7 +340,8 @@ R2_DEV void fft_generic(float2* buf, float2* scr, int N, const GenericPlan& plan
       case 3: generic_pass<3>(src, dst, N, Ns, tw, tid, nth); break;
       case 4: generic_pass<4>(src, dst, N, Ns, tw, tid, nth); break;
       case 5: generic_pass<5>(src, dst, N, Ns, tw, tid, nth); break;
-      default: generic_pass<8>(src, dst, N, Ns, tw, tid, nth); break;
+      case 8: generic_pass<8>(src, dst, N, Ns, tw, tid, nth); break;
+      default: generic_pass_any(src, dst, N, Ns, R, tw, tid, nth); break;
     }
     __syncthreads();
     Ns *= R;

@@ -1381,6 +1381,17 @@ static bool make_plan(int n, GenericPlan& p) {
       m /= r;
     }
   }
+  // any remaining prime factors: runtime-radix passes (generic_pass_any)
+  for (int r = 7; m > 1 && r * r <= m; r += 2) {
+    while (m % r == 0 && p.n_pass < 16) {
+      p.radix[p.n_pass++] = r;
+      m /= r;
+    }
+  }
+  if (m > 1 && p.n_pass < 16) {
+    p.radix[p.n_pass++] = m;
+    m = 1;
+  }
   return m == 1;
 }
 

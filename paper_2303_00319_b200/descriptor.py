@@ -70,10 +70,13 @@ def _mim_device(mim):
 
 
 def _kp_arrays(keypoints):
+    """int32 coordinates when every keypoint is integral (the detector's
+    output), else float64 for rift2_describe_f64 (ref: descriptor.py:105-125
+    samples fractional keypoints at floor(x + ux + 0.5))."""
     xs = np.array([k.x for k in keypoints], dtype=np.float64)
     ys = np.array([k.y for k in keypoints], dtype=np.float64)
     if np.any(xs != np.floor(xs)) or np.any(ys != np.floor(ys)):
-        raise ParameterError("keypoints must have integer coordinates (detector output always does)")
+        return xs, ys
     return xs.astype(np.int32), ys.astype(np.int32)
 
 

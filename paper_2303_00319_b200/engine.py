@@ -131,8 +131,9 @@ MODE_CODE = {"plain": 0, "ring": 1, "rift2": 2, "ring_pipeline": 3}
 def describe(mim: torch.Tensor, kp_x: torch.Tensor, kp_y: torch.Tensor, kp_count: torch.Tensor,
              n_orient: int, patch: int = 96, grid: int = 6, ratio: float = 0.8, rotate: bool = True,
              mode: str = "rift2", capacity: int | None = None, ws_key: str = "describe", out=None):
-    """mim (B, H, W) uint8 CUDA, keypoints (B, S) int32 -> dict(counts (B, cap,
-    224) f16, sqnorm, kp, variant, count, skipped)."""
+    """mim (B, H, W) uint8 CUDA, keypoints (B, S) int32 (or float64: any
+    coordinates, rift2_describe_f64) -> dict(counts (B, cap, 224) f16,
+    sqnorm, kp, variant, count, skipped)."""
     lib = _lib.load(require_gpu=True)
     B, H, W = mim.shape
     S = kp_x.shape[1]
@@ -151,7 +152,8 @@ def describe(mim: torch.Tensor, kp_x: torch.Tensor, kp_y: torch.Tensor, kp_count
                    variant=torch.zeros((B, cap), dtype=torch.uint8, device=dev),
                    count=torch.empty((B,), dtype=torch.int32, device=dev),
                    skipped=torch.empty((B,), dtype=torch.int32, device=dev))
-    rc = lib.rift2_describe(_ptr(mim.contiguous()), B, H, W, int(n_orient), _ptr(kp_x), _ptr(kp_y),
+    fn = lib.rift2_describe_f64 if kp_x.dtype == torch.float64 else lib.rift2_describe
+    rc = fn(_ptr(mim.contiguous()), B, H, W, int(n_orient), _ptr(kp_x), _ptr(kp_y),
                             _ptr(kp_count), S, int(patch), int(grid), float(ratio), 1 if rotate else 0,
                             MODE_CODE[mode], _ptr(out["counts"]), out["counts"].shape[2], out["counts"].shape[1],
                             _ptr(out["sqnorm"]), _ptr(out["kp"]), _ptr(out["variant"]), _ptr(out["count"]),

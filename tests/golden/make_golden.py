@@ -218,7 +218,54 @@ def case_evaluate():
     save("evaluate.npz", **out)
 
 
-CASES = dict(fields_small=case_fields_small, detector=case_detector, matcher=case_matcher, pair=case_pair,
+def desc_counts_general(dset, grid, cs):
+    """Integer counts of a descriptor set for any grid / cell size: every
+    cell holds cs^2 samples, so counts = v * cs^2 / sum_cell(v)."""
+    vec = np.array([d.vector for d in dset.descriptors]).reshape(len(dset), -1)
+    counts = np.zeros(vec.shape, np.uint16)
+    for i, v in enumerate(vec):
+        cells = v.reshape(grid * grid, -1)
+        c = np.rint(cells * (cs * cs / cells.sum(1, keepdims=True))).astype(np.int64).ravel()
+        counts[i] = c
+        assert np.array_equal(c / np.linalg.norm(c.astype(np.float64)), v)
+    return dict(counts=counts,
+                kp=np.array([d.keypoint_id for d in dset.descriptors], np.int32),
+                variant=np.array([d.variant for d in dset.descriptors], np.int8),
+                skipped=np.int64(dset.skipped))
+
+
+def case_desc_general():
+    """Descriptors outside the BASELINE shape, from the reference itself:
+    fractional keypoints (ref: descriptor.py:118-125), 8 orientations, 12-
+    and 24-pixel cells.  Index maps from compute_fields of a 224^2 image."""
+    from rift2.detector import Keypoint
+    a, _, _ = synth.make_pair(224, seed=5, theta_deg=20.0, looks=None)
+    rng = np.random.default_rng(21)
+    out = {}
+    # keypoints: fractional (incl. exact halves and a few integers), some near the border (skips)
+    n = 90
+    xs = rng.uniform(20.0, 204.0, n)
+    ys = rng.uniform(20.0, 204.0, n)
+    xs[:10] = np.floor(xs[:10]) + 0.5
+    ys[5:15] = np.floor(ys[5:15]) + 0.5
+    xs[15:20] = np.floor(xs[15:20])
+    ys[15:20] = np.floor(ys[15:20])
+    kps = [Keypoint(float(x), float(y), 1.0, "corner") for x, y in zip(xs, ys)]
+    out["kp_x"], out["kp_y"] = xs, ys
+    for tag, n_orient, patch, grid in (("o6", 6, 96, 6), ("o8", 8, 64, 4), ("c12", 6, 72, 6), ("c24", 6, 96, 4)):
+        cfg = RiftConfig(n_orient=n_orient, **BASE)
+        _, mim = compute_fields(a, cfg)
+        out[f"{tag}_mim"] = mim.indices.astype(np.int8)
+        cs = patch // grid
+        for mode, fn in (("rift2", lambda: describe_rift2(mim, kps, patch_size=patch, grid=grid)),
+                         ("ring", lambda: describe_ring(mim, kps, patch_size=patch, grid=grid)),
+                         ("plain", lambda: describe_plain(mim, kps, patch_size=patch, grid=grid))):
+            for k, v in desc_counts_general(fn(), grid, cs).items():
+                out[f"{tag}_{mode}_{k}"] = v
+    save("desc_general.npz", **out)
+
+
+CASES = dict(desc_general=case_desc_general, fields_small=case_fields_small, detector=case_detector, matcher=case_matcher, pair=case_pair,
              container=case_container, evaluate=case_evaluate)
 
 if __name__ == "__main__":

@@ -40,10 +40,26 @@ def test_fields_odd_shapes_vs_oracle(eng, shape):
     assert np.mean(out["mim"][0] == ref["mim"]) >= 0.999
 
 
+@pytest.mark.parametrize("shape", [(98, 98), (77, 91), (67, 71), (143, 52)])
+def test_fields_any_prime_factor_vs_oracle(eng, shape):
+    # lengths with prime factors above 5 (98 = 2*7^2, 77 = 7*11, 91 = 7*13,
+    # primes 67 and 71, 143 = 11*13): the reference takes any size >= 16
+    # (ref: loggabor.py:131-185); runtime-radix Stockham passes
+    rng = np.random.default_rng(12)
+    img = rng.random(shape)
+    bank = O.Bank()
+    out = _fields_gpu(eng, img[None], bank)
+    ref = O.fields(img, bank, workers=8)
+    assert max_norm_err(out["mmax"][0], ref["moment_max"]) <= 1e-4
+    assert max_norm_err(out["mmin"][0], ref["moment_min"]) <= 1e-4
+    assert max_norm_err(out["pc"][0], ref["pc"]) <= 1e-4
+    assert np.mean(out["mim"][0] == ref["mim"]) >= 0.999
+
+
 def test_fields_unsupported_size_is_parameter_error(eng):
     from paper_2303_00319_b200.errors import ParameterError
     with pytest.raises(ParameterError):
-        _fields_gpu(eng, np.zeros((1, 98, 98)), O.Bank())       # 98 = 2 * 7^2
+        _fields_gpu(eng, np.zeros((1, 8, 64)), O.Bank())        # below the reference's 16-pixel minimum
 
 
 @pytest.mark.parametrize("cap", [1, 7, 64])

@@ -50,7 +50,8 @@ def test_version_and_errors_without_gpu(lib):
     assert rc == 1 and b"n_scales" in lib.rift2_last_error()
     p = _lib.BankParamsC(4, 6, 3.0, 2.1, 0.55, 0.0, 2.0, 0.5, 10.0)
     assert lib.rift2_fields_workspace_size(1, 8, 64, ctypes.byref(p), ctypes.byref(n)) == 1
-    assert lib.rift2_fields_workspace_size(1, 64, 77, ctypes.byref(p), ctypes.byref(n)) == 2   # prime 7, 11
+    assert lib.rift2_fields_workspace_size(1, 64, 77, ctypes.byref(p), ctypes.byref(n)) == 0   # 7 * 11: any length
+    assert lib.rift2_fields_workspace_size(1, 64, 8192, ctypes.byref(p), ctypes.byref(n)) == 2   # above 4096
     assert lib.rift2_fields_workspace_size(2, 1024, 1024, ctypes.byref(p), ctypes.byref(n)) == 0
     assert n.value > 2 * 24 * 1024 * 1024 * 8
     with pytest.raises(Exception):
