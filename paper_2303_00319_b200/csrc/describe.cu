@@ -438,15 +438,16 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
       int pk = 0;
 #pragma unroll
       for (int v = 1; v < 8; ++v) if (v < O && hs[v] > hs[pk]) pk = v;
-      double rv = -1.0;
+      // (counts are integers: only the ratio test needs float64)
+      int rv = -1;
 #pragma unroll
-      for (int v = 0; v < 8; ++v) if (v < O && v != pk && (double)hs[v] > rv) rv = (double)hs[v];
+      for (int v = 0; v < 8; ++v) if (v < O && v != pk && (int)hs[v] > rv) rv = (int)hs[v];
       int picks[2] = {pk + 1, 0}, cand = 1;
-      if (rv >= c.ratio * (double)hs[pk]) {
+      if (rv >= 0 && (double)rv >= c.ratio * (double)hs[pk]) {
         int best = -1, bestd = 1 << 30;
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-          if (v >= O || v == pk || (double)hs[v] != rv) continue;
+          if (v >= O || v == pk || (int)hs[v] != rv) continue;
           const int d = v > pk ? v - pk : v - pk + O;
           if (d < bestd) { bestd = d; best = v; }
         }
