@@ -130,6 +130,12 @@ int32_t rift2_detect_f64(const double* min_maps, const double* max_maps, int32_t
  * kp_stride are clamped to it. */
 int32_t rift2_describe_workspace_size(int32_t batch, int32_t kp_stride, int32_t grid, int32_t n_orient,
                                       size_t* bytes);
+/* The larger workspace that also holds a shift-byte copy of the index maps
+ * (one pass before the per-keypoint kernel, so it stages them with no
+ * in-place transform): a workspace of this size makes rift2_describe
+ * faster at the same results; the smaller size above stays valid. */
+int32_t rift2_describe_workspace_size_hw(int32_t batch, int32_t height, int32_t width, int32_t kp_stride,
+                                         int32_t grid, int32_t n_orient, size_t* bytes);
 int32_t rift2_describe(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,
                        const int32_t* kp_x, const int32_t* kp_y, const int32_t* kp_count, int32_t kp_stride,
                        int32_t patch_size, int32_t grid, double dominant_ratio, int32_t rotate_patch,

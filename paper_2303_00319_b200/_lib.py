@@ -44,6 +44,8 @@ _SIGNATURES = {
     "rift2_detect_f64": (_c_int, [_c_p, _c_p, _c_int, _c_int, _c_int, _c_d, _c_int, _c_int, _c_int, _c_p,
                                   _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "rift2_describe_workspace_size": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_sz)]),
+    "rift2_describe_workspace_size_hw": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                                  ctypes.POINTER(_c_sz)]),
     "rift2_describe": (_c_int, [_c_p, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p, _c_int, _c_int, _c_int,
                                 _c_d, _c_int, _c_int, _c_p, _c_int, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p,
                                 _c_p, _c_sz, _c_p]),

@@ -99,8 +99,9 @@ class BatchPipeline:
         self.run_features()
 
     # our kernels per step: fields 10 (with the moment-range init) + detect 9
-    # (no k_minmax: the PC pass reduced the maps) + describe 1 + match 7
-    KERNELS_PER_STEP = 27
+    # (no k_minmax: the PC pass reduced the maps) + describe 2 (the shift-byte
+    # copy of the index maps, the per-keypoint kernel) + match 7
+    KERNELS_PER_STEP = 28
 
     # ---- graphs ------------------------------------------------------------
     def capture(self):

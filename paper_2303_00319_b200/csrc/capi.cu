@@ -214,6 +214,15 @@ int32_t rift2_describe_workspace_size(int32_t batch, int32_t kp_stride, int32_t 
   return RIFT2_OK;
 }
 
+int32_t rift2_describe_workspace_size_hw(int32_t batch, int32_t height, int32_t width, int32_t kp_stride,
+                                         int32_t grid, int32_t n_orient, size_t* bytes) {
+  if (batch < 1 || height < 1 || width < 1 || kp_stride < 0 || grid < 1 || grid > 16 || n_orient < 2 ||
+      n_orient > 16 || !bytes)
+    return fail(RIFT2_BAD_ARGUMENT, "bad describe dimensions");
+  *bytes = r2::describe_workspace_bytes_hw(batch, height, width, kp_stride, grid, n_orient);
+  return RIFT2_OK;
+}
+
 }  // extern "C"
 
 static int32_t describe_impl(const uint8_t* mim, int32_t batch, int32_t height, int32_t width, int32_t n_orient,

@@ -147,6 +147,7 @@ struct DescConst {
   int mode;
   int R, stride, rows;   // staging radius, staged row bytes, staged rows (2R+1)
   int tma;               // stage the neighbourhood with one TMA box load
+  int preshift;          // the TMA source already holds shift bytes 5(v-1) (k_mim_shift)
   int4 bbox[8];          // per-angle rotated-patch bounding boxes (dx_min, dx_max, dy_min, dy_max)
 };
 
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
     __syncthreads();
     mbar_wait(&s_bar, 0);
     uint4* q4 = reinterpret_cast<uint4*>(sw);
+    if (!c.preshift)
     for (int i = threadIdx.x; i < c.rows * c.stride / 16; i += kT) {
       uint4 w = q4[i];
       w.x = w.x * 5u - 0x05050505u;
@@ -733,6 +735,22 @@ __global__ void __launch_bounds__(kTG) k_desc_generic(const uint8_t* __restrict_
   }
 }
 
+// The index map as shift bytes 5(v-1) in one pass over the planes, so the
+// per-keypoint kernel stages them by TMA with no in-place transform of its
+// ~21 KB neighbourhood (that pass was a fifth of its shared-memory traffic).
+// Zero-filled bytes beyond the map then count as index 1, but no emitted
+// descriptor ever samples them (the skip tests bound every sample).
+__global__ void __launch_bounds__(256) k_mim_shift(const uint4* __restrict__ in, uint4* __restrict__ out, size_t n16) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    uint4 w = __ldg(&in[i]);
+    w.x = w.x * 5u - 0x05050505u;
+    w.y = w.y * 5u - 0x05050505u;
+    w.z = w.z * 5u - 0x05050505u;
+    w.w = w.w * 5u - 0x05050505u;
+    out[i] = w;
+  }
+}
+
 struct DescWs {
   size_t off_chain, off_ticket, total;
 };
@@ -759,6 +777,11 @@ size_t describe_workspace_bytes(int B, int kp_stride, int grid, int O) {
   (void)grid;
   (void)O;
   return plan_ws(B, kp_stride > 0 ? kp_stride : 1).total;
+}
+
+size_t describe_workspace_bytes_hw(int B, int H, int W, int kp_stride, int grid, int O) {
+  // + the shift-byte copy of the index maps (used when the workspace holds it)
+  return describe_workspace_bytes(B, kp_stride, grid, O) + al((size_t)B * H * W);
 }
 
 int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -813,15 +836,28 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
   dim3 grid(a.kp_stride, a.B);
   CUtensorMap tmap{};
   c.tma = 0;
+  c.preshift = 0;
   auto enc = get_encode();
   if (enc && c.W % 16 == 0 && c.stride <= 256 && c.rows <= 256 && ((uintptr_t)mim & 15) == 0) {
+    // the shift-byte copy when the workspace has room for it (the
+    // height/width-aware size query), else the in-place transform
+    const uint8_t* src = mim;
+    const size_t n = (size_t)a.B * a.H * a.W;
+    if (ws_bytes >= p.total + al(n)) {
+      uint8_t* sh = static_cast<uint8_t*>(ws) + p.total;
+      const size_t n16 = n / 16;
+      k_mim_shift<<<(unsigned)std::min<size_t>((n16 + 255) / 256, 148 * 16), 256, 0, st>>>(
+          reinterpret_cast<const uint4*>(mim), reinterpret_cast<uint4*>(sh), n16);
+      src = sh;
+      c.preshift = 1;
+    }
     // 2-D view (W, B*H): rows outside one image read its neighbour (or zeros
     // at the ends) -- never sampled by an emitted descriptor, see above
     cuuint64_t dims[2] = {(cuuint64_t)c.W, (cuuint64_t)c.H * a.B};
     cuuint64_t strides[1] = {(cuuint64_t)c.W};
     cuuint32_t box[2] = {(cuuint32_t)c.stride, (cuuint32_t)c.rows};
     cuuint32_t es[2] = {1, 1};
-    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(mim), dims, strides, box, es,
+    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(src), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
       c.tma = 1;

@@ -29,6 +29,7 @@ struct DescribeArgs {
 };
 
 size_t describe_workspace_bytes(int B, int kp_stride, int grid, int O);
+size_t describe_workspace_bytes_hw(int B, int H, int W, int kp_stride, int grid, int O);
 int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace r2

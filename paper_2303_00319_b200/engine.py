@@ -142,7 +142,7 @@ def describe(mim: torch.Tensor, kp_x: torch.Tensor, kp_y: torch.Tensor, kp_count
     dim = grid * grid * n_orient
     stride = DESC_STRIDE if dim <= DESC_STRIDE else int(math.ceil(dim / 32) * 32)
     nbytes = ctypes.c_size_t()
-    _lib.check(lib.rift2_describe_workspace_size(B, S, grid, n_orient, ctypes.byref(nbytes)), "describe")
+    _lib.check(lib.rift2_describe_workspace_size_hw(B, H, W, S, grid, n_orient, ctypes.byref(nbytes)), "describe")
     ws = WORKSPACES.get(ws_key, nbytes.value)
     dev = mim.device
     if out is None:

@@ -76,3 +76,44 @@ def test_integral_float64_keypoints_equal_int32_path(gold):
     assert n == int(b["count"][0]) and int(a["skipped"][0]) == int(b["skipped"][0])
     for k in ("counts", "sqnorm", "kp", "variant"):
         assert torch.equal(a[k][0, :n], b[k][0, :n]), k
+
+
+def test_preshift_workspace_equals_transform_path(gold):
+    # rift2_describe with the smaller workspace (in-kernel shift transform of
+    # the staged neighbourhood) and with the height/width-aware one (a
+    # shift-byte copy of the maps staged directly) give identical rows
+    import ctypes
+    from paper_2303_00319_b200 import _lib, engine
+    lib = _lib.load(require_gpu=True)
+    idx = torch.as_tensor(gold["o6_mim"].astype(np.uint8)).cuda()[None].contiguous()
+    _, H, W = idx.shape
+    xs = torch.as_tensor(np.floor(gold["kp_x"]), dtype=torch.int32).cuda()[None].contiguous()
+    ys = torch.as_tensor(np.floor(gold["kp_y"]), dtype=torch.int32).cuda()[None].contiguous()
+    S = xs.shape[1]
+    cnt = torch.tensor([S], dtype=torch.int32, device="cuda")
+    outs = []
+    for hw in (False, True):
+        n = ctypes.c_size_t()
+        if hw:
+            _lib.check(lib.rift2_describe_workspace_size_hw(1, H, W, S, 6, 6, ctypes.byref(n)), "ws")
+        else:
+            _lib.check(lib.rift2_describe_workspace_size(1, S, 6, 6, ctypes.byref(n)), "ws")
+        ws = torch.zeros(n.value, dtype=torch.uint8, device="cuda")
+        o = dict(counts=torch.zeros((1, 2 * S, 224), dtype=torch.float16, device="cuda"),
+                 sqnorm=torch.zeros((1, 2 * S), dtype=torch.int32, device="cuda"),
+                 kp=torch.zeros((1, 2 * S), dtype=torch.int32, device="cuda"),
+                 variant=torch.zeros((1, 2 * S), dtype=torch.uint8, device="cuda"),
+                 count=torch.zeros((1,), dtype=torch.int32, device="cuda"),
+                 skipped=torch.zeros((1,), dtype=torch.int32, device="cuda"))
+        p = engine._ptr
+        rc = lib.rift2_describe(p(idx), 1, H, W, 6, p(xs), p(ys), p(cnt), S, 96, 6, 0.8, 1, 2, p(o["counts"]), 224,
+                                2 * S, p(o["sqnorm"]), p(o["kp"]), p(o["variant"]), p(o["count"]), p(o["skipped"]),
+                                p(ws), ws.numel(), engine._stream())
+        _lib.check(rc, "rift2_describe")
+        outs.append(o)
+    torch.cuda.synchronize()
+    a, b = outs
+    n = int(a["count"][0])
+    assert n == int(b["count"][0]) and n > 0 and int(a["skipped"][0]) == int(b["skipped"][0])
+    for k in ("counts", "sqnorm", "kp", "variant"):
+        assert torch.equal(a[k][0, :n], b[k][0, :n]), k
