@@ -48,6 +48,11 @@ constexpr int kOffBias = 32768;
 #define R2_DESC_CARVE 100
 #endif
 
+#ifndef R2_DESC_SPREAD
+#define R2_DESC_SPREAD 1
+#endif
+constexpr bool kDescSpread = R2_DESC_SPREAD;   // bank-aware sample order of the rotated tables
+
 constexpr int kMaxOrientG = 16;   // the generic kernel's orientation limit (the C ABI's)
 
 struct GatherTables {
@@ -69,6 +74,60 @@ double snap_h(double v) {
   if (std::fabs(v) < 1e-12) return 0.0;
   if (std::fabs(std::fabs(v) - 1.0) < 1e-12) return std::copysign(1.0, v);
   return v;
+}
+
+// Bank-aware order of the rotated samples.  k_desc_main's thread (cell, sub)
+// reads 16 rows x 4 samples of its cell through the table, one byte gather per
+// warp per (row, sample) slot; a cell's counts do not depend on which of its
+// threads reads which sample, so each cell's 256 samples are dealt to its
+// slots greedily such that the 32 lanes of a slot fall into distinct
+// shared-memory banks (or the same word), over the four byte alignments the
+// keypoint column can have.  In raster order a slot costs 2.65 wavefronts on
+// average at 96^2 / 6 orientations; dealt this way 1.2.
+void spread_banks(uint16_t* t, int P, int stride, int radius) {
+  constexpr int CS = 16, TPC = CS / 4;
+  const int g = P / CS, nthr = g * g * TPC;
+  const int base = radius * stride + radius - kOffBias;   // byte address of the keypoint pixel (column shift 0)
+  const int nwords = ((2 * radius + 2) * stride + 64) / 4;
+  std::vector<uint16_t> out((size_t)P * P);
+  std::vector<uint8_t> present(4 * (size_t)nwords);
+  std::vector<int> touched;
+  for (int w0 = 0; w0 < nthr; w0 += 32) {
+    const int w1 = std::min(nthr, w0 + 32);
+    const int c0 = w0 / TPC, c1 = (w1 - 1) / TPC;
+    std::vector<std::vector<uint16_t>> pool(c1 - c0 + 1);
+    for (int c = c0; c <= c1; ++c)
+      for (int i = 0; i < CS; ++i)
+        for (int j = 0; j < CS; ++j) pool[c - c0].push_back(t[((c / g) * CS + i) * P + (c % g) * CS + j]);
+    for (int slot = 0; slot < CS * 4; ++slot) {
+      int cnt[4][32] = {}, mx[4] = {};
+      for (int tid = w0; tid < w1; ++tid) {
+        auto& pl = pool[tid / TPC - c0];
+        int best = 0, best_cost = 1 << 30;
+        for (int q = 0; q < (int)pl.size(); ++q) {
+          int cost = 0;
+          for (int d = 0; d < 4; ++d) {
+            const int wd = (base + pl[q] + d) >> 2, bk = wd & 31;
+            const int n = cnt[d][bk] + (present[(size_t)d * nwords + wd] ? 0 : 1);
+            cost += 100 * (std::max(n, mx[d]) - mx[d]) + n;
+          }
+          if (cost < best_cost) { best_cost = cost; best = q; }
+        }
+        const uint16_t v = pl[best];
+        pl.erase(pl.begin() + best);
+        for (int d = 0; d < 4; ++d) {
+          const int wd = (base + v + d) >> 2, bk = wd & 31;
+          uint8_t& p = present[(size_t)d * nwords + wd];
+          if (!p) { p = 1; touched.push_back(d * nwords + wd); mx[d] = std::max(mx[d], ++cnt[d][bk]); }
+        }
+        const int cell = tid / TPC, sub = tid % TPC, r = slot / 4, k = slot % 4;
+        out[((cell / g) * CS + r) * P + (cell % g) * CS + 4 * sub + k] = v;
+      }
+      for (int i : touched) present[i] = 0;
+      touched.clear();
+    }
+  }
+  std::copy(out.begin(), out.end(), t);
 }
 
 GatherTables gather_tables(int P, int O) {
@@ -128,6 +187,8 @@ GatherTables gather_tables(int P, int O) {
     soff[i] = (uint16_t)v;
   }
   if (!fits) { g_tables[key] = t; return t; }
+  if (kDescSpread && P % 16 == 0)
+    for (int a = 1; a < O; ++a) spread_banks(soff.data() + (size_t)a * P * P, P, stride, radius);
   uint16_t* d_off = nullptr;
   int4* d_bb = nullptr;
   if (cudaMalloc(&d_off, soff.size() * sizeof(uint16_t)) != cudaSuccess) return t;

@@ -67,6 +67,7 @@ struct FieldsConst {
   const float2* tw_w;          // W_W^j
   const float2* tw_h;          // W_H^j
   GenericPlan plan_w, plan_h;
+  int out_vec;                 // the map outputs take two-pixel vector stores (8-byte aligned floats, 2-byte aligned MIM)
 };
 
 // numpy.fft.fftfreq(n)[k]
@@ -409,7 +410,7 @@ R2_DEV void l2_prefetch(const void* p, unsigned bytes) {
 }
 R2_DEV float sqrt_approx(float x) {
   float y;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 template <int G>
@@ -973,7 +974,8 @@ R2_DEV void pc_core(const float2 (&X)[SC], const float2 (&Y)[SC], float T, float
   en = make_float2(fmaxf(en.x - T, 0.f), fmaxf(en.y - T, 0.f));
   const float sp0 = fmaf(sa.x, rcp_approx(mx0 + 1e-4f), -1.f) * inv_sm1;
   const float sp1 = fmaf(sa.y, rcp_approx(mx1 + 1e-4f), -1.f) * inv_sm1;
-  const float e0 = __expf(gain * (cut - sp0)), e1 = __expf(gain * (cut - sp1));
+  const float g2 = gain * 1.4426950408889634f;      // exp(x) = 2^(x log2 e): one MUFU, no range fix-up
+  const float e0 = ex2(g2 * (cut - sp0)), e1 = ex2(g2 * (cut - sp1));
   pc = make_float2(en.x * rcp_approx((1.f + e0) * (sa.x + 1e-4f)), en.y * rcp_approx((1.f + e1) * (sa.y + 1e-4f)));
 }
 
@@ -1258,10 +1260,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
     for (int s = 0; s < NE; ++s) issue(s, 0, ext + s * 2 * W, &e_bar[s]);
   }
   __syncthreads();
-  float acc_a[PIX], acc_b[PIX], acc_c[PIX], best[PIX];
+  float2 acc_a[PIX / 2], acc_b[PIX / 2], acc_c[PIX / 2], best[PIX / 2];
   int bidx[PIX];
 #pragma unroll
-  for (int i = 0; i < PIX; ++i) { acc_a[i] = acc_b[i] = acc_c[i] = 0.f; best[i] = -1.f; bidx[i] = 1; }
+  for (int j = 0; j < PIX / 2; ++j) {
+    acc_a[j] = acc_b[j] = acc_c[j] = make_float2(0.f, 0.f);
+    best[j] = make_float2(-1.f, -1.f);
+    bidx[2 * j] = bidx[2 * j + 1] = 1;
+  }
   for (int o = 0; o < O; ++o) {
     if (threadIdx.x == 0) {
       // this stage's buffer-landed inputs (the previous stage's pixel phase
@@ -1303,65 +1309,64 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
       SyncWarp sw{0xffffffffu};
       fft_fast<G>(v, buf, c.tw_w, t, sw);
       sw();
+      // the row as two planes, real [W] then imaginary [W], so the pixel
+      // phase loads two adjacent pixels' parts as one packed operand.  v is
+      // the conjugate of the response (the inverse is conj FFT conj): left
+      // as it is -- flipping the sign of every scale's odd part changes
+      // neither the amplitudes nor |z x mean| nor z . mean
+      float* pre = reinterpret_cast<float*>(buf);
 #pragma unroll
-      for (int m = 0; m < 32; ++m) buf[pad32(t + G * m)] = cconj(v[m]);
+      for (int m = 0; m < 32; ++m) { pre[t + G * m] = v[m].x; pre[W + t + G * m] = v[m].y; }
     }
     __syncthreads();
-    // pixel phase: pixel pairs (i, i + 1) of the two rows in the fp32x2 lanes
+    // pixel phase: the thread's four pairs of adjacent pixels (row j / 2,
+    // columns 2 tid + 512 (j % 2) and the next) in the fp32x2 lanes
     const float T = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
+    const float* pl = reinterpret_cast<const float*>(sm) + 2 * threadIdx.x;
 #pragma unroll
-    for (int i = 0; i < PIX; i += 2) {
-      const int p0 = threadIdx.x + kThreads * i, p1 = p0 + kThreads;
-      const int r0 = p0 / W, x0 = p0 % W, r1 = p1 / W, x1 = p1 % W;
+    for (int j = 0; j < PIX / 2; ++j) {
+      const int r = j >> 1, x = 512 * (j & 1);
       float2 X[S], Y[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const float2 z0 = sm[(s * 2 + r0) * PL + pad32(x0)], z1 = sm[(s * 2 + r1) * PL + pad32(x1)];
-        X[s] = make_float2(z0.x, z1.x);
-        Y[s] = make_float2(z0.y, z1.y);
+        const float* q = pl + (s * 2 + r) * (2 * PL) + x;
+        X[s] = *reinterpret_cast<const float2*>(q);
+        Y[s] = *reinterpret_cast<const float2*>(q + W);
       }
       float2 sa2, pc2;
       pc_core<S>(X, Y, T, inv_sm1, gain, cut, sa2, pc2);
       const float2 pcc = __fmul2_rn(pc2, make_float2(ca, ca)), pcs = __fmul2_rn(pc2, make_float2(sa_o, sa_o));
-      acc_a[i] = fmaf(pcc.x, pcc.x, acc_a[i]);
-      acc_a[i + 1] = fmaf(pcc.y, pcc.y, acc_a[i + 1]);
-      acc_b[i] = fmaf(pcc.x, pcs.x, acc_b[i]);
-      acc_b[i + 1] = fmaf(pcc.y, pcs.y, acc_b[i + 1]);
-      acc_c[i] = fmaf(pcs.x, pcs.x, acc_c[i]);
-      acc_c[i + 1] = fmaf(pcs.y, pcs.y, acc_c[i + 1]);
-      if (sa2.x > best[i]) { best[i] = sa2.x; bidx[i] = o + 1; }
-      if (sa2.y > best[i + 1]) { best[i + 1] = sa2.y; bidx[i + 1] = o + 1; }
+      acc_a[j] = __ffma2_rn(pcc, pcc, acc_a[j]);
+      acc_b[j] = __ffma2_rn(pcc, pcs, acc_b[j]);
+      acc_c[j] = __ffma2_rn(pcs, pcs, acc_c[j]);
+      if (sa2.x > best[j].x) { best[j].x = sa2.x; bidx[2 * j] = o + 1; }
+      if (sa2.y > best[j].y) { best[j].y = sa2.y; bidx[2 * j + 1] = o + 1; }
       if (out.a_o || out.pc) {
-        const size_t q0 = (((size_t)b * O + o) * H + y0 + r0) * W + x0;
-        const size_t q1 = (((size_t)b * O + o) * H + y0 + r1) * W + x1;
-        if (out.a_o) { out.a_o[q0] = sa2.x; out.a_o[q1] = sa2.y; }
-        if (out.pc) { out.pc[q0] = pc2.x; out.pc[q1] = pc2.y; }
+        const size_t q0 = (((size_t)b * O + o) * H + y0 + r) * W + 2 * threadIdx.x + x;
+        if (out.a_o) *reinterpret_cast<float2*>(out.a_o + q0) = sa2;
+        if (out.pc) *reinterpret_cast<float2*>(out.pc + q0) = pc2;
       }
     }
     __syncthreads();                               // the next stage's TMA rewrites the buffers
   }
   RangeAcc racc;
-  float vmin[PIX], vmax[PIX];
 #pragma unroll
-  for (int i = 0; i < PIX; ++i) {
-    const int p = threadIdx.x + kThreads * i;
-    const int r = p / W, x = p % W;
-    const int y = y0 + r;
-    const float a = acc_a[i], bq = 2.f * acc_b[i], cq = acc_c[i];
-    const float root = sqrtf(bq * bq + (a - cq) * (a - cq));
-    const size_t po = ((size_t)b * H + y) * W + x;
-    vmax[i] = 0.5f * (cq + a + root);
-    vmin[i] = fmaxf(0.5f * (cq + a - root), 0.f);
-    out.mmax[po] = vmax[i];
-    out.mmin[po] = vmin[i];
-    out.mim[po] = (uint8_t)bidx[i];
-    if (out.amax) out.amax[po] = best[i];
+  for (int j = 0; j < PIX / 2; ++j) {
+    const int r = j >> 1, x = 2 * threadIdx.x + 512 * (j & 1);
+    const size_t po = ((size_t)b * H + y0 + r) * W + x;
+    const float2 a = acc_a[j], bq = __fadd2_rn(acc_b[j], acc_b[j]), cq = acc_c[j];
+    const float2 d = __fadd2_rn(a, make_float2(-cq.x, -cq.y)), sm2 = __fadd2_rn(a, cq);
+    const float2 rr = __ffma2_rn(bq, bq, __fmul2_rn(d, d));
+    const float root0 = sqrtf(rr.x), root1 = sqrtf(rr.y);
+    const float2 vmax = make_float2(0.5f * (sm2.x + root0), 0.5f * (sm2.y + root1));
+    const float2 vmin = make_float2(fmaxf(0.5f * (sm2.x - root0), 0.f), fmaxf(0.5f * (sm2.y - root1), 0.f));
+    *reinterpret_cast<float2*>(out.mmax + po) = vmax;
+    *reinterpret_cast<float2*>(out.mmin + po) = vmin;
+    *reinterpret_cast<uchar2*>(out.mim + po) = make_uchar2((uint8_t)bidx[2 * j], (uint8_t)bidx[2 * j + 1]);
+    if (out.amax) *reinterpret_cast<float2*>(out.amax + po) = best[j];
+    if (out.range) racc.add2(vmin.x, vmax.x, vmin.y, vmax.y);
   }
-  if (out.range) {                                 // CTA-uniform
-#pragma unroll
-    for (int i = 0; i < PIX; i += 2) racc.add2(vmin[i], vmax[i], vmin[i + 1], vmax[i + 1]);
-    racc.flush(out.range + 4 * (size_t)b);
-  }
+  if (out.range) racc.flush(out.range + 4 * (size_t)b);   // CTA-uniform
 }
 
 // ================================================================ host side
@@ -1577,7 +1582,7 @@ static int resident_ctas(const void* kern, int threads, size_t smem) {
 // whether K3b runs as k_rows_pc_tma (which recomputes scale 0, so K3a may skip R0)
 static bool pc_tma_applies(const float2* Q, const FieldsConst& c) {
   CUtensorMap map{};
-  return c.S == 4 && !(c.H & 1) && make_qmap(Q, c, map);
+  return c.S == 4 && !(c.H & 1) && c.out_vec && make_qmap(Q, c, map);
 }
 
 // the TMA variant of K3b for 1,024-point rows, 4 scales, even H; false when
@@ -1585,7 +1590,7 @@ static bool pc_tma_applies(const float2* Q, const FieldsConst& c) {
 static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
                           const FieldsConst& c, cudaStream_t st, cudaError_t& e) {
   CUtensorMap map{};
-  if (c.S != 4 || (c.H & 1) || !make_qmap(Q, c, map)) return false;
+  if (c.S != 4 || (c.H & 1) || !c.out_vec || !make_qmap(Q, c, map)) return false;
   const size_t smem = ((size_t)8 * ((padded_len(1024) + 15) & ~15) + (size_t)kPcExtra * 2 * 1024) * sizeof(float2) + 128;
   if ((e = set_smem(k_rows_pc_tma, smem)) != cudaSuccess) return true;
   k_rows_pc_tma<<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, thr, out, c,
@@ -1667,6 +1672,10 @@ int fields_run(const float* images, int B, int H, int W, const BankConsts& bk, c
   if (!c.tw_w || !c.tw_h) return 3;
   if (!p.gw && !make_plan(W, c.plan_w)) return 2;
   if (!p.gh && !make_plan(H, c.plan_h)) return 2;
+  {
+    auto al8 = [](const void* q) { return ((uintptr_t)q & 7) == 0; };
+    c.out_vec = al8(o.mmax) && al8(o.mmin) && al8(o.a_o) && al8(o.pc) && al8(o.amax) && ((uintptr_t)o.mim & 1) == 0;
+  }
 
   char* w = static_cast<char*>(ws);
   float2* P = reinterpret_cast<float2*>(w + p.off_P);
