@@ -496,6 +496,10 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
 // row pairs arrive as 3-D boxes {2 rows of a 4-row column tile, 256 columns}
 // in the FFT buffers of the pair's two groups (128-byte pitch), so the
 // groups read their rows from shared memory; otherwise as k_rows_amp0<32>.
+#ifndef R2_AMP_TILE
+#define R2_AMP_TILE 1
+#endif
+constexpr bool kAmpTile = R2_AMP_TILE;   // K3a stages whole 4-row tile rows (bulk copies) instead of 2-row boxes
 __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constant__ CUtensorMap qmap,
                                                             const float2* __restrict__ Q, float2* __restrict__ R0,
                                                             float* __restrict__ amp0, unsigned* __restrict__ hist,
@@ -525,6 +529,14 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constan
   for (int yg = y_lo; yg < yend; yg += NG, ++it) {
     if (threadIdx.x == 0) {
       fence_proxy_async();                         // the previous group's buffers are free (barrier below)
+      if constexpr (kAmpTile) {
+        // whole 4-row tile rows (32 KB contiguous: one bulk copy, every byte used)
+        for (int p = 0; p < NG / 4; ++p) {
+          const int z = (b * F + o) * (c.Hp >> 2) + ((yg + 4 * p) >> 2);
+          mbar_expect_tx(&s_bar[p], (uint32_t)(4 * W * sizeof(float2)));
+          bulk_load(sm + 4 * p * PL, Q + (size_t)z * 4 * W, (uint32_t)(4 * W * sizeof(float2)), &s_bar[p]);
+        }
+      } else
       for (int p = 0; p < NG / 2; ++p) {
         const int y = yg + 2 * p;
         const int z = (b * F + o) * (c.Hp >> 2) + (y >> 2);
@@ -544,13 +556,14 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0_tma(const __grid_constan
         }
       }
     }
-    mbar_wait(&s_bar[g >> 1], (uint32_t)(it & 1));
+    constexpr int RT = kAmpTile ? 4 : 2;           // rows staged together
+    mbar_wait(&s_bar[g / RT], (uint32_t)(it & 1));
     const int y = yg + g;
-    const float2* st = sm + (g & ~1) * PL;         // [x][row] of the pair (g & ~1, g | 1)
+    const float2* st = sm + (g & ~(RT - 1)) * PL;  // [x][row] of the RT rows staged with this one
     float2 v[32];
 #pragma unroll
-    for (int m = 0; m < 32; ++m) v[m] = cconj(st[2 * (t + 32 * m) + (g & 1)]);
-    SyncNamed pair{8 + (g >> 1), 2 * G};           // both rows read before the FFT reuses the staging
+    for (int m = 0; m < 32; ++m) v[m] = cconj(st[RT * (t + 32 * m) + (g & (RT - 1))]);
+    SyncNamed pair{8 + g / RT, RT * G};            // all rows read before the FFT reuses the staging
     pair();
     SyncWarp sw{0xffffffffu};
     fft_fast<G>(v, buf, c.tw_w, t, sw);
@@ -1226,31 +1239,46 @@ constexpr int kPcExtra = R2_PC_EXTRA;
 #define R2_PC_DIST 1
 #endif
 constexpr int kPcDist = R2_PC_DIST;   // L2 prefetch distance in stages (0: none)
-__global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_constant__ CUtensorMap qmap,
+#ifndef R2_PC_PARISSUE
+#define R2_PC_PARISSUE 0
+#endif
+constexpr bool kPcParIssue = R2_PC_PARISSUE;   // each scale's TMA loads issued by its own first FFT warp
+#ifndef R2_PC_ROWS
+#define R2_PC_ROWS 2
+#endif
+constexpr int kPcRows = R2_PC_ROWS;   // rows per CTA: 2 (two CTAs per SM) or 4 (whole column tiles, one CTA per SM)
+template <int R>
+__global__ void __launch_bounds__(128 * R, R == 2 ? 2 : 1) k_rows_pc_tma(const __grid_constant__ CUtensorMap qmap,
                                                              const float2* __restrict__ Q,
                                                              const float* __restrict__ thr, PcOut out,
                                                              const __grid_constant__ FieldsConst c, int ahead) {
   // buffer pitch rounded to 128 bytes: TMA destinations must be 128-byte aligned
-  constexpr int G = 32, S = 4, W = 1024, PL = (padded_len(W) + 15) & ~15, PIX = 8, NE = kPcExtra;
+  constexpr int G = 32, S = 4, W = 1024, PL = (padded_len(W) + 15) & ~15, PIX = 8, NE = R == 2 ? kPcExtra : 0;
+  constexpr int T = 128 * R;                      // one warp per (scale, row)
   extern __shared__ float2 sm_raw[];
   __shared__ uint64_t s_bar[4];                   // one per scale: its FFT warps start on their own rows
   __shared__ uint64_t e_bar[NE > 0 ? NE : 1];     // one per extra staging slot
   float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
-  float2* ext = sm + 8 * PL;                      // [NE][2 W] staging slots, [x][row]
+  float2* ext = sm + S * R * PL;                  // [NE][2 W] staging slots, [x][row]
   const int H = c.H, O = c.O, F = S * O;
-  const int b = blockIdx.y, y0 = 2 * blockIdx.x;
+  const int b = blockIdx.y, y0 = R * blockIdx.x;
   const float* thr_b = thr + (size_t)b * O;
   const float inv_sm1 = c.inv_sm1, gain = c.spread_gain, cut = c.spread_cutoff;
   const int g = threadIdx.x / G, t = threadIdx.x % G;
-  // the two rows of scale s, orientation o as W / 256 boxes into dst
+  // the CTA's rows of scale s, orientation o into dst as [x][row]: W / 256
+  // boxes of two rows, or the whole 4-row tile row (contiguous: one bulk copy)
   auto issue = [&](int s, int o, float2* dst, uint64_t* bar) {
 #ifdef R2_EXP_NOLOAD
     return;                                        // timing experiment: compute on stale shared memory
 #endif
     const int z = (b * F + s * O + o) * (c.Hp >> 2) + (y0 >> 2);
-    mbar_expect_tx(bar, (uint32_t)(2 * W * sizeof(float2)));
-    for (int k = 0; k < W / kPcTmaBox; ++k)
-      tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, bar);
+    mbar_expect_tx(bar, (uint32_t)(R * W * sizeof(float2)));
+    if constexpr (R == 4) {
+      bulk_load(dst, Q + (size_t)z * 4 * W, (uint32_t)(4 * W * sizeof(float2)), bar);
+    } else {
+      for (int k = 0; k < W / kPcTmaBox; ++k)
+        tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, bar);
+    }
   };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(&qmap) : "memory");
@@ -1269,19 +1297,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
     bidx[2 * j] = bidx[2 * j + 1] = 1;
   }
   for (int o = 0; o < O; ++o) {
-    if (threadIdx.x == 0) {
-      // this stage's buffer-landed inputs (the previous stage's pixel phase
-      // is done with the buffers: the barrier at the end of the loop, then
-      // the proxy fence)
+    // this stage's inputs land in the buffers (the previous stage's pixel
+    // phase is done with them: the barrier at the end of the loop, then the
+    // proxy fence); each scale's loads are issued by its own first FFT warp,
+    // so the four issue sequences run side by side
+    if (kPcParIssue ? (t == 0 && g % R == 0 && g / R >= NE) : threadIdx.x == 0) {
       fence_proxy_async();
-      for (int s = NE; s < S; ++s) issue(s, o, sm + s * 2 * PL, &s_bar[s]);
-      // and stage o + kPcDist (or, past the last stage, that stage of the CTA
+      if (kPcParIssue) issue(g / R, o, sm + (g / R) * R * PL, &s_bar[g / R]);
+      else for (int s = NE; s < S; ++s) issue(s, o, sm + s * R * PL, &s_bar[s]);
+    }
+    if (threadIdx.x == (kPcParIssue ? G : 0)) {
+      // stage o + kPcDist (or, past the last stage, that stage of the CTA
       // one resident wave later) into L2
       int pb = b, py = y0, o1 = o + kPcDist;
       bool go = o1 < O;
       if (!go && ahead > 0) {
         const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + ahead;
-        if (lin < (long long)gridDim.x * gridDim.y) { pb = (int)(lin / gridDim.x); py = 2 * (int)(lin % gridDim.x); o1 -= O; go = true; }
+        if (lin < (long long)gridDim.x * gridDim.y) { pb = (int)(lin / gridDim.x); py = R * (int)(lin % gridDim.x); o1 -= O; go = true; }
       }
       if (go && kPcDist > 0) {
         const float2* pQ = Q + (size_t)pb * F * c.Hp * W;
@@ -1289,23 +1321,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
           l2_prefetch(pQ + ((size_t)(s * O + o1) * c.Hp + (py & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
       }
     }
-    {                                              // eight FFT warps: scale g / 2 (0 included), row g % 2
-      const int s = g >> 1, r = g & 1;
+    {                                              // 4 R FFT warps: scale g / R (0 included), row g % R
+      const int s = g / R, r = g % R;
       const bool staged = s < NE;
 #ifndef R2_EXP_NOLOAD
       mbar_wait(staged ? &e_bar[s] : &s_bar[s], (uint32_t)(o & 1));
 #endif
-      const float2* st = staged ? ext + s * 2 * W : sm + s * 2 * PL;   // [x][row]
+      const float2* st = staged ? ext + s * 2 * W : sm + s * R * PL;   // [x][row]
       float2 v[32];
 #pragma unroll
-      for (int m = 0; m < 32; ++m) v[m] = cconj(st[2 * (t + 32 * m) + r]);
-      SyncNamed pair{8 + s, 2 * G};                // both rows read before the slot / buffers are reused
-      pair();
+      for (int m = 0; m < 32; ++m) v[m] = cconj(st[R * (t + 32 * m) + r]);
+      SyncNamed grp{8 + s, R * G};                 // all rows read before the slot / buffers are reused
+      grp();
       if (staged && r == 0 && t == 0 && o + 1 < O) {
         fence_proxy_async();                       // the slot's generic reads precede the async refill
         issue(s, o + 1, ext + s * 2 * W, &e_bar[s]);
       }
-      float2* buf = sm + (s * 2 + r) * PL;
+      float2* buf = sm + (s * R + r) * PL;
       SyncWarp sw{0xffffffffu};
       fft_fast<G>(v, buf, c.tw_w, t, sw);
       sw();
@@ -1319,22 +1351,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
       for (int m = 0; m < 32; ++m) { pre[t + G * m] = v[m].x; pre[W + t + G * m] = v[m].y; }
     }
     __syncthreads();
-    // pixel phase: the thread's four pairs of adjacent pixels (row j / 2,
-    // columns 2 tid + 512 (j % 2) and the next) in the fp32x2 lanes
-    const float T = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
+    // pixel phase: the thread's four pairs of adjacent pixels (pair j at
+    // linear pixel 2 tid + 2 T j of the CTA's R rows) in the fp32x2 lanes
+    const float T_o = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
     const float* pl = reinterpret_cast<const float*>(sm) + 2 * threadIdx.x;
 #pragma unroll
     for (int j = 0; j < PIX / 2; ++j) {
-      const int r = j >> 1, x = 512 * (j & 1);
+      const int r = (2 * T * j) / W, x = (2 * T * j) % W;
       float2 X[S], Y[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const float* q = pl + (s * 2 + r) * (2 * PL) + x;
+        const float* q = pl + (s * R + r) * (2 * PL) + x;
         X[s] = *reinterpret_cast<const float2*>(q);
         Y[s] = *reinterpret_cast<const float2*>(q + W);
       }
       float2 sa2, pc2;
-      pc_core<S>(X, Y, T, inv_sm1, gain, cut, sa2, pc2);
+      pc_core<S>(X, Y, T_o, inv_sm1, gain, cut, sa2, pc2);
       const float2 pcc = __fmul2_rn(pc2, make_float2(ca, ca)), pcs = __fmul2_rn(pc2, make_float2(sa_o, sa_o));
       acc_a[j] = __ffma2_rn(pcc, pcc, acc_a[j]);
       acc_b[j] = __ffma2_rn(pcc, pcs, acc_b[j]);
@@ -1352,7 +1384,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rows_pc_tma(const __grid_consta
   RangeAcc racc;
 #pragma unroll
   for (int j = 0; j < PIX / 2; ++j) {
-    const int r = j >> 1, x = 2 * threadIdx.x + 512 * (j & 1);
+    const int r = (2 * T * j) / W, x = 2 * threadIdx.x + (2 * T * j) % W;
     const size_t po = ((size_t)b * H + y0 + r) * W + x;
     const float2 a = acc_a[j], bq = __fadd2_rn(acc_b[j], acc_b[j]), cq = acc_c[j];
     const float2 d = __fadd2_rn(a, make_float2(-cq.x, -cq.y)), sm2 = __fadd2_rn(a, cq);
@@ -1591,10 +1623,19 @@ static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, c
                           const FieldsConst& c, cudaStream_t st, cudaError_t& e) {
   CUtensorMap map{};
   if (c.S != 4 || (c.H & 1) || !c.out_vec || !make_qmap(Q, c, map)) return false;
-  const size_t smem = ((size_t)8 * ((padded_len(1024) + 15) & ~15) + (size_t)kPcExtra * 2 * 1024) * sizeof(float2) + 128;
-  if ((e = set_smem(k_rows_pc_tma, smem)) != cudaSuccess) return true;
-  k_rows_pc_tma<<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, thr, out, c,
-                                                            resident_ctas((const void*)k_rows_pc_tma, kThreads, smem));
+  const size_t pl = ((padded_len(1024) + 15) & ~15) * sizeof(float2);
+  if (kPcRows == 4 && c.H % 4 == 0) {
+    const size_t smem = 16 * pl + 128;
+    if ((e = set_smem(k_rows_pc_tma<4>, smem)) != cudaSuccess) return true;
+    k_rows_pc_tma<4><<<dim3(c.H / 4, c.B), 512, smem, st>>>(map, Q, thr, out, c,
+                                                             resident_ctas((const void*)k_rows_pc_tma<4>, 512, smem));
+    e = cudaPeekAtLastError();
+    return true;
+  }
+  const size_t smem = 8 * pl + (size_t)kPcExtra * 2 * 1024 * sizeof(float2) + 128;
+  if ((e = set_smem(k_rows_pc_tma<2>, smem)) != cudaSuccess) return true;
+  k_rows_pc_tma<2><<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, thr, out, c,
+                                                               resident_ctas((const void*)k_rows_pc_tma<2>, kThreads, smem));
   e = cudaPeekAtLastError();
   return true;
 }
