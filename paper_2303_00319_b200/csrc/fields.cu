@@ -416,7 +416,8 @@ R2_DEV float sqrt_approx(float x) {
 template <int G>
 __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict__ Q, float2* __restrict__ R0,
                                                         float* __restrict__ amp0, unsigned* __restrict__ hist,
-                                                        const __grid_constant__ FieldsConst c, int ahead) {
+                                                        const __grid_constant__ FieldsConst c, int ahead,
+                                                        int write_r0) {
   extern __shared__ float2 sm[];
   const int H = c.H, W = c.W, F = c.S * c.O;
   const int o = blockIdx.y, b = blockIdx.z;
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_amp0(const float2* __restrict
         const float2 z = cconj(v[m]);
         // MUFU sqrt: the median only needs amplitudes consistent with themselves
         const float a = sqrt_approx(fmaf(z.x, z.x, z.y * z.y));
-        Rp[(size_t)y * W + t + G * m] = z;
+        if (write_r0) Rp[(size_t)y * W + t + G * m] = z;   // not needed when K3b recomputes scale 0
         A[(size_t)y * W + t + G * m] = a;
         atomicAdd(&sh[__float_as_uint(a) >> 19], 1u);
       }
@@ -1223,122 +1224,113 @@ __global__ void __launch_bounds__(PcShape<G>::T, PcShape<G>::T == 512 ? 1 : 2) k
 // scale -- and all eight warps run one row FFT each: scale 0 is transformed
 // here again rather than read back from K3a, so K3a writes no R0 plane (1.6
 // GB per 32 images) and no warp idles in the FFT phase.  Buffers: scale s,
-// row r at s*2 + r (a scale's pair is contiguous: the staging of its boxes
-// as [x][row]).  The first kPcExtra scales are staged one whole stage ahead
-// in extra slots (the shared memory two CTAs per SM leave free): their TMA
-// for stage o+1 is issued as soon as stage o's FFT warps have read the slot,
-// so half of the warps start each stage without waiting for memory; the
-// other scales land in the buffers once the pixel phase has released them.
-// Same arithmetic as k_rows_pc, and bit-identical scale-0 responses (same
+// row r at s*R + r (a scale's rows are contiguous: the staging of its boxes
+// as [x][row]); after its FFT a warp leaves its row there as a real and an
+// imaginary plane.  The pixel phase first moves all of a thread's operands
+// (4 pixel pairs x 4 scales) into registers; one barrier later the buffers
+// are free, so the next stage's loads are issued *before* the pixel
+// arithmetic and land while it runs (kPcEarly) instead of after it.
+// Same arithmetic as k_rows_pc, and bit-identical scale-0 amplitudes (same
 // FFT, same input).
-#ifndef R2_PC_EXTRA
-#define R2_PC_EXTRA 0
-#endif
-constexpr int kPcExtra = R2_PC_EXTRA;
 #ifndef R2_PC_DIST
 #define R2_PC_DIST 1
 #endif
 constexpr int kPcDist = R2_PC_DIST;   // L2 prefetch distance in stages (0: none)
-#ifndef R2_PC_PARISSUE
-#define R2_PC_PARISSUE 0
+#ifndef R2_PC_EARLY
+#define R2_PC_EARLY 1
 #endif
-constexpr bool kPcParIssue = R2_PC_PARISSUE;   // each scale's TMA loads issued by its own first FFT warp
+constexpr bool kPcEarly = R2_PC_EARLY;
 #ifndef R2_PC_ROWS
 #define R2_PC_ROWS 2
 #endif
 constexpr int kPcRows = R2_PC_ROWS;   // rows per CTA: 2 (two CTAs per SM) or 4 (whole column tiles, one CTA per SM)
-template <int R>
-__global__ void __launch_bounds__(128 * R, R == 2 ? 2 : 1) k_rows_pc_tma(const __grid_constant__ CUtensorMap qmap,
+// Instances: 1,024-point rows with R = 2 (two CTAs per SM; R = 4 measured
+// slower: one CTA per SM runs its two phases in lockstep) and 512-point rows
+// with R = 4 (whole tiles, 16 half-warp FFTs).
+template <int R, int W>
+__global__ void __launch_bounds__(4 * R * (W / 32), R * W == 2048 ? 2 : 1) k_rows_pc_tma(const __grid_constant__ CUtensorMap qmap,
                                                              const float2* __restrict__ Q,
                                                              const float* __restrict__ thr, PcOut out,
                                                              const __grid_constant__ FieldsConst c, int ahead) {
   // buffer pitch rounded to 128 bytes: TMA destinations must be 128-byte aligned
-  constexpr int G = 32, S = 4, W = 1024, PL = (padded_len(W) + 15) & ~15, PIX = 8, NE = R == 2 ? kPcExtra : 0;
-  constexpr int T = 128 * R;                      // one warp per (scale, row)
+  constexpr int G = W / 32, S = 4, PL = (padded_len(W) + 15) & ~15, PIX = 8, NP = PIX / 2;
+  constexpr int T = S * R * G;                    // G threads per (scale, row)
+  static_assert(R * W == PIX * T, "8 pixels per thread");
+  // plane offset of odd rows (floats, inside the pitch slack): two 16-thread
+  // groups of one warp then store to different banks
+  constexpr int POFF = G < 32 ? 16 : 0;
+  static_assert(2 * W + POFF <= 2 * PL, "planes fit the buffer");
   extern __shared__ float2 sm_raw[];
   __shared__ uint64_t s_bar[4];                   // one per scale: its FFT warps start on their own rows
-  __shared__ uint64_t e_bar[NE > 0 ? NE : 1];     // one per extra staging slot
   float2* sm = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm_raw) + ((128u - (smem_u32(sm_raw) & 127u)) & 127u));
-  float2* ext = sm + S * R * PL;                  // [NE][2 W] staging slots, [x][row]
   const int H = c.H, O = c.O, F = S * O;
   const int b = blockIdx.y, y0 = R * blockIdx.x;
   const float* thr_b = thr + (size_t)b * O;
   const float inv_sm1 = c.inv_sm1, gain = c.spread_gain, cut = c.spread_cutoff;
   const int g = threadIdx.x / G, t = threadIdx.x % G;
-  // the CTA's rows of scale s, orientation o into dst as [x][row]: W / 256
-  // boxes of two rows, or the whole 4-row tile row (contiguous: one bulk copy)
-  auto issue = [&](int s, int o, float2* dst, uint64_t* bar) {
-#ifdef R2_EXP_NOLOAD
-    return;                                        // timing experiment: compute on stale shared memory
+  // (thread 0) stage o: the CTA's rows of every scale into the buffers as
+  // [x][row] -- W / 256 boxes of two rows, or the whole 4-row tile row
+  // (contiguous: one bulk copy) -- and stage o + kPcDist (past the last stage:
+  // that stage of the CTA one resident wave later) into L2
+  auto issue_stage = [&](int o) {
+#ifndef R2_EXP_NOLOAD                              // timing experiment: compute on stale shared memory
+    fence_proxy_async();                           // earlier generic accesses of the buffers precede the async writes
+    for (int s = 0; s < S; ++s) {
+      const int z = (b * F + s * O + o) * (c.Hp >> 2) + (y0 >> 2);
+      float2* dst = sm + s * R * PL;
+      mbar_expect_tx(&s_bar[s], (uint32_t)(R * W * sizeof(float2)));
+      if constexpr (R == 4) {
+        bulk_load(dst, Q + (size_t)z * 4 * W, (uint32_t)(4 * W * sizeof(float2)), &s_bar[s]);
+      } else {
+        for (int k = 0; k < W / kPcTmaBox; ++k)
+          tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, &s_bar[s]);
+      }
+    }
 #endif
-    const int z = (b * F + s * O + o) * (c.Hp >> 2) + (y0 >> 2);
-    mbar_expect_tx(bar, (uint32_t)(R * W * sizeof(float2)));
-    if constexpr (R == 4) {
-      bulk_load(dst, Q + (size_t)z * 4 * W, (uint32_t)(4 * W * sizeof(float2)), bar);
-    } else {
-      for (int k = 0; k < W / kPcTmaBox; ++k)
-        tma_load_3d(dst + 2 * kPcTmaBox * k, &qmap, 2 * (y0 & 3), kPcTmaBox * k, z, bar);
+    int pb = b, py = y0, o1 = o + kPcDist;
+    bool go = o1 < O;
+    if (!go && ahead > 0) {
+      const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + ahead;
+      if (lin < (long long)gridDim.x * gridDim.y) { pb = (int)(lin / gridDim.x); py = R * (int)(lin % gridDim.x); o1 -= O; go = true; }
+    }
+    if (go && kPcDist > 0) {
+      const float2* pQ = Q + (size_t)pb * F * c.Hp * W;
+      for (int s = 0; s < S; ++s)
+        l2_prefetch(pQ + ((size_t)(s * O + o1) * c.Hp + (py & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
     }
   };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(&qmap) : "memory");
     for (int q = 0; q < 4; ++q) mbar_init(&s_bar[q], 1);
-    for (int q = 0; q < NE; ++q) mbar_init(&e_bar[q], 1);
     mbar_fence_init();
-    for (int s = 0; s < NE; ++s) issue(s, 0, ext + s * 2 * W, &e_bar[s]);
+    if (kPcEarly) issue_stage(0);
   }
   __syncthreads();
-  float2 acc_a[PIX / 2], acc_b[PIX / 2], acc_c[PIX / 2], best[PIX / 2];
+  float2 acc_a[NP], acc_b[NP], acc_c[NP], best[NP];
   int bidx[PIX];
 #pragma unroll
-  for (int j = 0; j < PIX / 2; ++j) {
+  for (int j = 0; j < NP; ++j) {
     acc_a[j] = acc_b[j] = acc_c[j] = make_float2(0.f, 0.f);
     best[j] = make_float2(-1.f, -1.f);
     bidx[2 * j] = bidx[2 * j + 1] = 1;
   }
   for (int o = 0; o < O; ++o) {
-    // this stage's inputs land in the buffers (the previous stage's pixel
-    // phase is done with them: the barrier at the end of the loop, then the
-    // proxy fence); each scale's loads are issued by its own first FFT warp,
-    // so the four issue sequences run side by side
-    if (kPcParIssue ? (t == 0 && g % R == 0 && g / R >= NE) : threadIdx.x == 0) {
-      fence_proxy_async();
-      if (kPcParIssue) issue(g / R, o, sm + (g / R) * R * PL, &s_bar[g / R]);
-      else for (int s = NE; s < S; ++s) issue(s, o, sm + s * R * PL, &s_bar[s]);
-    }
-    if (threadIdx.x == (kPcParIssue ? G : 0)) {
-      // stage o + kPcDist (or, past the last stage, that stage of the CTA
-      // one resident wave later) into L2
-      int pb = b, py = y0, o1 = o + kPcDist;
-      bool go = o1 < O;
-      if (!go && ahead > 0) {
-        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + ahead;
-        if (lin < (long long)gridDim.x * gridDim.y) { pb = (int)(lin / gridDim.x); py = R * (int)(lin % gridDim.x); o1 -= O; go = true; }
-      }
-      if (go && kPcDist > 0) {
-        const float2* pQ = Q + (size_t)pb * F * c.Hp * W;
-        for (int s = (o1 == 0 ? 0 : NE); s < S; ++s)
-          l2_prefetch(pQ + ((size_t)(s * O + o1) * c.Hp + (py & ~3)) * W, (unsigned)(4 * W * sizeof(float2)));
-      }
-    }
+    // (late issue: the previous stage's pixel phase is done with the buffers,
+    // the barrier at the end of the loop)
+    if (!kPcEarly && threadIdx.x == 0) issue_stage(o);
     {                                              // 4 R FFT warps: scale g / R (0 included), row g % R
       const int s = g / R, r = g % R;
-      const bool staged = s < NE;
 #ifndef R2_EXP_NOLOAD
-      mbar_wait(staged ? &e_bar[s] : &s_bar[s], (uint32_t)(o & 1));
+      mbar_wait(&s_bar[s], (uint32_t)(o & 1));
 #endif
-      const float2* st = staged ? ext + s * 2 * W : sm + s * R * PL;   // [x][row]
+      const float2* st = sm + s * R * PL;          // [x][row]
       float2 v[32];
 #pragma unroll
-      for (int m = 0; m < 32; ++m) v[m] = cconj(st[R * (t + 32 * m) + r]);
-      SyncNamed grp{8 + s, R * G};                 // all rows read before the slot / buffers are reused
+      for (int m = 0; m < 32; ++m) v[m] = cconj(st[R * (t + G * m) + r]);
+      SyncNamed grp{8 + s, R * G};                 // all rows read before the buffers are reused
       grp();
-      if (staged && r == 0 && t == 0 && o + 1 < O) {
-        fence_proxy_async();                       // the slot's generic reads precede the async refill
-        issue(s, o + 1, ext + s * 2 * W, &e_bar[s]);
-      }
       float2* buf = sm + (s * R + r) * PL;
-      SyncWarp sw{0xffffffffu};
+      SyncWarp sw{group_mask(G)};
       fft_fast<G>(v, buf, c.tw_w, t, sw);
       sw();
       // the row as two planes, real [W] then imaginary [W], so the pixel
@@ -1346,7 +1338,7 @@ __global__ void __launch_bounds__(128 * R, R == 2 ? 2 : 1) k_rows_pc_tma(const _
       // the conjugate of the response (the inverse is conj FFT conj): left
       // as it is -- flipping the sign of every scale's odd part changes
       // neither the amplitudes nor |z x mean| nor z . mean
-      float* pre = reinterpret_cast<float*>(buf);
+      float* pre = reinterpret_cast<float*>(buf) + (r & 1) * POFF;
 #pragma unroll
       for (int m = 0; m < 32; ++m) { pre[t + G * m] = v[m].x; pre[W + t + G * m] = v[m].y; }
     }
@@ -1355,18 +1347,28 @@ __global__ void __launch_bounds__(128 * R, R == 2 ? 2 : 1) k_rows_pc_tma(const _
     // linear pixel 2 tid + 2 T j of the CTA's R rows) in the fp32x2 lanes
     const float T_o = thr_b[o], ca = c.cos_a[o], sa_o = c.sin_a[o];
     const float* pl = reinterpret_cast<const float*>(sm) + 2 * threadIdx.x;
-#pragma unroll
-    for (int j = 0; j < PIX / 2; ++j) {
+    float2 X[NP][S], Y[NP][S];
+    auto load_pair = [&](int j) {
       const int r = (2 * T * j) / W, x = (2 * T * j) % W;
-      float2 X[S], Y[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const float* q = pl + (s * R + r) * (2 * PL) + x;
-        X[s] = *reinterpret_cast<const float2*>(q);
-        Y[s] = *reinterpret_cast<const float2*>(q + W);
+        const float* q = pl + (s * R + r) * (2 * PL) + (r & 1) * POFF + x;
+        X[j][s] = *reinterpret_cast<const float2*>(q);
+        Y[j][s] = *reinterpret_cast<const float2*>(q + W);
       }
+    };
+    if (kPcEarly) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) load_pair(j);
+      __syncthreads();                             // every operand is in registers: the buffers are free
+      if (threadIdx.x == 0 && o + 1 < O) issue_stage(o + 1);
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const int r = (2 * T * j) / W, x = (2 * T * j) % W;
+      if (!kPcEarly) load_pair(j);
       float2 sa2, pc2;
-      pc_core<S>(X, Y, T_o, inv_sm1, gain, cut, sa2, pc2);
+      pc_core<S>(X[j], Y[j], T_o, inv_sm1, gain, cut, sa2, pc2);
       const float2 pcc = __fmul2_rn(pc2, make_float2(ca, ca)), pcs = __fmul2_rn(pc2, make_float2(sa_o, sa_o));
       acc_a[j] = __ffma2_rn(pcc, pcc, acc_a[j]);
       acc_b[j] = __ffma2_rn(pcc, pcs, acc_b[j]);
@@ -1379,11 +1381,11 @@ __global__ void __launch_bounds__(128 * R, R == 2 ? 2 : 1) k_rows_pc_tma(const _
         if (out.pc) *reinterpret_cast<float2*>(out.pc + q0) = pc2;
       }
     }
-    __syncthreads();                               // the next stage's TMA rewrites the buffers
+    if (!kPcEarly) __syncthreads();                // the next stage's TMA rewrites the buffers
   }
   RangeAcc racc;
 #pragma unroll
-  for (int j = 0; j < PIX / 2; ++j) {
+  for (int j = 0; j < NP; ++j) {
     const int r = (2 * T * j) / W, x = 2 * threadIdx.x + (2 * T * j) % W;
     const size_t po = ((size_t)b * H + y0 + r) * W + x;
     const float2 a = acc_a[j], bq = __fadd2_rn(acc_b[j], acc_b[j]), cq = acc_c[j];
@@ -1526,6 +1528,7 @@ static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c,
   return cudaPeekAtLastError();
 }
 
+static bool pc_tma_applies(const float2* Q, const FieldsConst& c);
 static bool launch_amp0_tma(const float2* Q, float2* R0, float* amp0, unsigned* hist, const FieldsConst& c,
                             cudaStream_t st, cudaError_t& e);
 
@@ -1552,7 +1555,8 @@ static cudaError_t launch_amp0(const float2* Q, float2* R0, float* amp0, unsigne
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_amp0<G>, kThreads, smem);
-  k_rows_amp0<G><<<grid, kThreads, smem, st>>>(Q, R0, amp0, hist, c, per_sm * n_sm);
+  k_rows_amp0<G><<<grid, kThreads, smem, st>>>(Q, R0, amp0, hist, c, per_sm * n_sm,
+                                               (G > 0 && pc_tma_applies(Q, c)) ? 0 : 1);
   return cudaPeekAtLastError();
 }
 
@@ -1611,32 +1615,39 @@ static int resident_ctas(const void* kern, int threads, size_t smem) {
   return per_sm * n_sm;
 }
 
-// whether K3b runs as k_rows_pc_tma (which recomputes scale 0, so K3a may skip R0)
+// whether K3b runs as k_rows_pc_tma (which recomputes scale 0, so K3a may skip R0):
+// 1,024-point rows (2-row boxes through the tensor map) or 512-point rows
+// (whole tile rows by bulk copies), 4 scales, two-pixel vector stores
 static bool pc_tma_applies(const float2* Q, const FieldsConst& c) {
+  if (!kPcTma || c.S != 4 || !c.out_vec || ((uintptr_t)Q & 15)) return false;
+  if (c.W == 512) return c.H % 4 == 0;
   CUtensorMap map{};
-  return c.S == 4 && !(c.H & 1) && c.out_vec && make_qmap(Q, c, map);
+  return c.W == 1024 && !(c.H & 1) && make_qmap(Q, c, map);
 }
 
-// the TMA variant of K3b for 1,024-point rows, 4 scales, even H; false when
-// it does not apply (or the tensor map cannot be encoded)
+template <int R, int W>
+static cudaError_t launch_pc_tma_rw(const CUtensorMap& map, const float2* Q, const float* thr, const PcOut& out,
+                                    const FieldsConst& c, cudaStream_t st) {
+  constexpr int T = 4 * R * (W / 32);
+  const size_t smem = (size_t)4 * R * ((padded_len(W) + 15) & ~15) * sizeof(float2) + 128;
+  cudaError_t e = set_smem(k_rows_pc_tma<R, W>, smem);
+  if (e != cudaSuccess) return e;
+  k_rows_pc_tma<R, W><<<dim3(c.H / R, c.B), T, smem, st>>>(map, Q, thr, out, c,
+                                                           resident_ctas((const void*)k_rows_pc_tma<R, W>, T, smem));
+  return cudaPeekAtLastError();
+}
+
+// the TMA variant of K3b; false when it does not apply (or the tensor map
+// cannot be encoded)
 static bool launch_pc_tma(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
                           const FieldsConst& c, cudaStream_t st, cudaError_t& e) {
+  (void)R0;
+  if (!pc_tma_applies(Q, c)) return false;
   CUtensorMap map{};
-  if (c.S != 4 || (c.H & 1) || !c.out_vec || !make_qmap(Q, c, map)) return false;
-  const size_t pl = ((padded_len(1024) + 15) & ~15) * sizeof(float2);
-  if (kPcRows == 4 && c.H % 4 == 0) {
-    const size_t smem = 16 * pl + 128;
-    if ((e = set_smem(k_rows_pc_tma<4>, smem)) != cudaSuccess) return true;
-    k_rows_pc_tma<4><<<dim3(c.H / 4, c.B), 512, smem, st>>>(map, Q, thr, out, c,
-                                                             resident_ctas((const void*)k_rows_pc_tma<4>, 512, smem));
-    e = cudaPeekAtLastError();
-    return true;
-  }
-  const size_t smem = 8 * pl + (size_t)kPcExtra * 2 * 1024 * sizeof(float2) + 128;
-  if ((e = set_smem(k_rows_pc_tma<2>, smem)) != cudaSuccess) return true;
-  k_rows_pc_tma<2><<<dim3(c.H / 2, c.B), kThreads, smem, st>>>(map, Q, thr, out, c,
-                                                               resident_ctas((const void*)k_rows_pc_tma<2>, kThreads, smem));
-  e = cudaPeekAtLastError();
+  if (c.W == 512) { e = launch_pc_tma_rw<4, 512>(map, Q, thr, out, c, st); return true; }
+  if (!make_qmap(Q, c, map)) return false;
+  if (kPcRows == 4 && c.H % 4 == 0) e = launch_pc_tma_rw<4, 1024>(map, Q, thr, out, c, st);
+  else e = launch_pc_tma_rw<2, 1024>(map, Q, thr, out, c, st);
   return true;
 }
 
@@ -1659,7 +1670,7 @@ static bool launch_amp0_tma(const float2* Q, float2* R0, float* amp0, unsigned* 
 template <int G>
 static cudaError_t launch_pc(const float2* Q, const float2* R0, const float* thr, const PcOut& out,
                              const FieldsConst& c, cudaStream_t st) {
-  if constexpr (G == 32) {
+  if constexpr (G == 32 || G == 16) {
     cudaError_t e = cudaSuccess;
     if (launch_pc_tma(Q, R0, thr, out, c, st, e)) return e;
   }
