@@ -99,9 +99,10 @@ class BatchPipeline:
         self.run_features()
 
     # our kernels per step: fields 10 (with the moment-range init) + detect 9
-    # (no k_minmax: the PC pass reduced the maps) + describe 2 (the shift-byte
-    # copy of the index maps, the per-keypoint kernel) + match 7
-    KERNELS_PER_STEP = 28
+    # (no k_minmax: the PC pass reduced the maps) + describe 3 (the shift-byte
+    # copy of the index maps, the dense cell sums, the per-keypoint kernel) +
+    # match 7
+    KERNELS_PER_STEP = 29
 
     # ---- graphs ------------------------------------------------------------
     def capture(self):

@@ -52,6 +52,10 @@ constexpr int kOffBias = 32768;
 #define R2_DESC_SPREAD 1
 #endif
 constexpr bool kDescSpread = R2_DESC_SPREAD;   // bank-aware sample order of the rotated tables
+#ifndef R2_DESC_DENSE
+#define R2_DESC_DENSE 1
+#endif
+constexpr bool kDescDense = R2_DESC_DENSE;     // axis-aligned patches from dense 16 x 16 cell sums
 
 constexpr int kMaxOrientG = 16;   // the generic kernel's orientation limit (the C ABI's)
 
@@ -209,6 +213,7 @@ struct DescConst {
   int R, stride, rows;   // staging radius, staged row bytes, staged rows (2R+1)
   int tma;               // stage the neighbourhood with one TMA box load
   int preshift;          // the TMA source already holds shift bytes 5(v-1) (k_mim_shift)
+  const uint2* dense;    // 16 x 16 cell sums of every pixel (k_cell_sums), or nullptr: count the axis patch
   int4 bbox[8];          // per-angle rotated-patch bounding boxes (dx_min, dx_max, dy_min, dy_max)
 };
 
@@ -297,6 +302,45 @@ R2_DEV void count_axis(const DescConst& c, const uint8_t* sreg, int off0, unsign
     }
   }
   reduce_cell<OT>(e, o, on && sub == 0, cnt + cell * O, O, sq, hist);
+}
+
+// axis-aligned patch from the dense cell sums: cell (cr, cc) of the patch at
+// (x0, y0) is the 16 x 16 window anchored at (x0 + 16 cc, y0 + 16 cr), whose
+// per-value counts k_cell_sums left as two words of 10-bit fields (the e / o
+// format of reduce_cell).  One thread per cell; warps 0 and 1 call this.
+template <int OT, int GT>
+R2_DEV void count_axis_dense(const DescConst& c, const uint2* __restrict__ cells, int x0, int y0, unsigned* cnt,
+                             int* sq, unsigned* hist) {
+  const int g = GT ? GT : c.g, O = OT ? OT : c.O;
+  const int t = threadIdx.x;
+  const bool on = t < g * g;
+  int q = 0;
+  uint32_t h01 = 0, h23 = 0, h45 = 0;
+  if (on) {
+    const int cr = t / g, cc = t % g;
+    const uint2 w = __ldg(cells + (size_t)(y0 + 16 * cr) * c.W + x0 + 16 * cc);
+    const uint32_t e = w.x, o = w.y;
+#pragma unroll
+    for (int v = 0; v < (OT ? OT : 8); ++v) {
+      if (!OT && v >= O) break;
+      const unsigned n = (((v & 1) ? o : e) >> (10 * (v >> 1))) & 1023u;
+      cnt[t * O + v] = n;
+      q += (int)(n * n);
+    }
+    h01 = (e & 1023u) | (o & 1023u) << 16;
+    h23 = ((e >> 10) & 1023u) | ((o >> 10) & 1023u) << 16;
+    h45 = ((e >> 20) & 1023u) | ((o >> 20) & 1023u) << 16;
+  }
+  q = __reduce_add_sync(0xffffffffu, q);
+  h01 = __reduce_add_sync(0xffffffffu, h01);
+  h23 = __reduce_add_sync(0xffffffffu, h23);
+  h45 = __reduce_add_sync(0xffffffffu, h45);
+  if ((t & 31) == 0) {
+    if (q) atomicAdd(sq, q);
+    if (h01) atomicAdd(&hist[0], h01);
+    if (h23) atomicAdd(&hist[1], h23);
+    if (h45) atomicAdd(&hist[2], h45);
+  }
 }
 
 // rotated patch of angle table t: sample (i, j) at ctr + t[i*P + j]
@@ -431,7 +475,9 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
     if (threadIdx.x < 8) s_hist[threadIdx.x] = 0;
     if (threadIdx.x == 0) { s_sq[0] = 0; s_sq[1] = 0; s_sq[2] = 0; }
     __syncthreads();
-    mbar_wait(&s_bar, 0);
+    // (with the dense cell sums the staged bytes are only needed by rotated
+    // picks: waited for below, once the picks are known)
+    if (!c.dense) mbar_wait(&s_bar, 0);
     uint4* q4 = reinterpret_cast<uint4*>(sw);
     if (!c.preshift)
     for (int i = threadIdx.x; i < c.rows * c.stride / 16; i += kT) {
@@ -479,7 +525,11 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   const int bx = x - ax0;                         // keypoint column within a staged row
   const uint8_t* ctr = sreg + c.R * c.stride + bx;   // keypoint pixel
   // ---- axis-aligned patch
-  count_axis<CS, OT, GT>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt, &s_sq[0], s_hist);
+  if (c.dense) {
+    if (threadIdx.x < 64) count_axis_dense<OT, GT>(c, c.dense + (size_t)b * c.H * c.W, x0, y0, cnt, &s_sq[0], s_hist);
+  } else {
+    count_axis<CS, OT, GT>(c, sreg + (c.R + y0 - y) * c.stride, bx + x0 - x, cnt, &s_sq[0], s_hist);
+  }
   __syncthreads();
   // ---- dominant index / runner-up (ref: mim.py:69-91), computed by every
   // thread from the 6-bin patch histogram (no extra barrier)
@@ -538,6 +588,14 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
   const bool rot_mode = mode == 2 && c.rotate;
   const int dom90 = (O % 2 == 0 && c.P % 2 == 0) ? O / 2 + 1 : -1;
   int nrot = 0;
+  bool need_rot = false;
+#pragma unroll
+  for (int q = 0; q < kMaxPick; ++q)
+    if (q < np && rot_mode && pick[q] != 1 && pick[q] != dom90) need_rot = true;
+  // the staged neighbourhood: every thread that gathers from it waits for the
+  // TMA box; a keypoint with no rotated pick never reads it, and thread 0
+  // alone sees the load land before the CTA gives its shared memory back
+  if (c.dense && need_rot) mbar_wait(&s_bar, 0);
 #pragma unroll
   for (int q = 0; q < kMaxPick; ++q) {
     if (q >= np) break;
@@ -595,6 +653,7 @@ __global__ void __launch_bounds__(kT) k_desc_main(const __grid_constant__ CUtens
     }
     if (rotated) ++r;
   }
+  if (c.dense && !need_rot && threadIdx.x == 0) mbar_wait(&s_bar, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -796,6 +855,69 @@ __global__ void __launch_bounds__(kTG) k_desc_generic(const uint8_t* __restrict_
   }
 }
 
+// Dense 16 x 16 cell sums: out[y][x] = per-value counts of the window
+// [y, y+16) x [x, x+16) of the index map, as two words of 10-bit fields
+// (values 1, 3, 5 in .x, values 2, 4, 6 in .y: the e / o words of
+// reduce_cell).  The axis-aligned patch of a keypoint is 36 such windows, so
+// k_desc_main reads 36 words instead of counting 9,216 pixels (the
+// keypoints' patches overlap ~44-fold at 5,000 keypoints per 1024^2 image).
+// Separable running sums per 64 x 64 tile over the shift-byte copy: two
+// threads per staged row slide a 16-wide window along x (5-bit fields), then
+// two threads per column slide 16 rows down (widened to the 10-bit fields).
+// Windows that leave the image are never read (ref: descriptor.py:196-198
+// skips those keypoints).
+constexpr int kCsT = 64, kCsH = 64, kCsIn = kCsT + 15, kCsInH = kCsH + 15;
+// six 5-bit fields (<= 16 per field) -> the e / o words of 10-bit fields
+R2_DEV void widen5(uint32_t x, uint32_t& e, uint32_t& o) {
+  e = x & 0x01f07c1fu;
+  o = (x >> 5) & 0x01f07c1fu;
+}
+// shb: the shift-byte copy of the index map (k_mim_shift): a pixel counts as 1 << byte
+__global__ void __launch_bounds__(128) k_cell_sums(const uint8_t* __restrict__ shb, uint2* __restrict__ out, int H, int W) {
+  __shared__ uint8_t in[kCsInH][84];          // 21-word pitch: a column of rows hits distinct banks
+  __shared__ uint32_t hs[kCsInH][kCsT + 1];   // horizontal 16-sums, 5-bit fields (odd pitch: conflict-free columns)
+  const int b = blockIdx.z, ty0 = blockIdx.y * kCsH, tx0 = blockIdx.x * kCsT;
+  const uint8_t* m = shb + (size_t)b * H * W;
+  for (int i = threadIdx.x; i < kCsInH * 20; i += 128) {      // 79 rows x 80 bytes as words
+    const int r = i / 20, q = i % 20;
+    const int y = ty0 + r, x = tx0 + 4 * q;
+    uint32_t v = 0;                           // beyond the map: only windows no descriptor reads
+    if (y < H) {
+      if (x + 3 < W && (W & 3) == 0) v = __ldg(reinterpret_cast<const uint32_t*>(m + (size_t)y * W + x));
+      else for (int e = 0; e < 4; ++e) if (x + e < W) v |= (uint32_t)m[(size_t)y * W + x + e] << (8 * e);
+    }
+    *reinterpret_cast<uint32_t*>(&in[r][4 * q]) = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * kCsInH; i += 128) {       // (staged row, half of its 64 windows)
+    const int r = i >> 1, x0 = (i & 1) * 32;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 15; ++j) acc += one_hot(in[r][x0 + j]);
+#pragma unroll 8
+    for (int x = x0; x < x0 + 32; ++x) {
+      acc += one_hot(in[r][x + 15]);
+      hs[r][x] = acc;
+      acc -= one_hot(in[r][x]);
+    }
+  }
+  __syncthreads();
+  {
+    const int x = threadIdx.x & 63, r0 = (threadIdx.x >> 6) * 32;   // two threads per column: 32 output rows each
+    uint32_t e = 0, o = 0, we, wo;
+#pragma unroll
+    for (int j = 0; j < 15; ++j) { widen5(hs[r0 + j][x], we, wo); e += we; o += wo; }
+#pragma unroll 8
+    for (int r = r0; r < r0 + 32; ++r) {
+      widen5(hs[r + 15][x], we, wo);
+      e += we; o += wo;
+      if (ty0 + r < H && tx0 + x < W) out[((size_t)b * H + ty0 + r) * W + tx0 + x] = make_uint2(e, o);
+      widen5(hs[r][x], we, wo);
+      e -= we; o -= wo;
+    }
+  }
+}
+
 // The index map as shift bytes 5(v-1) in one pass over the planes, so the
 // per-keypoint kernel stages them by TMA with no in-place transform of its
 // ~21 KB neighbourhood (that pass was a fifth of its shared-memory traffic).
@@ -841,8 +963,9 @@ size_t describe_workspace_bytes(int B, int kp_stride, int grid, int O) {
 }
 
 size_t describe_workspace_bytes_hw(int B, int H, int W, int kp_stride, int grid, int O) {
-  // + the shift-byte copy of the index maps (used when the workspace holds it)
-  return describe_workspace_bytes(B, kp_stride, grid, O) + al((size_t)B * H * W);
+  // + the shift-byte copy of the index maps and the dense 16 x 16 cell sums
+  // (each used when the workspace holds it)
+  return describe_workspace_bytes(B, kp_stride, grid, O) + al((size_t)B * H * W) + al((size_t)B * H * W * sizeof(uint2));
 }
 
 int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -911,6 +1034,12 @@ int describe_run(const uint8_t* mim, const DescribeArgs& a, void* ws, size_t ws_
           reinterpret_cast<const uint4*>(mim), reinterpret_cast<uint4*>(sh), n16);
       src = sh;
       c.preshift = 1;
+      // and the dense cell sums behind it (values 1..6 in 10-bit fields)
+      if (kDescDense && a.O <= 6 && ws_bytes >= p.total + al(n) + al(n * sizeof(uint2)) && a.H >= 16 && a.W >= 16) {
+        uint2* cs_out = reinterpret_cast<uint2*>(static_cast<uint8_t*>(ws) + p.total + al(n));
+        k_cell_sums<<<dim3((a.W + kCsT - 1) / kCsT, (a.H + kCsH - 1) / kCsH, a.B), 128, 0, st>>>(sh, cs_out, a.H, a.W);
+        c.dense = cs_out;
+      }
     }
     // 2-D view (W, B*H): rows outside one image read its neighbour (or zeros
     // at the ends) -- never sampled by an emitted descriptor, see above
