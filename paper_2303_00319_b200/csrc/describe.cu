@@ -17,6 +17,10 @@
 //                0xFF outside the image), so a sample counts as
 //                acc += 1 << s into six 5-bit fields.  Four threads share a
 //                cell (4 columns x cs rows each) and reduce with two shuffles.
+//                With the larger workspace the axis-aligned counts come
+//                instead from k_cell_sums (dense 16 x 16 window counts of
+//                every pixel, 36 loads per keypoint) and only keypoints
+//                with a rotated pick wait for the staged bytes.
 //                Then dominant index / runner-up (every thread, from the
 //                patch histogram), the rotated patch of each pick through a
 //                host-built offset table, recode (a per-cell permutation), and

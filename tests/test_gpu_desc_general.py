@@ -80,8 +80,9 @@ def test_integral_float64_keypoints_equal_int32_path(gold):
 
 def test_preshift_workspace_equals_transform_path(gold):
     # rift2_describe with the smaller workspace (in-kernel shift transform of
-    # the staged neighbourhood) and with the height/width-aware one (a
-    # shift-byte copy of the maps staged directly) give identical rows
+    # the staged neighbourhood), with room for the shift-byte copy of the maps
+    # only, and with the height/width-aware size (shift-byte copy + dense
+    # 16 x 16 cell sums for the axis-aligned patches) gives identical rows
     import ctypes
     from paper_2303_00319_b200 import _lib, engine
     lib = _lib.load(require_gpu=True)
@@ -92,13 +93,15 @@ def test_preshift_workspace_equals_transform_path(gold):
     S = xs.shape[1]
     cnt = torch.tensor([S], dtype=torch.int32, device="cuda")
     outs = []
-    for hw in (False, True):
-        n = ctypes.c_size_t()
-        if hw:
-            _lib.check(lib.rift2_describe_workspace_size_hw(1, H, W, S, 6, 6, ctypes.byref(n)), "ws")
-        else:
-            _lib.check(lib.rift2_describe_workspace_size(1, S, 6, 6, ctypes.byref(n)), "ws")
-        ws = torch.zeros(n.value, dtype=torch.uint8, device="cuda")
+    small, full = ctypes.c_size_t(), ctypes.c_size_t()
+    _lib.check(lib.rift2_describe_workspace_size(1, S, 6, 6, ctypes.byref(small)), "ws")
+    _lib.check(lib.rift2_describe_workspace_size_hw(1, H, W, S, 6, 6, ctypes.byref(full)), "ws")
+    # the size in between holds the shift-byte copy but not the dense cell
+    # sums (k_cell_sums): the axis-aligned patch is then counted per keypoint
+    mid = small.value + ((H * W + 255) & ~255)
+    assert small.value < mid < full.value
+    for nbytes in (small.value, mid, full.value):
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
         o = dict(counts=torch.zeros((1, 2 * S, 224), dtype=torch.float16, device="cuda"),
                  sqnorm=torch.zeros((1, 2 * S), dtype=torch.int32, device="cuda"),
                  kp=torch.zeros((1, 2 * S), dtype=torch.int32, device="cuda"),
@@ -112,8 +115,9 @@ def test_preshift_workspace_equals_transform_path(gold):
         _lib.check(rc, "rift2_describe")
         outs.append(o)
     torch.cuda.synchronize()
-    a, b = outs
+    a = outs[0]
     n = int(a["count"][0])
-    assert n == int(b["count"][0]) and n > 0 and int(a["skipped"][0]) == int(b["skipped"][0])
-    for k in ("counts", "sqnorm", "kp", "variant"):
-        assert torch.equal(a[k][0, :n], b[k][0, :n]), k
+    for b in outs[1:]:
+        assert n == int(b["count"][0]) and n > 0 and int(a["skipped"][0]) == int(b["skipped"][0])
+        for k in ("counts", "sqnorm", "kp", "variant"):
+            assert torch.equal(a[k][0, :n], b[k][0, :n]), k
