@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
       else cols_filters<G>(c, Sc, Geo, buf, Qb, xo, t, mir != 0, sn, qs, b);
       return;
     } else {
+    // 512-row columns (G = 16) also leave by TMA: one {4 rows x 1 column x 128
+    // tiles} box per column and filter, staged in natural row order in the
+    // group's exchange buffer
+    const CUtensorMap* qs = (G == 16 && use_tma) ? &qst : nullptr;
     for (int f = 0; f < F; ++f) {
       const int s = f / c.O, o = f % c.O;
       const float ll = c.ll_s[s], ang = c.ang_s[o];
@@ -342,7 +346,24 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
         const float gv = transfer_s(Geo[ky].x, th, ll, ang, c.two_pi_s);
         v[m] = make_float2(sv.x * gv, sv.y * gv);   // conj(spectrum * G) for the inverse
       }
+      if (qs) {
+        // the previous filter's tensor store has read buf before the FFT reuses it
+        if (t == 0) bulk_wait_read0();
+        sw();
+      }
       fft_fast<G>(v, buf, c.tw_h, t, sw);
+      if (qs) {
+        sw();
+#pragma unroll
+        for (int m = 0; m < 32; ++m) buf[t + G * m] = cconj(v[m]);
+        fence_proxy_async();
+        sw();
+        if (t == 0) {
+          tma_store_3d(qs, 0, xo, (b * F + f) * (c.Hp >> 2), buf);
+          bulk_commit();
+        }
+        continue;
+      }
       float2* Qf = Qb + (size_t)f * c.Hp * W;
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
@@ -350,6 +371,7 @@ __global__ void __launch_bounds__(ColsCfg<G>::T, ColsCfg<G>::T == 128 ? 3 : 1) k
         Qf[tq(y, xo, W)] = cconj(v[m]);
       }
     }
+    if (qs && t == 0) bulk_wait0();                // the last store has left shared memory
     }
   } else {
     // generic sizes: whole CTA per transform, 4 columns per CTA
@@ -1503,14 +1525,15 @@ static cudaError_t launch_cols(const float2* P, float2* Q, const FieldsConst& c,
     const int N = 32 * G, NG = ColsCfg<G>::T / G, CG = NG / 2, PL = padded_len(N), PLA = (PL + 15) & ~15;
     smem = ((size_t)CG * PL + (size_t)NG * PLA) * sizeof(float2) + 2 * (size_t)CG * N * sizeof(float) + 128;
     grid = dim3((c.Wh + CG - 1) / CG, c.B);
-    if constexpr (G >= 32) {
-      // columns of >= 1,024 rows leave by TMA: Q as 32-bit words (4 rows x 2
+    if constexpr (G >= 16) {
+      // columns of >= 512 rows leave by TMA: Q as 32-bit words (4 rows x 2
       // components, x, tile of all planes); a box is one column, 256 tiles
+      // (128: the whole 512-row column)
       auto enc = get_encode();
       if (kColsTma && enc && ((uintptr_t)Q & 15) == 0 && c.Hp == N) {
         cuuint64_t dims[3] = {8, (cuuint64_t)c.W, (cuuint64_t)c.B * c.S * c.O * (c.Hp / 4)};
         cuuint64_t strides[2] = {4 * sizeof(float2), (cuuint64_t)c.W * 4 * sizeof(float2)};
-        cuuint32_t box[3] = {8, 1, 256};
+        cuuint32_t box[3] = {8, 1, (cuuint32_t)(N >= 1024 ? 256 : N / 4)};
         cuuint32_t es[3] = {1, 1, 1};
         use_tma = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, Q, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
